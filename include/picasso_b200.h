@@ -1,0 +1,123 @@
+/*
+ * picasso_b200.h — C ABI of the B200 conflict-graph builder.
+ *
+ * Drop-in target: palettecolor.conflict.build(view, lists, *, edge_budget, threads,
+ * block_pairs, two_phase) -> ConflictGraph
+ *   (/root/reference/pkg/src/palettecolor/conflict.py:89-167).
+ * The reference has no FFI of its own (pure Python + numpy); these entry points are what a
+ * ctypes / cffi binding of that function binds — see INTEGRATION.md.  Plain pointers and
+ * sizes only; no torch types; no exceptions cross the ABI (every call returns a status).
+ *
+ * The two-phase contract of the reference (count -> budget check -> fill) is kept:
+ *   pcg_set_inputs   conflict.py:106-108   inputs of one build (words, active ids, lists)
+ *   pcg_count        conflict.py:110-116   count pass: degrees, |E_c|, view_edges_scanned
+ *                                          (the budget check, conflict.py:117-118, is the
+ *                                          caller's: it raises EdgeBudgetExceededError)
+ *   pcg_fill         conflict.py:119-161   fill pass + canonical CSR (members, offsets,
+ *                                          neighbors) written straight into caller buffers
+ * and, for pair-space sharding across GPUs (one process per GPU, host collectives):
+ *   pcg_copy_degrees / pcg_fill_rows       per-shard degrees out, global degrees in, shard
+ *                                          slice of the CSR out.
+ *
+ * Thread safety: one pcg_ctx per host thread; contexts share nothing.
+ */
+#ifndef PICASSO_B200_H
+#define PICASSO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCG_OK 0
+#define PCG_E_ARG 1      /* bad argument (null pointer, size out of range, bad qubit count) */
+#define PCG_E_CUDA 2     /* CUDA runtime error (see pcg_last_error) */
+#define PCG_E_OOM 3      /* device allocation failed */
+#define PCG_E_COLOR 4    /* a list color lies outside [palette_base, palette_base + palette_size) */
+#define PCG_E_STATE 5    /* call order violated (fill before count, ...) */
+
+typedef struct pcg_ctx pcg_ctx;
+
+/* Totals of one count pass (conflict.py:114-116). */
+typedef struct {
+    int64_t n_active;           /* rows of the build (view.n_active) */
+    int64_t anticommuting;      /* anticommuting pairs among the K1 tile shard */
+    int64_t pairs_in_shard;     /* unordered pairs covered by the K1 tile shard */
+    int64_t deg_sum;            /* sum of conflict degrees over the K2 row range */
+    int64_t deg_upper_sum;      /* sum over the row range of #admitted partners j > i */
+    int64_t members_in_range;   /* rows of the range with degree > 0 */
+    int32_t raw_words_mode;     /* 1 if invalid 3-bit codes forced the raw-word predicate */
+    int32_t reserved;
+} pcg_counts;
+
+int pcg_version(void);
+/* Creates a context bound to CUDA device `device` with its own stream. */
+int pcg_create(int device, pcg_ctx **out);
+int pcg_destroy(pcg_ctx *ctx);
+const char *pcg_last_error(const pcg_ctx *ctx);
+
+/*
+ * Stage the inputs of one build (host pointers, copied to the device).
+ *   words      (n_total, nwords) uint64: PauliSet.words (pauli.py:217, 240-246)
+ *   active     (n_active,) int64, sorted unique original ids (graph.py:291-303)
+ *   list_data  colors of every active row, row-major (ColorLists.array, driver.py:184-188)
+ *   list_off   (n_active+1,) int64 row offsets into list_data, or NULL when every row has
+ *              exactly list_len colors (the rectangular ColorLists.array case)
+ *   palette_base / palette_size: ColorLists.palette_base / palette_size
+ */
+int pcg_set_inputs(pcg_ctx *ctx, const uint64_t *words, int64_t n_total, int32_t nwords,
+                   int32_t num_qubits, const int64_t *active, int64_t n_active,
+                   const int64_t *list_data, const int64_t *list_off, int32_t list_len,
+                   int64_t palette_base, int64_t palette_size);
+
+/*
+ * Count pass.  The commuting-pair count (view_edges_scanned) runs over tile shard
+ * `shard` of `nshards` of the upper triangle; conflict degrees are computed for full
+ * rows [row_begin, row_end).  Single GPU: shard=0, nshards=1, rows [0, n_active).
+ * view_edges_scanned = pairs - anticommuting (summed over shards); |E_c| = deg_sum / 2
+ * (summed over row ranges).
+ */
+int pcg_count(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t row_begin,
+              int64_t row_end, pcg_counts *out);
+
+/* Degrees of rows [row_begin,row_end) from the last count: deg (full row) and deg_upper
+ * (partners j > i), int32 host buffers of (row_end-row_begin) entries; either may be NULL. */
+int pcg_copy_degrees(pcg_ctx *ctx, int32_t *deg, int32_t *deg_upper);
+
+/*
+ * Fill pass + CSR for the single-GPU case (count must cover all rows).  Host outputs,
+ * int64 like the reference: members (n_members), offsets (n_members+1),
+ * neighbors (2*edge_count).  n_members = rows with degree > 0.
+ */
+int pcg_fill(pcg_ctx *ctx, int64_t *members, int64_t *offsets, int64_t *neighbors);
+
+/*
+ * Sharded fill.  global_deg: (n_active,) int32 degrees of ALL rows (gathered from every
+ * shard, host pointer).  Writes the neighbor entries of rows [row_begin,row_end) — a
+ * contiguous slice of the global CSR neighbor array starting at entry *slice_begin —
+ * into `neighbors` (host, int64, capacity (*slice_end - *slice_begin)).
+ * Call with neighbors == NULL first to learn the slice bounds.
+ */
+int pcg_fill_rows(pcg_ctx *ctx, const int32_t *global_deg, int64_t *neighbors,
+                  int64_t *slice_begin, int64_t *slice_end);
+
+/* Device-resident timing hooks for the benchmark (no host traffic): re-run count and fill
+ * on the inputs already staged; outputs stay in HBM.  *launches receives the number of
+ * kernels this call launched. */
+int pcg_count_device(pcg_ctx *ctx, pcg_counts *out, int32_t *launches);
+int pcg_fill_device(pcg_ctx *ctx, int32_t *launches);
+/* Average device time (ms) of each kernel family in the last *_device call:
+ * [0] commute sweep (K1), [1] conflict-row count (K2c), [2] conflict-row fill (K2f),
+ * [3] compaction/offsets, [4] input prep.  Requires pcg_set_profiling(ctx, 1). */
+int pcg_set_profiling(pcg_ctx *ctx, int32_t on);
+int pcg_kernel_times(pcg_ctx *ctx, float *ms, int32_t n);
+/* Kernel configuration knobs (testing/tuning): 0 = auto.
+ *   K1 algorithm: 1 = direct LOP3/POPC tiles, 2 = four-Russians smem tables. */
+int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PICASSO_B200_H */
