@@ -1,0 +1,203 @@
+"""ctypes binding of libpicasso_b200.so (the C ABI in include/picasso_b200.h).
+
+There is no CPU path: if the library is missing or no CUDA device is visible, every entry
+point raises.  ctypes releases the GIL for the duration of each foreign call, and each host
+thread gets its own ``pcg_ctx`` (contexts share nothing), so concurrent builds from several
+threads (tuner.sweep with cell_workers > 1, tuner.py:138-141) are safe.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from .errors import DeviceError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpicasso_b200.so")
+
+PCG_OK, PCG_E_ARG, PCG_E_CUDA, PCG_E_OOM, PCG_E_COLOR, PCG_E_STATE = range(6)
+
+
+class Counts(ctypes.Structure):
+    _fields_ = [
+        ("n_active", ctypes.c_int64),
+        ("anticommuting", ctypes.c_int64),
+        ("pairs_in_shard", ctypes.c_int64),
+        ("deg_sum", ctypes.c_int64),
+        ("deg_upper_sum", ctypes.c_int64),
+        ("members_in_range", ctypes.c_int64),
+        ("raw_words_mode", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+    ]
+
+
+_lib = None
+_lib_lock = threading.Lock()
+_VP = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int32
+
+
+def library():
+    """Load the CUDA library (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build the CUDA extension first "
+                "(python -c 'import __graft_entry__; __graft_entry__.build()')")
+        lib = ctypes.CDLL(LIB_PATH)
+        lib.pcg_version.restype = ctypes.c_int
+        lib.pcg_create.argtypes = [ctypes.c_int, ctypes.POINTER(_VP)]
+        lib.pcg_destroy.argtypes = [_VP]
+        lib.pcg_last_error.argtypes = [_VP]
+        lib.pcg_last_error.restype = ctypes.c_char_p
+        lib.pcg_set_inputs.argtypes = [_VP, _VP, _I64, _I32, _I32, _VP, _I64, _VP, _VP, _I32,
+                                       _I64, _I64]
+        lib.pcg_count.argtypes = [_VP, _I32, _I32, _I64, _I64, ctypes.POINTER(Counts)]
+        lib.pcg_copy_degrees.argtypes = [_VP, _VP, _VP]
+        lib.pcg_fill.argtypes = [_VP, _VP, _VP, _VP]
+        lib.pcg_fill_rows.argtypes = [_VP, _VP, _VP, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]
+        lib.pcg_count_device.argtypes = [_VP, ctypes.POINTER(Counts), ctypes.POINTER(_I32)]
+        lib.pcg_fill_device.argtypes = [_VP, ctypes.POINTER(_I32)]
+        lib.pcg_set_profiling.argtypes = [_VP, _I32]
+        lib.pcg_kernel_times.argtypes = [_VP, _VP, _I32]
+        lib.pcg_set_option.argtypes = [_VP, ctypes.c_char_p, _I64]
+        for name in ("pcg_create", "pcg_destroy", "pcg_set_inputs", "pcg_count",
+                     "pcg_copy_degrees", "pcg_fill", "pcg_fill_rows", "pcg_count_device",
+                     "pcg_fill_device", "pcg_set_profiling", "pcg_kernel_times",
+                     "pcg_set_option"):
+            getattr(lib, name).restype = ctypes.c_int
+        _lib = lib
+        return lib
+
+
+EXPORTED = (
+    "pcg_version", "pcg_create", "pcg_destroy", "pcg_last_error", "pcg_set_inputs", "pcg_count",
+    "pcg_copy_degrees", "pcg_fill", "pcg_fill_rows", "pcg_count_device", "pcg_fill_device",
+    "pcg_set_profiling", "pcg_kernel_times", "pcg_set_option",
+)
+
+
+def _ptr(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(_VP)
+
+
+class Context:
+    """One pcg_ctx (device state of a build) bound to one CUDA device."""
+
+    def __init__(self, device: int = 0):
+        self.lib = library()
+        h = _VP()
+        rc = self.lib.pcg_create(int(device), ctypes.byref(h))
+        if rc != PCG_OK:
+            raise DeviceError(f"pcg_create(device={device}) failed with code {rc}: "
+                              "no usable CUDA device")
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.pcg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int, what: str):
+        if rc == PCG_OK:
+            return
+        msg = self.lib.pcg_last_error(self.h).decode(errors="replace")
+        if rc == PCG_E_COLOR:
+            raise ValueError(f"{what}: {msg}")
+        if rc == PCG_E_ARG:
+            raise ValueError(f"{what}: {msg}")
+        if rc == PCG_E_OOM:
+            raise MemoryError(f"{what}: {msg}")
+        raise DeviceError(f"{what} failed (code {rc}): {msg}")
+
+    def option(self, key: str, value: int):
+        self._check(self.lib.pcg_set_option(self.h, key.encode(), int(value)), "pcg_set_option")
+
+    def profiling(self, on: bool):
+        self._check(self.lib.pcg_set_profiling(self.h, 1 if on else 0), "pcg_set_profiling")
+
+    def kernel_times(self) -> list:
+        out = np.zeros(5, dtype=np.float32)
+        self._check(self.lib.pcg_kernel_times(self.h, _ptr(out), 5), "pcg_kernel_times")
+        return out.tolist()
+
+    def set_inputs(self, words: np.ndarray, num_qubits: int, active: np.ndarray,
+                   list_data: np.ndarray, list_off: np.ndarray | None, list_len: int,
+                   palette_base: int, palette_size: int):
+        self._keep = (words, active, list_data, list_off)
+        rc = self.lib.pcg_set_inputs(
+            self.h, _ptr(words), int(words.shape[0]), int(words.shape[1]), int(num_qubits),
+            _ptr(active), int(active.size), _ptr(list_data), _ptr(list_off), int(list_len),
+            int(palette_base), int(palette_size))
+        self._check(rc, "pcg_set_inputs")
+
+    def count(self, shard: int = 0, nshards: int = 1, row_begin: int = 0,
+              row_end: int | None = None, n: int | None = None) -> Counts:
+        c = Counts()
+        if row_end is None:
+            row_end = n
+        self._check(self.lib.pcg_count(self.h, shard, nshards, row_begin, row_end, ctypes.byref(c)),
+                    "pcg_count")
+        return c
+
+    def degrees(self, rows: int) -> tuple:
+        deg = np.zeros(rows, dtype=np.int32)
+        degu = np.zeros(rows, dtype=np.int32)
+        self._check(self.lib.pcg_copy_degrees(self.h, _ptr(deg), _ptr(degu)), "pcg_copy_degrees")
+        return deg, degu
+
+    def fill(self, members: np.ndarray, offsets: np.ndarray, neighbors: np.ndarray):
+        self._check(self.lib.pcg_fill(self.h, _ptr(members), _ptr(offsets), _ptr(neighbors)),
+                    "pcg_fill")
+
+    def fill_rows(self, global_deg: np.ndarray, neighbors: np.ndarray | None) -> tuple:
+        lo, hi = _I64(0), _I64(0)
+        g = np.ascontiguousarray(global_deg, dtype=np.int32)
+        self._check(self.lib.pcg_fill_rows(self.h, _ptr(g), _ptr(neighbors), ctypes.byref(lo),
+                                           ctypes.byref(hi)), "pcg_fill_rows")
+        return int(lo.value), int(hi.value)
+
+    def count_device(self) -> tuple:
+        c = Counts()
+        n = _I32(0)
+        self._check(self.lib.pcg_count_device(self.h, ctypes.byref(c), ctypes.byref(n)),
+                    "pcg_count_device")
+        return c, int(n.value)
+
+    def fill_device(self) -> int:
+        n = _I32(0)
+        self._check(self.lib.pcg_fill_device(self.h, ctypes.byref(n)), "pcg_fill_device")
+        return int(n.value)
+
+
+_tls = threading.local()
+
+
+def context(device: int | None = None) -> Context:
+    """The calling thread's context on ``device`` (default: $PICASSO_DEVICE or LOCAL_RANK or 0)."""
+    if device is None:
+        device = int(os.environ.get("PICASSO_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+    cache = getattr(_tls, "ctxs", None)
+    if cache is None:
+        cache = _tls.ctxs = {}
+    ctx = cache.get(device)
+    if ctx is None:
+        ctx = cache[device] = Context(device)
+    return ctx

@@ -1,0 +1,663 @@
+// C ABI of the B200 conflict-graph builder (include/picasso_b200.h).
+//
+// Host orchestration of one build, mirroring palettecolor.conflict.build
+// (conflict.py:89-167): stage inputs (K0), count (K1 + K2 count), let the caller check
+// the budget, then fill (compaction + K2 fill) straight into the caller's buffers.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "pcg_internal.cuh"
+
+namespace pcg {
+
+cudaError_t ensure(DevBuf &b, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (b.cap >= bytes) return cudaSuccess;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+    size_t want = bytes + bytes / 8;  // headroom for slightly larger next builds
+    cudaError_t e = cudaMalloc(&b.p, want);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        e = cudaMalloc(&b.p, bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            b.p = nullptr;
+            return e;
+        }
+        want = bytes;
+    }
+    b.cap = want;
+    return cudaSuccess;
+}
+
+void release(DevBuf &b) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+}
+
+namespace {
+
+struct DegPositive {
+    const int32_t *d;
+    int64_t n;
+    __host__ __device__ int32_t operator()(int64_t i) const { return (i < n && d[i] > 0) ? 1 : 0; }
+};
+struct DegAt {
+    const int32_t *d;
+    int64_t n;
+    __host__ __device__ int64_t operator()(int64_t i) const { return i < n ? (int64_t)d[i] : 0; }
+};
+
+__global__ void k_sum_degrees(const int32_t *__restrict__ deg, const int32_t *__restrict__ degu,
+                              int64_t r0, int64_t r1, unsigned long long *out) {
+    unsigned long long s = 0, su = 0, m = 0;
+    for (int64_t i = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r1;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int d = deg[i];
+        s += d;
+        su += degu[i];
+        m += d > 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_down_sync(0xffffffffu, s, o);
+        su += __shfl_down_sync(0xffffffffu, su, o);
+        m += __shfl_down_sync(0xffffffffu, m, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(out + 1, s);
+        atomicAdd(out + 2, su);
+        atomicAdd(out + 3, m);
+    }
+}
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+}  // namespace
+}  // namespace pcg
+
+using namespace pcg;
+
+#define PCG_TRY_CUDA(ctx, expr)                                                      \
+    do {                                                                            \
+        cudaError_t _e = (expr);                                                    \
+        if (_e != cudaSuccess) {                                                    \
+            (ctx)->err = std::string(#expr) + ": " + cudaGetErrorString(_e);        \
+            return _e == cudaErrorMemoryAllocation ? PCG_E_OOM : PCG_E_CUDA;        \
+        }                                                                           \
+    } while (0)
+
+#define PCG_ALLOC(ctx, buf, bytes)                                                   \
+    do {                                                                            \
+        cudaError_t _e = ensure((buf), (bytes));                                    \
+        if (_e != cudaSuccess) {                                                    \
+            (ctx)->err = std::string("device allocation of ") +                     \
+                         std::to_string((size_t)(bytes)) + " bytes failed: " +      \
+                         cudaGetErrorString(_e);                                    \
+            return PCG_E_OOM;                                                       \
+        }                                                                           \
+    } while (0)
+
+#define PCG_CHECK_LAUNCH(ctx) PCG_TRY_CUDA(ctx, cudaGetLastError())
+
+static int fail(pcg_ctx *ctx, int code, const std::string &msg) {
+    if (ctx) ctx->err = msg;
+    return code;
+}
+
+extern "C" {
+
+int pcg_version(void) { return 1; }
+
+int pcg_create(int device, pcg_ctx **out) {
+    if (!out) return PCG_E_ARG;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return PCG_E_CUDA;
+    }
+    pcg_ctx *ctx = new pcg_ctx();
+    ctx->device = device;
+    if (cudaSetDevice(device) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete ctx;
+        return PCG_E_CUDA;
+    }
+    cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
+    for (auto &e : ctx->ev) cudaEventCreate(&e);
+    *out = ctx;
+    return PCG_OK;
+}
+
+int pcg_destroy(pcg_ctx *ctx) {
+    if (!ctx) return PCG_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    DevBuf *bufs[] = {&ctx->words, &ctx->active, &ctx->lists64, &ctx->loff, &ctx->A, &ctx->B,
+                      &ctx->H, &ctx->lrel, &ctx->rowof, &ctx->keys2, &ctx->vals2, &ctx->bstart,
+                      &ctx->cubtmp, &ctx->deg, &ctx->degu, &ctx->compact, &ctx->rowoff,
+                      &ctx->scal, &ctx->bad, &ctx->members_o, &ctx->offsets_o, &ctx->nbr_o,
+                      &ctx->gdeg, &ctx->items};
+    for (DevBuf *b : bufs) release(*b);
+    for (auto &e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return PCG_OK;
+}
+
+const char *pcg_last_error(const pcg_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
+    if (!ctx || !key) return PCG_E_ARG;
+    if (!strcmp(key, "k1_algo")) ctx->k1_algo = (int)value;
+    else if (!strcmp(key, "window")) ctx->window = (int)value;
+    else if (!strcmp(key, "fr_ichunk")) ctx->fr_ichunk = (int)value;
+    else return fail(ctx, PCG_E_ARG, std::string("unknown option ") + key);
+    return PCG_OK;
+}
+
+int pcg_set_profiling(pcg_ctx *ctx, int32_t on) {
+    if (!ctx) return PCG_E_ARG;
+    ctx->prof = on != 0;
+    return PCG_OK;
+}
+
+int pcg_kernel_times(pcg_ctx *ctx, float *ms, int32_t n) {
+    if (!ctx || !ms) return PCG_E_ARG;
+    for (int k = 0; k < n && k < 5; ++k) ms[k] = ctx->ktimes[k];
+    return PCG_OK;
+}
+
+}  // extern "C"
+
+// --------------------------------------------------------------------------------------
+// input staging (K0)
+// --------------------------------------------------------------------------------------
+static int encode_vectors(pcg_ctx *ctx, bool raw) {
+    cudaStream_t s = ctx->stream;
+    ctx->raw = raw;
+    ctx->kw = raw ? 2 * ctx->nwords : 2 * ((ctx->q + 31) / 32);
+    PCG_ALLOC(ctx, ctx->A, (size_t)ctx->npad * ctx->kw * 4);
+    PCG_ALLOC(ctx, ctx->B, (size_t)ctx->npad * ctx->kw * 4);
+    PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->bad.p, 0, 8, s));
+    launch_encode(ctx->words.as<uint64_t>(), ctx->nwords, ctx->active.as<int64_t>(), ctx->n,
+                  ctx->npad, ctx->q, raw ? 1 : 0, ctx->A.as<uint32_t>(), ctx->B.as<uint32_t>(),
+                  ctx->kw, ctx->bad.as<int32_t>(), s);
+    PCG_CHECK_LAUNCH(ctx);
+    return PCG_OK;
+}
+
+extern "C" int pcg_set_inputs(pcg_ctx *ctx, const uint64_t *words, int64_t n_total,
+                              int32_t nwords, int32_t num_qubits, const int64_t *active,
+                              int64_t n_active, const int64_t *list_data,
+                              const int64_t *list_off, int32_t list_len, int64_t palette_base,
+                              int64_t palette_size) {
+    if (!ctx) return PCG_E_ARG;
+    ctx->err.clear();
+    ctx->staged = false;
+    ctx->counted = false;
+    if (n_active < 0 || n_total < 0 || n_active > n_total || num_qubits < 1 || nwords < 1 ||
+        (int64_t)nwords * 64 < 3LL * num_qubits || palette_size < 0 || n_active > (1LL << 30))
+        return fail(ctx, PCG_E_ARG, "bad build dimensions");
+    if (n_active > 0 && (!words || !active || !list_data))
+        return fail(ctx, PCG_E_ARG, "null input pointer");
+    if (!list_off && list_len < 1 && n_active > 0)
+        return fail(ctx, PCG_E_ARG, "rectangular lists need list_len >= 1");
+    PCG_TRY_CUDA(ctx, cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+
+    ctx->n_total = n_total;
+    ctx->n = n_active;
+    ctx->nwords = nwords;
+    ctx->q = num_qubits;
+    ctx->base = palette_base;
+    // the reference's mask has ceil(P/64) (at least 1) words: every relative color below
+    // that many bits is a legal list entry (driver.py:152-172)
+    ctx->P = std::max<int64_t>(1, (palette_size + 63) / 64) * 64;
+    palette_size = ctx->P;
+    ctx->ragged = list_off != nullptr;
+    ctx->npad = round_up(n_active, K1_FR_JB);
+    int64_t entries = 0;
+    int32_t lmax = list_len;
+    if (ctx->ragged) {
+        entries = list_off[n_active] - list_off[0];
+        lmax = 0;
+        for (int64_t i = 0; i < n_active; ++i)
+            lmax = std::max<int32_t>(lmax, (int32_t)(list_off[i + 1] - list_off[i]));
+        if (list_off[0] != 0) return fail(ctx, PCG_E_ARG, "list_off[0] must be 0");
+    } else {
+        entries = n_active * (int64_t)list_len;
+    }
+    ctx->L = list_len;
+    ctx->lmax = std::max<int32_t>(lmax, 1);
+    ctx->entries = entries;
+    if (entries >= (1LL << 31)) return fail(ctx, PCG_E_ARG, "too many list entries");
+
+    PCG_ALLOC(ctx, ctx->bad, 16);
+    PCG_ALLOC(ctx, ctx->scal, 64);
+    if (n_active == 0) {
+        ctx->kw = 2;
+        ctx->staged = true;
+        return PCG_OK;
+    }
+    PCG_ALLOC(ctx, ctx->words, (size_t)n_total * nwords * 8);
+    PCG_ALLOC(ctx, ctx->active, (size_t)n_active * 8);
+    PCG_ALLOC(ctx, ctx->lists64, (size_t)entries * 8);
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->words.p, words, (size_t)n_total * nwords * 8,
+                                      cudaMemcpyHostToDevice, s));
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->active.p, active, (size_t)n_active * 8,
+                                      cudaMemcpyHostToDevice, s));
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->lists64.p, list_data, (size_t)entries * 8,
+                                      cudaMemcpyHostToDevice, s));
+    if (ctx->ragged) {
+        PCG_ALLOC(ctx, ctx->loff, (size_t)(n_active + 1) * 8);
+        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->loff.p, list_off, (size_t)(n_active + 1) * 8,
+                                          cudaMemcpyHostToDevice, s));
+    }
+    if (ctx->prof) cudaEventRecord(ctx->ev[10], s);
+
+    // Pauli words -> bit-plane vectors (raw 3-bit words if any code is invalid)
+    int rc = encode_vectors(ctx, false);
+    if (rc) return rc;
+    // color lists -> relative int32 + row ids
+    PCG_ALLOC(ctx, ctx->lrel, (size_t)entries * 4);
+    PCG_ALLOC(ctx, ctx->rowof, (size_t)entries * 4);
+    launch_lists(ctx->lists64.as<int64_t>(), ctx->ragged ? ctx->loff.as<int64_t>() : nullptr,
+                 n_active, list_len, entries, palette_base, palette_size, ctx->lrel.as<int32_t>(),
+                 ctx->rowof.as<int32_t>(), ctx->bad.as<int32_t>() + 1, s);
+    PCG_CHECK_LAUNCH(ctx);
+    int32_t bad[2] = {0, 0};
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(bad, ctx->bad.p, 8, cudaMemcpyDeviceToHost, s));
+    PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+    if (bad[1]) return fail(ctx, PCG_E_COLOR, "a list color lies outside the palette");
+    if (bad[0]) {
+        rc = encode_vectors(ctx, true);
+        if (rc) return rc;
+    }
+
+    // color buckets: stable radix sort of (color, row) in row-major order -> ascending rows
+    int end_bit = 1;
+    while ((1LL << end_bit) < palette_size) ++end_bit;
+    PCG_ALLOC(ctx, ctx->keys2, (size_t)entries * 4);
+    PCG_ALLOC(ctx, ctx->vals2, (size_t)entries * 4);
+    size_t tmp = 0;
+    PCG_TRY_CUDA(ctx, cub::DeviceRadixSort::SortPairs(
+                          nullptr, tmp, ctx->lrel.as<int32_t>(), ctx->keys2.as<int32_t>(),
+                          ctx->rowof.as<int32_t>(), ctx->vals2.as<int32_t>(), (int)entries, 0,
+                          end_bit, s));
+    PCG_ALLOC(ctx, ctx->cubtmp, tmp);
+    PCG_TRY_CUDA(ctx, cub::DeviceRadixSort::SortPairs(
+                          ctx->cubtmp.p, tmp, ctx->lrel.as<int32_t>(), ctx->keys2.as<int32_t>(),
+                          ctx->rowof.as<int32_t>(), ctx->vals2.as<int32_t>(), (int)entries, 0,
+                          end_bit, s));
+    PCG_ALLOC(ctx, ctx->bstart, (size_t)(palette_size + 1) * 4);
+    launch_bucket_bounds(ctx->keys2.as<int32_t>(), entries, palette_size,
+                         ctx->bstart.as<int32_t>(), s);
+    PCG_CHECK_LAUNCH(ctx);
+
+    // four-Russians row offsets
+    if (fr_supported(ctx->kw)) {
+        PCG_ALLOC(ctx, ctx->H, (size_t)ctx->npad * ctx->kw * 4 * 4);
+        launch_fr_prep(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
+        PCG_CHECK_LAUNCH(ctx);
+    }
+    PCG_ALLOC(ctx, ctx->deg, (size_t)n_active * 4);
+    PCG_ALLOC(ctx, ctx->degu, (size_t)n_active * 4);
+    if (ctx->prof) {
+        cudaEventRecord(ctx->ev[11], s);
+        cudaEventSynchronize(ctx->ev[11]);
+        cudaEventElapsedTime(&ctx->ktimes[4], ctx->ev[10], ctx->ev[11]);
+    }
+    ctx->staged = true;
+    return PCG_OK;
+}
+
+// --------------------------------------------------------------------------------------
+// count pass
+// --------------------------------------------------------------------------------------
+static int k1_algo(const pcg_ctx *ctx) {
+    if (ctx->k1_algo == 1) return 1;
+    if (ctx->k1_algo == 2 && fr_supported(ctx->kw)) return 2;
+    return fr_supported(ctx->kw) ? 2 : 1;
+}
+
+static int64_t fr_ichunk(const pcg_ctx *ctx) { return ctx->fr_ichunk > 0 ? ctx->fr_ichunk : 2048; }
+
+// pairs (i<j, both < n) inside four-Russians item (jb, rows [i0,i1))
+static int64_t fr_item_pairs(int64_t n, int64_t jb, int64_t i0, int64_t i1) {
+    const int64_t jlo = jb * K1_FR_JB, jhi = std::min(n, jlo + (int64_t)K1_FR_JB);
+    int64_t p = 0;
+    const int64_t full_hi = std::min(i1, jlo);
+    if (full_hi > i0) p += (full_hi - i0) * (jhi - jlo);
+    const int64_t a = std::max(i0, jlo), b = std::min(i1, jhi);
+    for (int64_t i = a; i < b; ++i) p += jhi - 1 - i;
+    return p;
+}
+
+// pairs inside direct tiles [t0,t1) (row-major upper triangle of T x T tiles)
+static int64_t direct_pairs(int64_t n, int64_t T, int64_t t0, int64_t t1) {
+    int64_t p = 0, t = 0;
+    for (int64_t bi = 0; bi < T && t < t1; ++bi) {
+        const int64_t row_tiles = T - bi;
+        const int64_t a = std::max(t0, t), b = std::min(t1, t + row_tiles);
+        const int64_t rlo = bi * K1_TILE, rhi = std::min(n, rlo + (int64_t)K1_TILE);
+        const int64_t rows = std::max<int64_t>(0, rhi - rlo);
+        for (int64_t tt = a; tt < b; ++tt) {
+            const int64_t bj = bi + (tt - t);
+            const int64_t clo = bj * K1_TILE, chi = std::min(n, clo + (int64_t)K1_TILE);
+            const int64_t cols = std::max<int64_t>(0, chi - clo);
+            p += bi == bj ? rows * (rows - 1) / 2 : rows * cols;
+        }
+        t += row_tiles;
+    }
+    return p;
+}
+
+static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, int *launches) {
+    cudaStream_t s = ctx->stream;
+    unsigned long long *anti = ctx->scal.as<unsigned long long>();
+    const int64_t n = ctx->n;
+    if (k1_algo(ctx) == 2) {
+        const int64_t njb = ctx->npad / K1_FR_JB, ic = fr_ichunk(ctx);
+        std::vector<int64_t> start(njb + 1, 0);
+        for (int64_t jb = 0; jb < njb; ++jb) {
+            const int64_t jlast = std::min(n, (jb + 1) * (int64_t)K1_FR_JB);
+            start[jb + 1] = start[jb] + (jlast + ic - 1) / ic;
+        }
+        const int64_t items = start[njb];
+        const int64_t i0 = items * shard / nshards, i1 = items * (shard + 1) / nshards;
+        if (nshards == 1) {
+            *pairs = n * (n - 1) / 2;
+        } else {
+            int64_t p = 0, jb = 0;
+            for (int64_t it = i0; it < i1; ++it) {
+                while (start[jb + 1] <= it) ++jb;
+                const int64_t jlast = std::min(n, (jb + 1) * (int64_t)K1_FR_JB);
+                const int64_t r0 = (it - start[jb]) * ic, r1 = std::min(r0 + ic, jlast);
+                p += fr_item_pairs(n, jb, r0, r1);
+            }
+            *pairs = p;
+        }
+        // pageable H2D: the copy is complete (staged) before cudaMemcpyAsync returns
+        PCG_ALLOC(ctx, ctx->items, (size_t)(njb + 1) * 8);
+        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->items.p, start.data(), (size_t)(njb + 1) * 8,
+                                          cudaMemcpyHostToDevice, s));
+        *launches += launch_commute_fr_items(ctx->B.as<uint32_t>(), ctx->H.as<uint32_t>(),
+                                             ctx->kw, n, ctx->items.as<int64_t>(), njb,
+                                             (int32_t)ic, i0, i1, anti, ctx->sms, s);
+    } else {
+        const int64_t T = ctx->npad / K1_TILE, NT = tri_tiles(T);
+        const int64_t t0 = NT * shard / nshards, t1 = NT * (shard + 1) / nshards;
+        *pairs = nshards == 1 ? n * (n - 1) / 2 : direct_pairs(n, T, t0, t1);
+        *launches += launch_commute_direct(ctx->A.as<uint32_t>(), ctx->B.as<uint32_t>(), ctx->kw,
+                                           ctx->npad, t0, t1, anti, ctx->sms, s);
+    }
+    PCG_CHECK_LAUNCH(ctx);
+    return PCG_OK;
+}
+
+static int32_t pick_window(const pcg_ctx *ctx) {
+    if (ctx->window > 0) return (int32_t)round_up(ctx->window, 4096);
+    const int64_t w = round_up(std::max<int64_t>(ctx->n, 1), 4096);
+    return (int32_t)std::min<int64_t>(w, 32768);
+}
+
+static RowArgs row_args(const pcg_ctx *ctx, int64_t r0, int64_t r1) {
+    RowArgs a{};
+    a.n = (int32_t)ctx->n;
+    a.row_begin = r0;
+    a.row_end = r1;
+    a.A = ctx->A.as<uint32_t>();
+    a.B = ctx->B.as<uint32_t>();
+    a.kw = ctx->kw;
+    a.lrel = ctx->lrel.as<int32_t>();
+    a.loff = ctx->ragged ? ctx->loff.as<int64_t>() : nullptr;
+    a.L = ctx->L;
+    a.bstart = ctx->bstart.as<int32_t>();
+    a.bmem = ctx->vals2.as<int32_t>();
+    a.deg = ctx->deg.as<int32_t>();
+    a.degu = ctx->degu.as<int32_t>();
+    a.window = pick_window(ctx);
+    a.slot_cap = ctx->lmax;
+    return a;
+}
+
+static int count_impl(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t r0, int64_t r1,
+                      pcg_counts *out, int *launches) {
+    if (!ctx->staged) return fail(ctx, PCG_E_STATE, "pcg_count before pcg_set_inputs");
+    if (nshards < 1 || shard < 0 || shard >= nshards || r0 < 0 || r1 < r0 || r1 > ctx->n)
+        return fail(ctx, PCG_E_ARG, "bad shard or row range");
+    PCG_TRY_CUDA(ctx, cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    pcg_counts c{};
+    c.n_active = ctx->n;
+    c.raw_words_mode = ctx->raw ? 1 : 0;
+    ctx->counted = false;
+    if (ctx->n < 2) {  // no pairs: every degree is zero
+        if (ctx->n == 1) {
+            PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->deg.p, 0, 4, s));
+            PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->degu.p, 0, 4, s));
+            PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+        }
+        ctx->cnt_row_begin = r0;
+        ctx->cnt_row_end = r1;
+        ctx->last = c;
+        ctx->counted = true;
+        if (out) *out = c;
+        return PCG_OK;
+    }
+    PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->scal.p, 0, 32, s));
+    if (ctx->prof) cudaEventRecord(ctx->ev[0], s);
+    int64_t pairs = 0;
+    int rc = run_k1(ctx, shard, nshards, &pairs, launches);
+    if (rc) return rc;
+    if (ctx->prof) cudaEventRecord(ctx->ev[1], s);
+    const RowArgs a = row_args(ctx, r0, r1);
+    *launches += launch_rows(a, false, false, ctx->sms, s);
+    PCG_CHECK_LAUNCH(ctx);
+    if (ctx->prof) cudaEventRecord(ctx->ev[2], s);
+    if (r1 > r0) {
+        k_sum_degrees<<<std::min<int64_t>((r1 - r0 + 255) / 256, 4 * ctx->sms), 256, 0, s>>>(
+            ctx->deg.as<int32_t>(), ctx->degu.as<int32_t>(), r0, r1,
+            ctx->scal.as<unsigned long long>());
+        *launches += 1;
+        PCG_CHECK_LAUNCH(ctx);
+    }
+    unsigned long long h[4];
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(h, ctx->scal.p, 32, cudaMemcpyDeviceToHost, s));
+    PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+    if (ctx->prof) {
+        cudaEventElapsedTime(&ctx->ktimes[0], ctx->ev[0], ctx->ev[1]);
+        cudaEventElapsedTime(&ctx->ktimes[1], ctx->ev[1], ctx->ev[2]);
+    }
+    c.anticommuting = (int64_t)h[0];
+    c.pairs_in_shard = pairs;
+    c.deg_sum = (int64_t)h[1];
+    c.deg_upper_sum = (int64_t)h[2];
+    c.members_in_range = (int64_t)h[3];
+    ctx->cnt_row_begin = r0;
+    ctx->cnt_row_end = r1;
+    ctx->last = c;
+    ctx->counted = true;
+    if (out) *out = c;
+    return PCG_OK;
+}
+
+extern "C" int pcg_count(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t row_begin,
+                         int64_t row_end, pcg_counts *out) {
+    if (!ctx) return PCG_E_ARG;
+    int launches = 0;
+    return count_impl(ctx, shard, nshards, row_begin, row_end, out, &launches);
+}
+
+extern "C" int pcg_copy_degrees(pcg_ctx *ctx, int32_t *deg, int32_t *deg_upper) {
+    if (!ctx) return PCG_E_ARG;
+    if (!ctx->counted) return fail(ctx, PCG_E_STATE, "pcg_copy_degrees before pcg_count");
+    PCG_TRY_CUDA(ctx, cudaSetDevice(ctx->device));
+    const int64_t r0 = ctx->cnt_row_begin, r1 = ctx->cnt_row_end;
+    if (r1 == r0) return PCG_OK;
+    cudaStream_t s = ctx->stream;
+    if (deg)
+        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(deg, ctx->deg.as<int32_t>() + r0, (r1 - r0) * 4,
+                                          cudaMemcpyDeviceToHost, s));
+    if (deg_upper)
+        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(deg_upper, ctx->degu.as<int32_t>() + r0, (r1 - r0) * 4,
+                                          cudaMemcpyDeviceToHost, s));
+    PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+    return PCG_OK;
+}
+
+// --------------------------------------------------------------------------------------
+// fill pass
+// --------------------------------------------------------------------------------------
+// compact ids + row offsets from a full degree array (device pointer `deg`, n entries).
+static int prefix_structures(pcg_ctx *ctx, const int32_t *deg, int64_t *n_members) {
+    cudaStream_t s = ctx->stream;
+    const int64_t n = ctx->n;
+    PCG_ALLOC(ctx, ctx->compact, (size_t)(n + 1) * 4);
+    PCG_ALLOC(ctx, ctx->rowoff, (size_t)(n + 1) * 8);
+    cub::CountingInputIterator<int64_t> idx(0);
+    cub::TransformInputIterator<int32_t, DegPositive, cub::CountingInputIterator<int64_t>> pos(
+        idx, DegPositive{deg, n});
+    cub::TransformInputIterator<int64_t, DegAt, cub::CountingInputIterator<int64_t>> dv(
+        idx, DegAt{deg, n});
+    size_t t1 = 0, t2 = 0;
+    PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, t1, pos, ctx->compact.as<int32_t>(),
+                                                    n + 1, s));
+    PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, t2, dv, ctx->rowoff.as<int64_t>(),
+                                                    n + 1, s));
+    PCG_ALLOC(ctx, ctx->cubtmp, std::max(t1, t2));
+    PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->cubtmp.p, t1, pos,
+                                                    ctx->compact.as<int32_t>(), n + 1, s));
+    PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->cubtmp.p, t2, dv,
+                                                    ctx->rowoff.as<int64_t>(), n + 1, s));
+    int32_t nm = 0;
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&nm, ctx->compact.as<int32_t>() + n, 4,
+                                      cudaMemcpyDeviceToHost, s));
+    PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+    *n_members = nm;
+    return PCG_OK;
+}
+
+static int fill_impl(pcg_ctx *ctx, bool to_host, int64_t *members, int64_t *offsets,
+                     int64_t *neighbors, int *launches) {
+    if (!ctx->counted || ctx->cnt_row_begin != 0 || ctx->cnt_row_end != ctx->n)
+        return fail(ctx, PCG_E_STATE, "pcg_fill needs a count over all rows first");
+    PCG_TRY_CUDA(ctx, cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const int64_t n = ctx->n;
+    const int64_t nm = ctx->last.members_in_range, nnz = ctx->last.deg_sum;
+    if (to_host && n < 2) {
+        if (offsets) offsets[0] = 0;
+        return PCG_OK;
+    }
+    if (n < 2) return PCG_OK;
+    if (ctx->prof) cudaEventRecord(ctx->ev[3], s);
+    int64_t nm2 = 0;
+    int rc = prefix_structures(ctx, ctx->deg.as<int32_t>(), &nm2);
+    if (rc) return rc;
+    if (nm2 != nm) return fail(ctx, PCG_E_STATE, "member count mismatch");
+    PCG_ALLOC(ctx, ctx->members_o, (size_t)std::max<int64_t>(nm, 1) * 8);
+    PCG_ALLOC(ctx, ctx->offsets_o, (size_t)(nm + 1) * 8);
+    PCG_ALLOC(ctx, ctx->nbr_o, (size_t)std::max<int64_t>(nnz, 1) * 8);
+    *launches += launch_compact(ctx->deg.as<int32_t>(), n,
+                                nm == n ? nullptr : ctx->compact.as<int32_t>(),
+                                ctx->rowoff.as<int64_t>(), ctx->active.as<int64_t>(),
+                                ctx->members_o.as<int64_t>(), ctx->offsets_o.as<int64_t>(), s);
+    PCG_CHECK_LAUNCH(ctx);
+    if (ctx->prof) cudaEventRecord(ctx->ev[4], s);
+    RowArgs a = row_args(ctx, 0, n);
+    a.rowoff = ctx->rowoff.as<int64_t>();
+    a.compact = nm == n ? nullptr : ctx->compact.as<int32_t>();
+    a.out = ctx->nbr_o.p;
+    a.out_base = 0;
+    if (nnz > 0) *launches += launch_rows(a, true, true, ctx->sms, s);
+    PCG_CHECK_LAUNCH(ctx);
+    if (ctx->prof) cudaEventRecord(ctx->ev[5], s);
+    if (to_host) {
+        if (nm > 0 && members)
+            PCG_TRY_CUDA(ctx, cudaMemcpyAsync(members, ctx->members_o.p, nm * 8,
+                                              cudaMemcpyDeviceToHost, s));
+        if (offsets)
+            PCG_TRY_CUDA(ctx, cudaMemcpyAsync(offsets, ctx->offsets_o.p, (nm + 1) * 8,
+                                              cudaMemcpyDeviceToHost, s));
+        if (nnz > 0 && neighbors)
+            PCG_TRY_CUDA(ctx, cudaMemcpyAsync(neighbors, ctx->nbr_o.p, nnz * 8,
+                                              cudaMemcpyDeviceToHost, s));
+    }
+    PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+    if (ctx->prof) {
+        cudaEventElapsedTime(&ctx->ktimes[3], ctx->ev[3], ctx->ev[4]);
+        cudaEventElapsedTime(&ctx->ktimes[2], ctx->ev[4], ctx->ev[5]);
+    }
+    return PCG_OK;
+}
+
+extern "C" int pcg_fill(pcg_ctx *ctx, int64_t *members, int64_t *offsets, int64_t *neighbors) {
+    if (!ctx) return PCG_E_ARG;
+    int launches = 0;
+    return fill_impl(ctx, true, members, offsets, neighbors, &launches);
+}
+
+extern "C" int pcg_count_device(pcg_ctx *ctx, pcg_counts *out, int32_t *launches) {
+    if (!ctx) return PCG_E_ARG;
+    int l = 0;
+    int rc = count_impl(ctx, 0, 1, 0, ctx->n, out, &l);
+    if (launches) *launches = l;
+    return rc;
+}
+
+extern "C" int pcg_fill_device(pcg_ctx *ctx, int32_t *launches) {
+    if (!ctx) return PCG_E_ARG;
+    int l = 0;
+    int rc = fill_impl(ctx, false, nullptr, nullptr, nullptr, &l);
+    if (launches) *launches = l;
+    return rc;
+}
+
+extern "C" int pcg_fill_rows(pcg_ctx *ctx, const int32_t *global_deg, int64_t *neighbors,
+                             int64_t *slice_begin, int64_t *slice_end) {
+    if (!ctx || !global_deg || !slice_begin || !slice_end) return PCG_E_ARG;
+    if (!ctx->counted) return fail(ctx, PCG_E_STATE, "pcg_fill_rows before pcg_count");
+    PCG_TRY_CUDA(ctx, cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const int64_t n = ctx->n, r0 = ctx->cnt_row_begin, r1 = ctx->cnt_row_end;
+    if (n < 2) {
+        *slice_begin = *slice_end = 0;
+        return PCG_OK;
+    }
+    PCG_ALLOC(ctx, ctx->gdeg, (size_t)n * 4);
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->gdeg.p, global_deg, n * 4, cudaMemcpyHostToDevice, s));
+    int64_t nm = 0;
+    int rc = prefix_structures(ctx, ctx->gdeg.as<int32_t>(), &nm);
+    if (rc) return rc;
+    int64_t lohi[2];
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&lohi[0], ctx->rowoff.as<int64_t>() + r0, 8,
+                                      cudaMemcpyDeviceToHost, s));
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&lohi[1], ctx->rowoff.as<int64_t>() + r1, 8,
+                                      cudaMemcpyDeviceToHost, s));
+    PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+    *slice_begin = lohi[0];
+    *slice_end = lohi[1];
+    if (!neighbors) return PCG_OK;
+    const int64_t cnt = lohi[1] - lohi[0];
+    if (cnt == 0) return PCG_OK;
+    PCG_ALLOC(ctx, ctx->nbr_o, (size_t)cnt * 8);
+    RowArgs a = row_args(ctx, r0, r1);
+    a.rowoff = ctx->rowoff.as<int64_t>();
+    a.compact = nm == n ? nullptr : ctx->compact.as<int32_t>();
+    a.out = ctx->nbr_o.p;
+    a.out_base = lohi[0];
+    launch_rows(a, true, true, ctx->sms, s);
+    PCG_CHECK_LAUNCH(ctx);
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(neighbors, ctx->nbr_o.p, cnt * 8, cudaMemcpyDeviceToHost, s));
+    PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+    return PCG_OK;
+}

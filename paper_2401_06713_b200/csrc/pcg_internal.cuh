@@ -1,0 +1,115 @@
+// Internal declarations of the B200 conflict-graph builder (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/picasso_b200.h"
+
+namespace pcg {
+
+// ---------------------------------------------------------------------------
+// Device memory: grow-only buffers owned by one context.
+// ---------------------------------------------------------------------------
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    template <typename T>
+    T *as() const { return static_cast<T *>(p); }
+};
+
+cudaError_t ensure(DevBuf &b, size_t bytes);
+void release(DevBuf &b);
+
+// ---------------------------------------------------------------------------
+// Geometry of the commuting-pair sweep (K1).
+// ---------------------------------------------------------------------------
+constexpr int K1_TILE = 128;  // rows == cols of one upper-triangle tile (direct kernel)
+constexpr int K1_FR_JB = 1024;  // j-block of the four-Russians kernel (32 lanes x 32 bits)
+
+// ---------------------------------------------------------------------------
+// Arguments of the conflict-row kernels (K2).
+// ---------------------------------------------------------------------------
+struct RowArgs {
+    int32_t n;              // active rows of the build
+    int64_t row_begin, row_end;
+    const uint32_t *B;      // (npad, kw) partner vectors
+    const uint32_t *A;      // (npad, kw) row vectors
+    int32_t kw;
+    const int32_t *lrel;    // colors relative to palette_base, CSR by row
+    const int64_t *loff;    // (n+1) row offsets into lrel, or null (rectangular, L each)
+    int32_t L;
+    const int32_t *bstart;  // (P+1) color bucket starts
+    const int32_t *bmem;    // bucket members (ascending local ids per bucket)
+    int32_t *deg;           // count pass: full conflict degree per row
+    int32_t *degu;          // count pass: partners j > i per row
+    const int64_t *rowoff;  // fill pass: (n+1) exclusive prefix of deg
+    const int32_t *compact; // fill pass: compact id per local row (null = identity)
+    void *out;              // fill pass: neighbor slice (int64 or int32)
+    int64_t out_base;       // global entry index of out[0]
+    int32_t window;         // bitmap window (bits), multiple of 4096
+    int32_t slot_cap;       // color slots reserved per warp (>= max list length)
+};
+
+// Launchers (each returns the number of kernels it launched).
+int launch_encode(const uint64_t *words, int32_t nwords, const int64_t *active, int64_t n,
+                  int64_t npad, int32_t q, int raw, uint32_t *A, uint32_t *B, int32_t kw,
+                  int32_t *bad, cudaStream_t s);
+int launch_lists(const int64_t *lists, const int64_t *loff, int64_t n, int32_t L,
+                 int64_t entries, int64_t base, int64_t P, int32_t *lrel, int32_t *row_of,
+                 int32_t *bad, cudaStream_t s);
+int launch_bucket_bounds(const int32_t *sorted_colors, int64_t entries, int64_t P,
+                         int32_t *bstart, cudaStream_t s);
+int launch_commute_direct(const uint32_t *A, const uint32_t *B, int32_t kw, int64_t npad,
+                          int64_t tile0, int64_t tile1, unsigned long long *anti, int sms,
+                          cudaStream_t s);
+bool fr_supported(int32_t kw);
+int launch_commute_fr_items(const uint32_t *B, const uint32_t *H, int32_t kw, int64_t n,
+                            const int64_t *item_start, int64_t njb, int32_t ichunk,
+                            int64_t item0, int64_t item1, unsigned long long *anti, int sms,
+                            cudaStream_t s);
+int launch_fr_prep(const uint32_t *A, int32_t kw, int64_t npad, uint32_t *H, cudaStream_t s);
+int launch_rows(const RowArgs &a, bool fill, bool out64, int sms, cudaStream_t s);
+int launch_compact(const int32_t *deg, int64_t n, const int32_t *compact, const int64_t *rowoff,
+                   const int64_t *active, int64_t *members_out, int64_t *offsets_out,
+                   cudaStream_t s);
+
+// Tile arithmetic shared by host and kernels.
+__host__ __device__ inline int64_t tri_tiles(int64_t T) { return T * (T + 1) / 2; }
+
+}  // namespace pcg
+
+struct pcg_ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    std::string err;
+
+    // staged inputs
+    int64_t n_total = 0, n = 0, npad = 0;
+    int32_t nwords = 0, q = 0, L = 0, kw = 0, lmax = 0;
+    int64_t base = 0, P = 0, entries = 0;
+    bool ragged = false, raw = false, staged = false;
+
+    // options
+    int k1_algo = 0;    // 0 auto, 1 direct, 2 four-Russians
+    int window = 0;     // K2 window bits (0 auto)
+    int fr_ichunk = 0;  // four-Russians i-chunk (0 auto)
+
+    // state of the last count
+    bool counted = false;
+    int64_t cnt_row_begin = 0, cnt_row_end = 0;
+    pcg_counts last{};
+
+    // profiling
+    bool prof = false;
+    cudaEvent_t ev[12] = {};
+    float ktimes[5] = {0, 0, 0, 0, 0};
+
+    // device buffers
+    pcg::DevBuf words, active, lists64, loff, A, B, H, lrel, rowof, keys2, vals2, bstart,
+        cubtmp, deg, degu, compact, rowoff, scal, bad, members_o, offsets_o, nbr_o, gdeg, items;
+};

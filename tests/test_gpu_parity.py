@@ -1,0 +1,191 @@
+"""Parity of the CUDA builder with the reference (golden vectors) and the oracle.
+
+Every test here calls the product path (paper_2401_06713_b200.build -> C ABI -> sm_100a
+kernels).  Bit-exact equality is required everywhere: this is integer/index work.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2401_06713_b200 as b200
+from paper_2401_06713_b200 import _native
+from paper_2401_06713_b200.conflict import last_stats, one_phase_projection
+from paper_2401_06713_b200.errors import EdgeBudgetExceededError
+from conftest import oracle_builder, pauli_view, random_lists, sha
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(params=[1, 2], ids=["k1-direct", "k1-fourrussians"])
+def k1_algo(request):
+    ctx = _native.context()
+    ctx.option("k1_algo", request.param)
+    yield request.param
+    ctx.option("k1_algo", 0)
+
+
+def test_every_golden_build(golden_cases, k1_algo):
+    for case in golden_cases:
+        case.check(b200.build(case.view, case.lists))
+
+
+@pytest.mark.parametrize("n", [5000, 10000, 20000])
+def test_hashed_q32_builds(golden_ref, n):
+    g = golden_ref["builds_hashed"][f"q32_n{n}"]
+    v = pauli_view(n, 32, 0)
+    lists = random_lists(v, seed=0)
+    assert sha(lists.array) == g["lists_sha"]
+    gc = b200.build(v, lists)
+    assert gc.edge_count == g["edge_count"]
+    assert gc.view_edges_scanned == g["view_edges_scanned"]
+    assert (sha(gc.members), sha(gc.graph.offsets), sha(gc.graph.neighbors)) == (
+        g["members_sha"], g["offsets_sha"], g["neighbors_sha"])
+
+
+@pytest.mark.parametrize("window", [4096, 8192, 32768])
+def test_window_geometry_does_not_change_rows(golden_ref, window):
+    g = golden_ref["builds_hashed"]["q32_n10000"]
+    ctx = _native.context()
+    ctx.option("window", window)
+    try:
+        v = pauli_view(10000, 32, 0)
+        gc = b200.build(v, random_lists(v, seed=0))
+    finally:
+        ctx.option("window", 0)
+    assert sha(gc.graph.neighbors) == g["neighbors_sha"]
+
+
+@pytest.mark.parametrize("name", ["c1", "tout_k0", "tout_k1", "tout_k2", "tout_k3", "tout_k4",
+                                  "cli_fixture", "static_natural", "static_ldf", "static_sdl",
+                                  "static_random", "aggressive"])
+def test_whole_run_identical_coloring(golden_ref, name):
+    r = golden_ref["runs"][name]
+    v = pauli_view(r["n"], r["q"], r["gen_seed"])
+    res = b200.run(v, b200.PaletteParams(r["palette_pct"], r["alpha"], seed=r["seed"]),
+                   strategy=r["strategy"])
+    assert sha(res.color) == r["color_sha"]
+    assert res.total_colors == r["colors"]
+    assert len(res.iterations) == r["iterations"]
+    assert res.oracle_edges == r["oracle_edges"]
+    assert res.peak_conflict_edges == r["peak_conflict_edges"]
+
+
+def test_per_iteration_csr_hashes_of_c1(golden_ref):
+    """Every residue build of the c1 run (induced views, later palettes) hashes like the reference."""
+    want = golden_ref["runs"]["c1"]["builds"]
+    got = []
+
+    def tracing(view, lists, **kw):
+        gc = b200.build(view, lists, **kw)
+        got.append(dict(n_active=view.n_active, active_sha=sha(view.active), lists_sha=sha(lists.array),
+                        members_sha=sha(gc.members), offsets_sha=sha(gc.graph.offsets),
+                        neighbors_sha=sha(gc.graph.neighbors), edge_count=gc.edge_count,
+                        view_edges_scanned=gc.view_edges_scanned))
+        return gc
+
+    v = pauli_view(2000, 16, 0)
+    b200.run(v, b200.PaletteParams(12.5, 2.0, seed=0), builder=tracing)
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        for k in g:
+            assert g[k] == w[k], k
+
+
+def test_edge_budget_two_phase_and_one_phase():
+    v = pauli_view(400, 6, 1)
+    lists = random_lists(v, seed=3)
+    full = b200.build(v, lists)
+    assert b200.build(v, lists, edge_budget=full.edge_count).edge_count == full.edge_count
+    with pytest.raises(EdgeBudgetExceededError) as ei:
+        b200.build(v, lists, edge_budget=full.edge_count - 1)
+    assert ei.value.projected == full.edge_count
+    # one-phase: partial count at the first overrunning reference block
+    from oracle.oracle import oracle_build
+
+    deg_upper = oracle_build(v, lists).deg_upper
+    for block_pairs, budget in ((64, 10), (4096, 500), (1 << 20, full.edge_count - 1)):
+        with pytest.raises(EdgeBudgetExceededError) as ei:
+            b200.build(v, lists, edge_budget=budget, two_phase=False, block_pairs=block_pairs)
+        assert ei.value.projected == one_phase_projection(deg_upper, block_pairs, budget)
+
+
+def test_threads_and_block_pairs_do_not_change_result():
+    v = pauli_view(150, 6, 9)
+    lists = random_lists(v, seed=7)
+    base = b200.build(v, lists)
+    for kw in (dict(threads=4), dict(block_pairs=64), dict(two_phase=False, threads=3)):
+        other = b200.build(v, lists, **kw)
+        assert np.array_equal(base.graph.neighbors, other.graph.neighbors)
+        assert np.array_equal(base.graph.offsets, other.graph.offsets)
+
+
+def test_invalid_codes_use_raw_word_predicate():
+    """Hand-built words with non-Pauli 3-bit codes: the build must follow popcount(a & b)
+    over the raw words exactly like the reference (pauli.py:258-268)."""
+    rs = np.random.default_rng(5)
+    n, q = 700, 21  # 63 bits: one word
+    words = rs.integers(0, 1 << 63, size=(n, 1), dtype=np.uint64)
+    ps = b200.PauliSet(["I" * q] * n, words)
+    v = b200.pauli_view(ps)
+    lists = random_lists(v, seed=2)
+    gc = b200.build(v, lists)
+    assert last_stats.raw_words_mode
+    want = oracle_builder(v, lists)
+    assert np.array_equal(gc.graph.neighbors, want.graph.neighbors)
+    assert gc.view_edges_scanned == want.view_edges_scanned
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3])
+def test_tiny_views(n):
+    v = pauli_view(10, 4, 0).induce(np.arange(n))
+    lists = b200.ColorLists.from_array(v.active, np.zeros((n, 1), dtype=np.int64), 0, 1)
+    gc = b200.build(v, lists)
+    want = oracle_builder(v, lists)
+    assert np.array_equal(gc.members, want.members)
+    assert np.array_equal(gc.graph.offsets, want.graph.offsets)
+    assert np.array_equal(gc.graph.neighbors, want.graph.neighbors)
+    assert gc.view_edges_scanned == want.view_edges_scanned
+    assert gc.graph.neighbors.dtype == np.int64 and gc.graph.offsets.dtype == np.int64
+
+
+@pytest.mark.parametrize("n,q", [(1500, 5), (3000, 20), (2500, 33), (5000, 64), (1200, 100),
+                                 (1100, 130), (2049, 128)])
+def test_commute_count_both_kernels_vs_oracle(n, q, k1_algo):
+    from oracle.oracle import OracleInstance
+
+    v = pauli_view(n, q, n + q)
+    lists = random_lists(v, seed=1)
+    gc = b200.build(v, lists)
+    inst = OracleInstance(v.backing.words, v.active, lists)
+    assert gc.view_edges_scanned == inst.commute_count()
+    for i in (0, n // 3, n - 1):
+        row, _ = inst.row(i)
+        assert np.array_equal(gc.graph.neighbors[gc.graph.offsets[i]:gc.graph.offsets[i + 1]], row)
+
+
+def test_full_size_config2_properties():
+    """BASELINE config 2 (100k x 32q): the oracle cannot build it in test time, so check
+    size-independent properties: commuting-pair total against the oracle's popcount sweep,
+    sampled full rows against the oracle, sortedness, degree/offset consistency, symmetry of
+    sampled rows."""
+    from oracle.oracle import OracleInstance
+
+    n = 100_000
+    v = pauli_view(n, 32, 0)
+    lists = random_lists(v, seed=0)
+    gc = b200.build(v, lists)
+    nb, off = gc.graph.neighbors, gc.graph.offsets
+    assert off[0] == 0 and off[-1] == nb.size == 2 * gc.edge_count
+    src = np.repeat(np.arange(gc.graph.n, dtype=np.int64), np.diff(off))
+    same = src[1:] == src[:-1]
+    assert np.all(np.diff(nb)[same] > 0)
+    assert not np.any(nb == src)
+    inst = OracleInstance(v.backing.words, v.active, lists)
+    assert gc.view_edges_scanned == inst.commute_count()
+    rs = np.random.default_rng(0)
+    for i in rs.choice(n, size=12, replace=False):
+        row, _ = inst.row(int(i))
+        got = nb[off[i]:off[i + 1]]
+        assert np.array_equal(got, row)
+        for j in got[:5]:  # symmetry
+            assert i in nb[off[j]:off[j + 1]]

@@ -1,0 +1,133 @@
+"""Host-side mirror of the reference API (no GPU): encoding, RNG, plan, block geometry,
+one-phase budget projection, and whole runs driven by the oracle builder."""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_2401_06713_b200 as b200
+from paper_2401_06713_b200 import rng
+from paper_2401_06713_b200.conflict import one_phase_projection
+from paper_2401_06713_b200.graph import pair_chunks
+from conftest import oracle_builder, pauli_view, sha
+
+
+def test_encode_known_answers(golden_ref):
+    enc = golden_ref["encode"]
+    assert b200.random_pauli_strings(2000, 16, seed=0)[:3] == enc["c1_first3"]
+    words = b200.PauliSet.from_strings(enc["c1_first3"]).words[:, 0]
+    assert [f"0x{int(w):016x}" for w in words] == enc["c1_words_first3"]
+    assert b200.encode("XYZI").value == enc["XYZI"] == 0b000011101110
+    w22 = b200.PauliSet.from_strings(["XYZI" * 5 + "YZ"]).words.ravel()
+    assert [f"0x{int(w):016x}" for w in w22] == enc["q22_words"]
+    assert b200.random_pauli_strings(8, 1, seed=2, exclude_identity=True) == enc["gen_exclude_identity"]
+
+
+def test_generator_hashes(golden_ref):
+    import hashlib
+
+    for key, want in golden_ref["encode"]["gen_hash"].items():
+        n, rest = key.split("x")
+        q, s = rest.split("s")
+        text = "\n".join(b200.random_pauli_strings(int(n), int(q), seed=int(s)))
+        assert hashlib.sha256(text.encode()).hexdigest()[:16] == want
+
+
+def test_single_letters_and_decode():
+    for ch, code in (("I", 0), ("X", 0b110), ("Y", 0b101), ("Z", 0b011)):
+        assert b200.encode(ch).value == code
+    s = "XYZIIZYXXZ" * 3
+    assert b200.decode(b200.encode(s)) == s
+
+
+def test_predicate_exhaustive_two_qubits():
+    import itertools
+
+    strings = ["".join(p) for p in itertools.product("IXYZ", repeat=2)]
+    ps = b200.PauliSet.from_strings(strings)
+    for a in range(16):
+        for b in range(16):
+            assert ps.anticommutes(a, b) == b200.anticommutes_oracle(strings[a], strings[b])
+
+
+def test_bad_inputs():
+    from paper_2401_06713_b200.errors import BadSymbolError, EmptyInputError, MixedLengthError
+
+    with pytest.raises(BadSymbolError):
+        b200.PauliSet.from_strings(["XQ"])
+    with pytest.raises(MixedLengthError):
+        b200.PauliSet.from_strings(["XX", "X"])
+    with pytest.raises(EmptyInputError):
+        b200.PauliSet.from_strings([])
+
+
+def test_rng_known_answers(golden_ref):
+    r = golden_ref["rng"]
+    hexes = lambda a: [f"0x{int(x):016x}" for x in a]  # noqa: E731
+    assert hexes(rng.mix64(np.array([0, 1, 2], dtype=np.uint64))) == r["mix64_0_1_2"]
+    keys = rng.stream_keys(0, 1, [0, 1, 2])
+    assert hexes(keys) == r["stream_keys_0_1"]
+    assert hexes(rng.stream_keys(-5, 3, [0, 7, 1 << 40])) == r["stream_keys_neg"]
+    assert rng.sample_distinct(keys, 250, 15)[0].tolist() == r["sample_250_15_row0"]
+    import re
+
+    for key, want in r["sample_hash"].items():
+        s, it, P, L, n = map(int, re.findall(r"\d+", key))
+        assert sha(rng.sample_distinct(rng.stream_keys(s, it, np.arange(n)), P, L)) == want
+
+
+def test_plan_values():
+    p = b200.plan_iteration(1, 1000, b200.PaletteParams(12.5, 2.0))
+    assert (p.palette_size, p.list_size) == (125, round(2 * math.log(1000)))
+    assert b200.plan_iteration(1, 100, b200.PaletteParams(3.0, 30.0)).list_size == 3
+    esc = b200.plan_iteration(2, 1000, b200.PaletteParams(12.5, 2.0), stall_count=2)
+    assert esc.palette_size == 500
+
+
+def _reference_chunks(n, target):
+    """graph.py:379-388 restated as the reference's loop."""
+    r0 = 0
+    while r0 < n - 1:
+        r1, pairs = r0, 0
+        while r1 < n - 1 and pairs < target:
+            pairs += n - 1 - r1
+            r1 += 1
+        yield r0, r1
+        r0 = r1
+
+
+@pytest.mark.parametrize("n,target", [(2, 1), (3, 64), (150, 64), (150, 10_000), (1000, 1 << 20),
+                                      (777, 1), (500, 1000)])
+def test_pair_chunks_geometry(n, target):
+    assert list(pair_chunks(n, target)) == list(_reference_chunks(n, target))
+
+
+def test_one_phase_projection():
+    rs = np.random.default_rng(3)
+    deg_upper = rs.integers(0, 5, size=300)
+    deg_upper[-1] = 0  # the last row has no partner j > i
+    for target in (64, 1000, 1 << 20):
+        for budget in (0, 10, 100, int(deg_upper.sum()) - 1):
+            total = 0
+            want = None
+            for r0, r1 in _reference_chunks(300, target):
+                total += int(deg_upper[r0:r1].sum())
+                if total > budget:
+                    want = total
+                    break
+            assert one_phase_projection(deg_upper, target, budget) == want
+
+
+@pytest.mark.parametrize("name", ["c1", "tout_k0", "tout_k3", "cli_fixture", "static_sdl",
+                                  "static_random", "aggressive"])
+def test_whole_runs_with_oracle_builder(golden_ref, name):
+    r = golden_ref["runs"][name]
+    v = pauli_view(r["n"], r["q"], r["gen_seed"])
+    res = b200.run(v, b200.PaletteParams(r["palette_pct"], r["alpha"], seed=r["seed"]),
+                   strategy=r["strategy"], builder=oracle_builder)
+    assert sha(res.color) == r["color_sha"]
+    assert sha(res.colored_at) == r["colored_at_sha"]
+    assert res.total_colors == r["colors"]
+    assert [rec.conflict_edges for rec in res.iterations] == [x["conflict_edges"] for x in r["records"]]
+    assert res.oracle_edges == r["oracle_edges"]

@@ -1,0 +1,44 @@
+"""Quick device timing of one build configuration (development aid, not the bench)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import time
+
+import numpy as np
+
+import paper_2401_06713_b200 as b200
+from paper_2401_06713_b200 import _native
+from paper_2401_06713_b200.conflict import stage
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=100_000)
+ap.add_argument("--q", type=int, default=32)
+ap.add_argument("--algo", type=int, default=0)
+ap.add_argument("--window", type=int, default=0)
+ap.add_argument("--reps", type=int, default=3)
+a = ap.parse_args()
+
+t = time.time()
+v = b200.pauli_view(b200.PauliSet.from_strings(b200.random_pauli_strings(a.n, a.q, seed=0)))
+plan = b200.plan_iteration(1, a.n, b200.PaletteParams(12.5, 2.0, seed=0))
+lists = b200.assign_random_lists(plan, v.active, 0)
+print(f"inputs {time.time()-t:.1f}s  P={plan.palette_size} L={plan.list_size}", flush=True)
+ctx = _native.context()
+ctx.option("k1_algo", a.algo)
+ctx.option("window", a.window)
+ctx.profiling(True)
+stage(v, lists, ctx)
+print("prep ms", ctx.kernel_times()[4])
+pairs = a.n * (a.n - 1) // 2
+for r in range(a.reps):
+    c, l1 = ctx.count_device()
+    l2 = ctx.fill_device()
+    kt = ctx.kernel_times()
+    print(f"rep {r}: K1 {kt[0]:.3f} ms ({pairs/kt[0]/1e9:.1f} Gpair/s)  K2count {kt[1]:.3f} ms  "
+          f"compact {kt[3]:.3f} ms  K2fill {kt[2]:.3f} ms  |E_c|={c.deg_sum//2} |E|={c.pairs_in_shard-c.anticommuting}",
+          flush=True)
+t = time.time()
+gc = b200.build(v, lists)
+print(f"e2e build {time.time()-t:.3f} s")
