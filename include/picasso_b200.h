@@ -107,13 +107,18 @@ int pcg_fill_rows(pcg_ctx *ctx, const int32_t *global_deg, int64_t *neighbors,
  * kernels this call launched. */
 int pcg_count_device(pcg_ctx *ctx, pcg_counts *out, int32_t *launches);
 int pcg_fill_device(pcg_ctx *ctx, int32_t *launches);
+/* One whole build on the staged raw inputs, device only: input prep (bit planes, color
+ * buckets, bucket commute masks) + count + fill; the CSR stays in HBM. */
+int pcg_build_device(pcg_ctx *ctx, pcg_counts *out, int32_t *launches);
 /* Average device time (ms) of each kernel family in the last *_device call:
  * [0] commute sweep (K1), [1] conflict-row count (K2c), [2] conflict-row fill (K2f),
  * [3] compaction/offsets, [4] input prep.  Requires pcg_set_profiling(ctx, 1). */
 int pcg_set_profiling(pcg_ctx *ctx, int32_t on);
 int pcg_kernel_times(pcg_ctx *ctx, float *ms, int32_t n);
 /* Kernel configuration knobs (testing/tuning): 0 = auto.
- *   K1 algorithm: 1 = direct LOP3/POPC tiles, 2 = four-Russians smem tables. */
+ *   "k1_algo": 1 = direct LOP3/POPC tiles, 2 = four-Russians smem tables
+ *   "k2_mode": 1 = row pass gathers partner vectors, 2 = bucket commute masks
+ *   "window": bitmap window of the row pass (ids), "fr_ichunk": rows per K1 work item */
 int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value);
 
 #ifdef __cplusplus

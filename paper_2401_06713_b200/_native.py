@@ -68,13 +68,14 @@ def library():
         lib.pcg_fill_rows.argtypes = [_VP, _VP, _VP, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]
         lib.pcg_count_device.argtypes = [_VP, ctypes.POINTER(Counts), ctypes.POINTER(_I32)]
         lib.pcg_fill_device.argtypes = [_VP, ctypes.POINTER(_I32)]
+        lib.pcg_build_device.argtypes = [_VP, ctypes.POINTER(Counts), ctypes.POINTER(_I32)]
         lib.pcg_set_profiling.argtypes = [_VP, _I32]
         lib.pcg_kernel_times.argtypes = [_VP, _VP, _I32]
         lib.pcg_set_option.argtypes = [_VP, ctypes.c_char_p, _I64]
         for name in ("pcg_create", "pcg_destroy", "pcg_set_inputs", "pcg_count",
                      "pcg_copy_degrees", "pcg_fill", "pcg_fill_rows", "pcg_count_device",
-                     "pcg_fill_device", "pcg_set_profiling", "pcg_kernel_times",
-                     "pcg_set_option"):
+                     "pcg_fill_device", "pcg_build_device", "pcg_set_profiling",
+                     "pcg_kernel_times", "pcg_set_option"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
         return lib
@@ -83,7 +84,7 @@ def library():
 EXPORTED = (
     "pcg_version", "pcg_create", "pcg_destroy", "pcg_last_error", "pcg_set_inputs", "pcg_count",
     "pcg_copy_degrees", "pcg_fill", "pcg_fill_rows", "pcg_count_device", "pcg_fill_device",
-    "pcg_set_profiling", "pcg_kernel_times", "pcg_set_option",
+    "pcg_build_device", "pcg_set_profiling", "pcg_kernel_times", "pcg_set_option",
 )
 
 
@@ -179,6 +180,13 @@ class Context:
         n = _I32(0)
         self._check(self.lib.pcg_count_device(self.h, ctypes.byref(c), ctypes.byref(n)),
                     "pcg_count_device")
+        return c, int(n.value)
+
+    def build_device(self) -> tuple:
+        c = Counts()
+        n = _I32(0)
+        self._check(self.lib.pcg_build_device(self.h, ctypes.byref(c), ctypes.byref(n)),
+                    "pcg_build_device")
         return c, int(n.value)
 
     def fill_device(self) -> int:

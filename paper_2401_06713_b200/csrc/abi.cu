@@ -143,7 +143,8 @@ int pcg_destroy(pcg_ctx *ctx) {
                       &ctx->H, &ctx->lrel, &ctx->rowof, &ctx->keys2, &ctx->vals2, &ctx->bstart,
                       &ctx->cubtmp, &ctx->deg, &ctx->degu, &ctx->compact, &ctx->rowoff,
                       &ctx->scal, &ctx->bad, &ctx->members_o, &ctx->offsets_o, &ctx->nbr_o,
-                      &ctx->gdeg, &ctx->items};
+                      &ctx->gdeg, &ctx->items, &ctx->eidx, &ctx->bpos, &ctx->bmemp,
+                      &ctx->posof, &ctx->maskoff, &ctx->masks};
     for (DevBuf *b : bufs) release(*b);
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
@@ -159,6 +160,7 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     if (!strcmp(key, "k1_algo")) ctx->k1_algo = (int)value;
     else if (!strcmp(key, "window")) ctx->window = (int)value;
     else if (!strcmp(key, "fr_ichunk")) ctx->fr_ichunk = (int)value;
+    else if (!strcmp(key, "k2_mode")) ctx->k2_mode = (int)value;
     else return fail(ctx, PCG_E_ARG, std::string("unknown option ") + key);
     return PCG_OK;
 }
@@ -191,6 +193,155 @@ static int encode_vectors(pcg_ctx *ctx, bool raw) {
                   ctx->npad, ctx->q, raw ? 1 : 0, ctx->A.as<uint32_t>(), ctx->B.as<uint32_t>(),
                   ctx->kw, ctx->bad.as<int32_t>(), s);
     PCG_CHECK_LAUNCH(ctx);
+    return PCG_OK;
+}
+
+
+namespace pcg_prep {
+struct PaddedSize {
+    const int32_t *bstart;
+    int64_t P;
+    __host__ __device__ int32_t operator()(int64_t c) const {
+        if (c >= P) return 0;
+        const int32_t m = bstart[c + 1] - bstart[c];
+        return (m + 3) & ~3;
+    }
+};
+struct MaskWords {
+    const int32_t *bstart;
+    int64_t P;
+    __host__ __device__ int64_t operator()(int64_t c) const {
+        if (c >= P) return 0;
+        const int64_t m = bstart[c + 1] - bstart[c];
+        return m * ((m + 31) / 32);
+    }
+};
+__global__ void k_iota(int32_t *x, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) x[i] = (int32_t)i;
+}
+}  // namespace pcg_prep
+using namespace pcg_prep;
+
+// K0 on the device-resident raw inputs: vectors, relative lists, color buckets, bucket
+// commute masks (K2a), four-Russians offsets.  Everything a build computes besides the count
+// and fill passes; the benchmark times it as part of every step.
+static int prep_device(pcg_ctx *ctx) {
+    cudaStream_t s = ctx->stream;
+    const int64_t n_active = ctx->n, entries = ctx->entries, P = ctx->P;
+    if (n_active == 0) return PCG_OK;
+    if (ctx->prof) cudaEventRecord(ctx->ev[10], s);
+    int rc = encode_vectors(ctx, false);
+    if (rc) return rc;
+    PCG_ALLOC(ctx, ctx->lrel, (size_t)entries * 4);
+    PCG_ALLOC(ctx, ctx->rowof, (size_t)entries * 4);
+    launch_lists(ctx->lists64.as<int64_t>(), ctx->ragged ? ctx->loff.as<int64_t>() : nullptr,
+                 n_active, ctx->L, entries, ctx->base, P, ctx->lrel.as<int32_t>(),
+                 ctx->rowof.as<int32_t>(), ctx->bad.as<int32_t>() + 1, s);
+    PCG_CHECK_LAUNCH(ctx);
+    int32_t bad[2] = {0, 0};
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(bad, ctx->bad.p, 8, cudaMemcpyDeviceToHost, s));
+    PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+    if (bad[1]) return fail(ctx, PCG_E_COLOR, "a list color lies outside the palette");
+    if (bad[0]) {
+        rc = encode_vectors(ctx, true);
+        if (rc) return rc;
+    }
+
+    // color buckets: stable radix sort of (color, entry) in row-major entry order, so each
+    // bucket lists its rows ascending
+    int end_bit = 1;
+    while ((1LL << end_bit) < P) ++end_bit;
+    PCG_ALLOC(ctx, ctx->eidx, (size_t)entries * 4);
+    PCG_ALLOC(ctx, ctx->keys2, (size_t)entries * 4);
+    PCG_ALLOC(ctx, ctx->vals2, (size_t)entries * 4);
+    k_iota<<<(unsigned)((entries + 255) / 256), 256, 0, s>>>(ctx->eidx.as<int32_t>(), entries);
+    size_t tmp = 0;
+    PCG_TRY_CUDA(ctx, cub::DeviceRadixSort::SortPairs(
+                          nullptr, tmp, ctx->lrel.as<int32_t>(), ctx->keys2.as<int32_t>(),
+                          ctx->eidx.as<int32_t>(), ctx->vals2.as<int32_t>(), (int)entries, 0,
+                          end_bit, s));
+    PCG_ALLOC(ctx, ctx->cubtmp, tmp);
+    PCG_TRY_CUDA(ctx, cub::DeviceRadixSort::SortPairs(
+                          ctx->cubtmp.p, tmp, ctx->lrel.as<int32_t>(), ctx->keys2.as<int32_t>(),
+                          ctx->eidx.as<int32_t>(), ctx->vals2.as<int32_t>(), (int)entries, 0,
+                          end_bit, s));
+    PCG_ALLOC(ctx, ctx->bstart, (size_t)(P + 1) * 4);
+    launch_bucket_bounds(ctx->keys2.as<int32_t>(), entries, P, ctx->bstart.as<int32_t>(), s);
+    PCG_CHECK_LAUNCH(ctx);
+
+    // padded bucket starts and mask offsets (exclusive scans over P+1 colors)
+    PCG_ALLOC(ctx, ctx->bpos, (size_t)(P + 1) * 4);
+    PCG_ALLOC(ctx, ctx->maskoff, (size_t)(P + 1) * 8);
+    cub::CountingInputIterator<int64_t> cidx(0);
+    cub::TransformInputIterator<int32_t, PaddedSize, cub::CountingInputIterator<int64_t>> padded(
+        cidx, PaddedSize{ctx->bstart.as<int32_t>(), P});
+    cub::TransformInputIterator<int64_t, MaskWords, cub::CountingInputIterator<int64_t>> mwords(
+        cidx, MaskWords{ctx->bstart.as<int32_t>(), P});
+    size_t t1 = 0, t2 = 0;
+    PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, t1, padded, ctx->bpos.as<int32_t>(),
+                                                    P + 1, s));
+    PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, t2, mwords,
+                                                    ctx->maskoff.as<int64_t>(), P + 1, s));
+    PCG_ALLOC(ctx, ctx->cubtmp, std::max(t1, t2));
+    PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->cubtmp.p, t1, padded,
+                                                    ctx->bpos.as<int32_t>(), P + 1, s));
+    PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->cubtmp.p, t2, mwords,
+                                                    ctx->maskoff.as<int64_t>(), P + 1, s));
+    int32_t padded_total = 0;
+    int64_t mask_total = 0;
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&padded_total, ctx->bpos.as<int32_t>() + P, 4,
+                                      cudaMemcpyDeviceToHost, s));
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&mask_total, ctx->maskoff.as<int64_t>() + P, 8,
+                                      cudaMemcpyDeviceToHost, s));
+    PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+    // bucket masks when they fit comfortably (dense corners with huge buckets use the
+    // partner-gather row kernel instead; both are exact)
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const size_t mask_bytes = (size_t)mask_total * 4;
+    ctx->masked = ctx->k2_mode == 2 ||
+                  (ctx->k2_mode == 0 && mask_bytes <= std::min<size_t>(free_b / 4, 24ull << 30));
+
+    PCG_ALLOC(ctx, ctx->bmemp, (size_t)(padded_total + 16) * 4);
+    PCG_ALLOC(ctx, ctx->posof, (size_t)entries * 4);
+    PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->bmemp.p, 0x7f, (size_t)(padded_total + 16) * 4, s));
+    BucketArgs b{};
+    b.P = P;
+    b.bstart = ctx->bstart.as<int32_t>();
+    b.sorted_e = ctx->vals2.as<int32_t>();
+    b.row_of = ctx->rowof.as<int32_t>();
+    b.bpos = ctx->bpos.as<int32_t>();
+    b.maskoff = ctx->maskoff.as<int64_t>();
+    b.bmemp = ctx->bmemp.as<int32_t>();
+    b.bmem = ctx->masked ? nullptr : ctx->keys2.as<int32_t>();  // keys are dead after bounds
+    b.posof = ctx->posof.as<int32_t>();
+    b.A = ctx->A.as<uint32_t>();
+    b.B = ctx->B.as<uint32_t>();
+    b.kw = ctx->kw;
+    launch_bucket_layout(b, entries, s);
+    PCG_CHECK_LAUNCH(ctx);
+    if (ctx->masked) {
+        PCG_ALLOC(ctx, ctx->masks, std::max<size_t>(mask_bytes, 16));
+        b.masks = ctx->masks.as<uint32_t>();
+        launch_bucket_masks(b, ctx->sms, s);
+        PCG_CHECK_LAUNCH(ctx);
+    }
+
+    // four-Russians row offsets
+    if (fr_supported(ctx->kw)) {
+        PCG_ALLOC(ctx, ctx->H, (size_t)ctx->npad * ctx->kw * 4 * 4);
+        launch_fr_prep(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
+        PCG_CHECK_LAUNCH(ctx);
+    }
+    PCG_ALLOC(ctx, ctx->deg, (size_t)n_active * 4);
+    PCG_ALLOC(ctx, ctx->degu, (size_t)n_active * 4);
+    ctx->prep_launches = 5 + (bad[0] ? 1 : 0) + (ctx->masked ? 1 : 0) + (fr_supported(ctx->kw) ? 1 : 0);
+    if (ctx->prof) {
+        cudaEventRecord(ctx->ev[11], s);
+        cudaEventSynchronize(ctx->ev[11]);
+        cudaEventElapsedTime(&ctx->ktimes[4], ctx->ev[10], ctx->ev[11]);
+    }
     return PCG_OK;
 }
 
@@ -261,62 +412,10 @@ extern "C" int pcg_set_inputs(pcg_ctx *ctx, const uint64_t *words, int64_t n_tot
         PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->loff.p, list_off, (size_t)(n_active + 1) * 8,
                                           cudaMemcpyHostToDevice, s));
     }
-    if (ctx->prof) cudaEventRecord(ctx->ev[10], s);
-
-    // Pauli words -> bit-plane vectors (raw 3-bit words if any code is invalid)
-    int rc = encode_vectors(ctx, false);
-    if (rc) return rc;
-    // color lists -> relative int32 + row ids
-    PCG_ALLOC(ctx, ctx->lrel, (size_t)entries * 4);
-    PCG_ALLOC(ctx, ctx->rowof, (size_t)entries * 4);
-    launch_lists(ctx->lists64.as<int64_t>(), ctx->ragged ? ctx->loff.as<int64_t>() : nullptr,
-                 n_active, list_len, entries, palette_base, palette_size, ctx->lrel.as<int32_t>(),
-                 ctx->rowof.as<int32_t>(), ctx->bad.as<int32_t>() + 1, s);
-    PCG_CHECK_LAUNCH(ctx);
-    int32_t bad[2] = {0, 0};
-    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(bad, ctx->bad.p, 8, cudaMemcpyDeviceToHost, s));
-    PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
-    if (bad[1]) return fail(ctx, PCG_E_COLOR, "a list color lies outside the palette");
-    if (bad[0]) {
-        rc = encode_vectors(ctx, true);
-        if (rc) return rc;
-    }
-
-    // color buckets: stable radix sort of (color, row) in row-major order -> ascending rows
-    int end_bit = 1;
-    while ((1LL << end_bit) < palette_size) ++end_bit;
-    PCG_ALLOC(ctx, ctx->keys2, (size_t)entries * 4);
-    PCG_ALLOC(ctx, ctx->vals2, (size_t)entries * 4);
-    size_t tmp = 0;
-    PCG_TRY_CUDA(ctx, cub::DeviceRadixSort::SortPairs(
-                          nullptr, tmp, ctx->lrel.as<int32_t>(), ctx->keys2.as<int32_t>(),
-                          ctx->rowof.as<int32_t>(), ctx->vals2.as<int32_t>(), (int)entries, 0,
-                          end_bit, s));
-    PCG_ALLOC(ctx, ctx->cubtmp, tmp);
-    PCG_TRY_CUDA(ctx, cub::DeviceRadixSort::SortPairs(
-                          ctx->cubtmp.p, tmp, ctx->lrel.as<int32_t>(), ctx->keys2.as<int32_t>(),
-                          ctx->rowof.as<int32_t>(), ctx->vals2.as<int32_t>(), (int)entries, 0,
-                          end_bit, s));
-    PCG_ALLOC(ctx, ctx->bstart, (size_t)(palette_size + 1) * 4);
-    launch_bucket_bounds(ctx->keys2.as<int32_t>(), entries, palette_size,
-                         ctx->bstart.as<int32_t>(), s);
-    PCG_CHECK_LAUNCH(ctx);
-
-    // four-Russians row offsets
-    if (fr_supported(ctx->kw)) {
-        PCG_ALLOC(ctx, ctx->H, (size_t)ctx->npad * ctx->kw * 4 * 4);
-        launch_fr_prep(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
-        PCG_CHECK_LAUNCH(ctx);
-    }
-    PCG_ALLOC(ctx, ctx->deg, (size_t)n_active * 4);
-    PCG_ALLOC(ctx, ctx->degu, (size_t)n_active * 4);
-    if (ctx->prof) {
-        cudaEventRecord(ctx->ev[11], s);
-        cudaEventSynchronize(ctx->ev[11]);
-        cudaEventElapsedTime(&ctx->ktimes[4], ctx->ev[10], ctx->ev[11]);
-    }
     ctx->staged = true;
-    return PCG_OK;
+    const int rc = prep_device(ctx);
+    if (rc) ctx->staged = false;
+    return rc;
 }
 
 // --------------------------------------------------------------------------------------
@@ -406,7 +505,7 @@ static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, 
 static int32_t pick_window(const pcg_ctx *ctx) {
     if (ctx->window > 0) return (int32_t)round_up(ctx->window, 4096);
     const int64_t w = round_up(std::max<int64_t>(ctx->n, 1), 4096);
-    return (int32_t)std::min<int64_t>(w, 32768);
+    return (int32_t)std::min<int64_t>(w, ctx->masked ? 65536 : 32768);
 }
 
 static RowArgs row_args(const pcg_ctx *ctx, int64_t r0, int64_t r1) {
@@ -421,7 +520,14 @@ static RowArgs row_args(const pcg_ctx *ctx, int64_t r0, int64_t r1) {
     a.loff = ctx->ragged ? ctx->loff.as<int64_t>() : nullptr;
     a.L = ctx->L;
     a.bstart = ctx->bstart.as<int32_t>();
-    a.bmem = ctx->vals2.as<int32_t>();
+    a.bmem = ctx->keys2.as<int32_t>();
+    if (ctx->masked) {
+        a.bpos = ctx->bpos.as<int32_t>();
+        a.bmemp = ctx->bmemp.as<int32_t>();
+        a.posof = ctx->posof.as<int32_t>();
+        a.maskoff = ctx->maskoff.as<int64_t>();
+        a.masks = ctx->masks.as<uint32_t>();
+    }
     a.deg = ctx->deg.as<int32_t>();
     a.degu = ctx->degu.as<int32_t>();
     a.window = pick_window(ctx);
@@ -610,6 +716,20 @@ extern "C" int pcg_count_device(pcg_ctx *ctx, pcg_counts *out, int32_t *launches
     if (!ctx) return PCG_E_ARG;
     int l = 0;
     int rc = count_impl(ctx, 0, 1, 0, ctx->n, out, &l);
+    if (launches) *launches = l;
+    return rc;
+}
+
+extern "C" int pcg_build_device(pcg_ctx *ctx, pcg_counts *out, int32_t *launches) {
+    if (!ctx) return PCG_E_ARG;
+    if (!ctx->staged) return fail(ctx, PCG_E_STATE, "pcg_build_device before pcg_set_inputs");
+    PCG_TRY_CUDA(ctx, cudaSetDevice(ctx->device));
+    int rc = prep_device(ctx);
+    if (rc) return rc;
+    int l = ctx->prep_launches;
+    rc = count_impl(ctx, 0, 1, 0, ctx->n, out, &l);
+    if (rc) return rc;
+    rc = fill_impl(ctx, false, nullptr, nullptr, nullptr, &l);
     if (launches) *launches = l;
     return rc;
 }

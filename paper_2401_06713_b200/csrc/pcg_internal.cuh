@@ -52,6 +52,28 @@ struct RowArgs {
     int64_t out_base;       // global entry index of out[0]
     int32_t window;         // bitmap window (bits), multiple of 4096
     int32_t slot_cap;       // color slots reserved per warp (>= max list length)
+    // bucket-mask mode (K2a + K2b): no partner gathers in the row pass
+    const int32_t *bpos;    // (P+1) 4-aligned start of each padded bucket in bmemp
+    const int32_t *bmemp;   // padded bucket members (ascending local ids, pad = sentinel)
+    const int32_t *posof;   // per list entry: position of its row inside the color's bucket
+    const int64_t *maskoff; // (P+1) word offset of each color's commute-mask matrix
+    const uint32_t *masks;  // per color: m rows of ceil(m/32) words, bit t = commute(k, t)
+};
+
+struct BucketArgs {
+    int64_t P;
+    const int32_t *bstart;    // (P+1) bucket bounds in the sorted entry array
+    const int32_t *sorted_e;  // list-entry index of every sorted position
+    const int32_t *row_of;    // row of every list entry
+    const int32_t *bpos;      // (P+1) padded bucket starts
+    const int64_t *maskoff;   // (P+1)
+    int32_t *bmemp;           // out: padded members
+    int32_t *bmem;            // out: unpadded members (direct mode), may be null
+    int32_t *posof;           // out: position of each entry in its bucket
+    uint32_t *masks;          // out: commute masks
+    const uint32_t *A;
+    const uint32_t *B;
+    int32_t kw;
 };
 
 // Launchers (each returns the number of kernels it launched).
@@ -73,6 +95,8 @@ int launch_commute_fr_items(const uint32_t *B, const uint32_t *H, int32_t kw, in
                             cudaStream_t s);
 int launch_fr_prep(const uint32_t *A, int32_t kw, int64_t npad, uint32_t *H, cudaStream_t s);
 int launch_rows(const RowArgs &a, bool fill, bool out64, int sms, cudaStream_t s);
+int launch_bucket_layout(const BucketArgs &b, int64_t entries, cudaStream_t s);
+int launch_bucket_masks(const BucketArgs &b, int sms, cudaStream_t s);
 int launch_compact(const int32_t *deg, int64_t n, const int32_t *compact, const int64_t *rowoff,
                    const int64_t *active, int64_t *members_out, int64_t *offsets_out,
                    cudaStream_t s);
@@ -98,6 +122,7 @@ struct pcg_ctx {
     int k1_algo = 0;    // 0 auto, 1 direct, 2 four-Russians
     int window = 0;     // K2 window bits (0 auto)
     int fr_ichunk = 0;  // four-Russians i-chunk (0 auto)
+    int k2_mode = 0;    // 0 auto, 1 direct partner gathers, 2 bucket masks
 
     // state of the last count
     bool counted = false;
@@ -111,5 +136,8 @@ struct pcg_ctx {
 
     // device buffers
     pcg::DevBuf words, active, lists64, loff, A, B, H, lrel, rowof, keys2, vals2, bstart,
-        cubtmp, deg, degu, compact, rowoff, scal, bad, members_o, offsets_o, nbr_o, gdeg, items;
+        cubtmp, deg, degu, compact, rowoff, scal, bad, members_o, offsets_o, nbr_o, gdeg, items,
+        eidx, bpos, bmemp, posof, maskoff, masks;
+    int prep_launches = 0;
+    bool masked = false;  // K2 uses bucket masks (K2a/K2b) instead of partner gathers
 };

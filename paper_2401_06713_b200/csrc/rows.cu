@@ -5,18 +5,31 @@
 //
 // Exact list intersection without the reference's dense ceil(P/64)-word masks: the
 // candidates of row i are the union of its L color buckets (bucket c = ascending local ids
-// holding color c).  One warp per row:
-//   mark   — lanes walk the L buckets (one bucket per lane, 4 loads in flight) and set
-//            bits in a per-warp shared-memory bitmap covering a window of `window` ids;
-//            duplicates (pairs sharing several colors) collapse in the bitmap.
-//   test   — lane l owns a contiguous segment of the window; it queues its set bits and
-//            tests them 8 at a time (8 independent partner loads in flight): commute
-//            predicate parity(popc(A_i & B_j)).
-//   emit   — count pass: degree and upper degree (j > i).  Fill pass: admitted bits are
-//            written back into the bitmap, a warp exclusive scan of the lane counts gives
-//            each lane's output offset, and lanes write their ids in order.
-// Windows advance left to right, so rows come out sorted.  Rows are independent: the
-// multi-GPU path simply gives each GPU a row range.
+// holding color c).  Two variants, bit-identical results:
+//
+//  * bucket-mask mode (default):
+//      K2a (color-major) k_bucket_masks — for every color c with members v_0 < ... < v_{m-1},
+//          the m x m commute matrix mask_c[k][t] = commute(v_k, v_t) && k != t, as m rows of
+//          ceil(m/32) words.  A member's partner vector is loaded once per color (one
+//          broadcast per warp) instead of once per (row, candidate): sum_c m_c = n*L loads
+//          instead of sum_c m_c^2 gathers.
+//      K2b (row-major) k_rows_masked — row i is member k of bucket c in each of its L
+//          colors; its admitted partners through c are the set bits of mask_c[k], in member
+//          order.  No partner vectors are touched.
+//  * gather mode (k_rows; dense corners where the masks would not fit): every candidate's
+//    partner vector is gathered and the predicate evaluated in the row pass.
+//
+// Both row passes: one warp per row, the id range swept in windows of `window` ids; lane s
+// walks bucket s of the row (8 members per round, all loads in flight) and admitted members
+// set their bit in a per-warp shared-memory bitmap of the window, which deduplicates
+// partners shared through several colors and sorts them.  Marking is a plain load / or /
+// store per round plus one verify pass; only bits lost to a same-word store of the same round
+// are re-applied with an atomic (shared atomics cost ~2 cycles per lane, so they stay off the
+// common path).  Harvest: lane l owns a contiguous segment of the window; the count pass
+// popcounts it (degree, and upper degree j > i), the fill pass takes a warp exclusive scan of
+// the segment popcounts and writes ids in ascending order.  Rows are independent: the
+// multi-GPU path gives each GPU a row range.
+#include <algorithm>
 #include <climits>
 
 #include "pcg_internal.cuh"
@@ -26,7 +39,9 @@ namespace pcg {
 namespace {
 
 constexpr int RW_WARPS = 8;
-constexpr int QLEN = 8;
+constexpr int UNR = 8;          // bucket members per lane per round
+constexpr int MASK_KG = 4;      // rows of one color per lane per pass in K2a (32*KG per pass)
+constexpr int MASK_WARPS = 8;
 
 template <int KW>
 struct RowVec {
@@ -82,21 +97,149 @@ __device__ __forceinline__ int warp_excl_scan(int v, int lane, int &total) {
     return x - v;
 }
 
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint4 lds_u128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_u128(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// Popcount of the bits of one 128-bit harvest chunk (ids jlo .. jlo+127) above `self`.
+__device__ __forceinline__ int upper_count(uint4 q, int32_t jlo, int32_t self) {
+    if (jlo > self) return __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
+    if (jlo + 128 <= self) return 0;
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+    int c = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int32_t d = self - (jlo + 32 * u);
+        const uint32_t m = d < 0 ? 0xffffffffu : (d >= 31 ? 0u : ~((2u << d) - 1u));
+        c += __popc(w[u] & m);
+    }
+    return c;
+}
+
+// Marks UNR candidate bits per lane (addr = shared byte address of the word, bit = 0 for
+// "nothing": such lanes hit their private dummy word).  Plain load / or / store, then one
+// verify; lost bits (same word stored twice in this round) go through an atomic.
+__device__ __forceinline__ void mark_round(const uint32_t (&addr)[UNR], const uint32_t (&bit)[UNR]) {
+    uint32_t old[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) old[u] = lds_u32(addr[u]);
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) sts_u32(addr[u], old[u] | bit[u]);
+    __syncwarp();
+    uint32_t lost = 0u;
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+        old[u] = bit[u] & ~lds_u32(addr[u]);
+        lost |= old[u];
+    }
+    if (__any_sync(0xffffffffu, lost != 0u)) {
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+            if (old[u])
+                atomicOr(reinterpret_cast<uint32_t *>(__cvta_shared_to_generic(addr[u])), old[u]);
+    }
+    __syncwarp();
+}
+
+// Harvest of one window: the count pass accumulates degree / upper degree; the fill pass
+// writes the admitted ids in ascending order.  Clears the lane's bitmap segment.
+template <bool FILL, typename OutT>
+__device__ __forceinline__ void harvest(uint32_t seg_s, int seg0, int SPL, int32_t w0, int32_t self,
+                                        int lane, int &cnt, int &cntu, int64_t &outpos,
+                                        OutT *out, const int32_t *compact) {
+    if constexpr (!FILL) {
+        for (int tt = 0; tt < SPL; tt += 4) {
+            const uint4 q4 = lds_u128(seg_s + tt * 4);
+            if ((q4.x | q4.y | q4.z | q4.w) == 0u) continue;
+            sts_u128(seg_s + tt * 4, make_uint4(0u, 0u, 0u, 0u));
+            cnt += __popc(q4.x) + __popc(q4.y) + __popc(q4.z) + __popc(q4.w);
+            cntu += upper_count(q4, w0 + (seg0 + tt) * 32, self);
+        }
+    } else {
+        int mine = 0;
+        for (int tt = 0; tt < SPL; tt += 4) {
+            const uint4 q4 = lds_u128(seg_s + tt * 4);
+            mine += __popc(q4.x) + __popc(q4.y) + __popc(q4.z) + __popc(q4.w);
+        }
+        int total;
+        const int base = warp_excl_scan(mine, lane, total);
+        int64_t pos = outpos + base;
+        for (int tt = 0; tt < SPL; tt += 4) {
+            const uint4 q4 = lds_u128(seg_s + tt * 4);
+            if ((q4.x | q4.y | q4.z | q4.w) == 0u) continue;
+            sts_u128(seg_s + tt * 4, make_uint4(0u, 0u, 0u, 0u));
+            const uint32_t wv[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                uint32_t wd = wv[u];
+                const int32_t jb = w0 + ((seg0 + tt + u) << 5);
+                while (wd) {
+                    const int b = __ffs(wd) - 1;
+                    wd &= wd - 1u;
+                    const int32_t j = jb + b;
+                    out[pos++] = (OutT)(compact ? compact[j] : j);
+                }
+            }
+        }
+        outpos += total;
+    }
+}
+
+template <bool FILL>
+__device__ __forceinline__ void finish_row(int64_t i, int lane, int cnt, int cntu, int32_t *deg,
+                                           int32_t *degu) {
+    if constexpr (!FILL) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            cnt += __shfl_down_sync(0xffffffffu, cnt, o);
+            cntu += __shfl_down_sync(0xffffffffu, cntu, o);
+        }
+        if (lane == 0) {
+            deg[i] = cnt;
+            degu[i] = cntu;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// gather mode
+// ---------------------------------------------------------------------------------------
 template <int KW, bool FILL, typename OutT>
 __global__ void __launch_bounds__(RW_WARPS * 32) k_rows(RowArgs a) {
     extern __shared__ __align__(16) uint32_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int WW = a.window >> 5;  // bitmap words
-    const int SPL = WW >> 5;       // words per lane segment (multiple of 4)
-    const int slots = (2 * a.slot_cap + 3) & ~3;  // keep every warp region 16-byte aligned
-    uint32_t *bm = smem + (size_t)warp * (WW + QLEN * 32 + slots);
-    int32_t *q = reinterpret_cast<int32_t *>(bm + WW);
-    int32_t *cur = q + QLEN * 32;
+    const int WW = a.window >> 5;
+    const int SPL = WW >> 5;
+    const int slots = (2 * a.slot_cap + 3) & ~3;
+    uint32_t *bm = smem + (size_t)warp * (WW + 32 + slots);
+    int32_t *cur = reinterpret_cast<int32_t *>(bm + WW + 32);
     int32_t *cend = cur + a.slot_cap;
+    const uint32_t bm_s = (uint32_t)__cvta_generic_to_shared(bm);
+    const uint32_t dummy_s = bm_s + (uint32_t)(WW + lane) * 4u;
     for (int k = lane; k < WW; k += 32) bm[k] = 0u;
     __syncwarp();
 
     OutT *out = reinterpret_cast<OutT *>(a.out);
+    const int seg0 = lane * SPL;
+    const uint32_t seg_s = bm_s + (uint32_t)seg0 * 4u;
     const int64_t stride = (int64_t)gridDim.x * RW_WARPS;
     for (int64_t i = a.row_begin + (int64_t)blockIdx.x * RW_WARPS + warp; i < a.row_end;
          i += stride) {
@@ -110,155 +253,254 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_rows(RowArgs a) {
         RowVec<KW> ai;
         ai.load(a.A, i, a.kw);
         __syncwarp();
-
         int cnt = 0, cntu = 0;
         int64_t outpos = FILL ? (a.rowoff[i] - a.out_base) : 0;
         const int32_t self = (int32_t)i;
         for (int32_t w0 = 0; w0 < a.n; w0 += a.window) {
             const int32_t w1 = (int32_t)min((int64_t)a.n, (int64_t)w0 + a.window);
-            // ---- mark the candidates of this window
-            for (int s = lane; s < Li; s += 32) {
-                int p = cur[s];
-                const int e = cend[s];
-                while (p < e) {
-                    int m[4];
+            for (int sg = 0; sg < Li; sg += 32) {
+                const int s = sg + lane;
+                const bool act = s < Li;
+                int p = act ? cur[s] : 0;
+                const int e = act ? cend[s] : 0;
+                bool go = act && p < e;
+                while (__any_sync(0xffffffffu, go)) {
+                    int m[UNR];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) m[u] = (p + u < e) ? __ldg(a.bmem + p + u) : INT_MAX;
+                    for (int u = 0; u < UNR; ++u)
+                        m[u] = (go && p + u < e) ? __ldg(a.bmem + p + u) : INT_MAX;
                     int k = 0;
 #pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        if (m[u] < w1) {
-                            const int off = m[u] - w0;
-                            atomicOr(&bm[off >> 5], 1u << (off & 31));
-                            ++k;
-                        }
+                    for (int u = 0; u < UNR; ++u) k += m[u] < w1 ? 1 : 0;
                     p += k;
-                    if (k < 4) break;
+                    go = go && k == UNR;
+                    uint32_t addr[UNR], bit[UNR];
+#pragma unroll
+                    for (int u = 0; u < UNR; ++u) {
+                        const bool adm = m[u] < w1 && m[u] != self &&
+                                         ai.parity(a.B, m[u], a.kw) == 0u;
+                        const uint32_t off = (uint32_t)(m[u] - w0);
+                        addr[u] = adm ? bm_s + ((off >> 5) << 2) : dummy_s;
+                        bit[u] = adm ? (1u << (off & 31)) : 0u;
+                    }
+                    mark_round(addr, bit);
                 }
-                cur[s] = p;
+                if (act) cur[s] = p;
             }
             __syncwarp();
-            if (lane == 0 && self >= w0 && self < w1) {
-                const int off = self - w0;
-                atomicAnd(&bm[off >> 5], ~(1u << (off & 31)));
-            }
-            __syncwarp();
-
-            // ---- test this lane's segment
-            const int seg0 = lane * SPL;
-            int nq = 0, lane_adm = 0;
-            auto flush = [&](int cntq) {
-                uint32_t par[QLEN];
-                int offs[QLEN];
-#pragma unroll
-                for (int k = 0; k < QLEN; ++k) {
-                    offs[k] = k < cntq ? q[k * 32 + lane] : 0;
-                    par[k] = k < cntq ? ai.parity(a.B, w0 + offs[k], a.kw) : 1u;
-                }
-#pragma unroll
-                for (int k = 0; k < QLEN; ++k) {
-                    if (k < cntq && par[k] == 0u) {
-                        ++lane_adm;
-                        if constexpr (FILL) {
-                            bm[offs[k] >> 5] |= 1u << (offs[k] & 31);
-                        } else {
-                            ++cnt;
-                            cntu += (w0 + offs[k] > self) ? 1 : 0;
-                        }
-                    }
-                }
-            };
-            for (int t = 0; t < SPL; t += 4) {
-                uint4 *p4 = reinterpret_cast<uint4 *>(bm + seg0 + t);
-                const uint4 v = *p4;
-                if ((v.x | v.y | v.z | v.w) == 0u) continue;
-                *p4 = make_uint4(0u, 0u, 0u, 0u);
-                const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    uint32_t wd = wv[u];
-                    while (wd) {
-                        const int b = __ffs(wd) - 1;
-                        wd &= wd - 1u;
-                        q[nq * 32 + lane] = ((seg0 + t + u) << 5) | b;
-                        if (++nq == QLEN) {
-                            flush(QLEN);
-                            nq = 0;
-                        }
-                    }
-                }
-            }
-            if (nq) flush(nq);
-
-            if constexpr (FILL) {
-                int total;
-                const int base = warp_excl_scan(lane_adm, lane, total);
-                int64_t pos = outpos + base;
-                for (int t = 0; t < SPL; t += 4) {
-                    uint4 *p4 = reinterpret_cast<uint4 *>(bm + seg0 + t);
-                    const uint4 v = *p4;
-                    if ((v.x | v.y | v.z | v.w) == 0u) continue;
-                    *p4 = make_uint4(0u, 0u, 0u, 0u);
-                    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        uint32_t wd = wv[u];
-                        while (wd) {
-                            const int b = __ffs(wd) - 1;
-                            wd &= wd - 1u;
-                            const int32_t j = w0 + (((seg0 + t + u) << 5) | b);
-                            out[pos++] = (OutT)(a.compact ? a.compact[j] : j);
-                        }
-                    }
-                }
-                outpos += total;
-            }
+            harvest<FILL, OutT>(seg_s, seg0, SPL, w0, self, lane, cnt, cntu, outpos, out, a.compact);
             __syncwarp();
         }
-        if constexpr (!FILL) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                cnt += __shfl_down_sync(0xffffffffu, cnt, o);
-                cntu += __shfl_down_sync(0xffffffffu, cntu, o);
-            }
-            if (lane == 0) {
-                a.deg[i] = cnt;
-                a.degu[i] = cntu;
-            }
-        }
+        finish_row<FILL>(i, lane, cnt, cntu, a.deg, a.degu);
         __syncwarp();
     }
 }
 
-template <int KW, bool FILL, typename OutT>
-int run_rows(const RowArgs &a, int sms, cudaStream_t s) {
-    const size_t per_warp = (size_t)((a.window >> 5) + QLEN * 32 + ((2 * a.slot_cap + 3) & ~3)) * 4;
+// ---------------------------------------------------------------------------------------
+// bucket-mask mode: K2a
+// ---------------------------------------------------------------------------------------
+__global__ void k_bucket_layout(BucketArgs b, int64_t entries) {
+    const int64_t pos = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (pos >= entries) return;
+    const int32_t e = b.sorted_e[pos];
+    int64_t lo = 0, hi = b.P;  // color of this sorted position (bstart is monotone)
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (b.bstart[mid] <= pos) lo = mid; else hi = mid;
+    }
+    const int32_t t = (int32_t)(pos - b.bstart[lo]);
+    const int32_t r = b.row_of[e];
+    b.bmemp[b.bpos[lo] + t] = r;
+    b.posof[e] = t;
+    if (b.bmem) b.bmem[pos] = r;
+}
+
+template <int KW>
+__global__ void __launch_bounds__(MASK_WARPS * 32) k_bucket_masks(BucketArgs b) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = blockIdx.x * (int64_t)MASK_WARPS + (threadIdx.x >> 5);
+    const int64_t nw = (int64_t)gridDim.x * MASK_WARPS;
+    for (int64_t c = gw; c < b.P; c += nw) {
+        const int m = b.bstart[c + 1] - b.bstart[c];
+        if (m < 2) {
+            if (m == 1 && lane == 0) b.masks[b.maskoff[c]] = 0u;
+            continue;
+        }
+        const int W = (m + 31) >> 5;
+        const int32_t *mem = b.bmemp + b.bpos[c];
+        uint32_t *out = b.masks + b.maskoff[c];
+        for (int kb = 0; kb < m; kb += 32 * MASK_KG) {
+            RowVec<KW> ak[MASK_KG];
+            int kk[MASK_KG];
+#pragma unroll
+            for (int g = 0; g < MASK_KG; ++g) {
+                kk[g] = kb + 32 * g + lane;
+                ak[g].load(b.A, kk[g] < m ? mem[kk[g]] : mem[0], b.kw);
+            }
+            for (int w = 0; w < W; ++w) {
+                uint32_t bits[MASK_KG];
+#pragma unroll
+                for (int g = 0; g < MASK_KG; ++g) bits[g] = 0u;
+                const int tend = min(32, m - 32 * w);
+                for (int tt = 0; tt < tend; ++tt) {
+                    const int t = 32 * w + tt;
+                    const int32_t j = mem[t];  // same address in every lane: one broadcast
+#pragma unroll
+                    for (int g = 0; g < MASK_KG; ++g) {
+                        const uint32_t par = ak[g].parity(b.B, j, b.kw);
+                        bits[g] |= ((par ^ 1u) & (t != kk[g] ? 1u : 0u)) << tt;
+                    }
+                }
+#pragma unroll
+                for (int g = 0; g < MASK_KG; ++g)
+                    if (kk[g] < m) out[(int64_t)kk[g] * W + w] = bits[g];
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// bucket-mask mode: K2b
+// ---------------------------------------------------------------------------------------
+template <bool FILL, typename OutT>
+__global__ void __launch_bounds__(RW_WARPS * 32) k_rows_masked(RowArgs a) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int WW = a.window >> 5;
+    const int SPL = WW >> 5;
+    // per-warp region: bitmap (WW) | 32 dummy words | slot arrays (t, m, base | row int64)
+    const int off_r = (3 * a.slot_cap + 1) & ~1;
+    const int slot_words = (off_r + 2 * a.slot_cap + 3) & ~3;
+    uint32_t *bm = smem + (size_t)warp * (WW + 32 + slot_words);
+    int32_t *st = reinterpret_cast<int32_t *>(bm + WW + 32);
+    int32_t *sm = st + a.slot_cap;
+    int32_t *sb = sm + a.slot_cap;
+    int64_t *sr = reinterpret_cast<int64_t *>(st + off_r);
+    const uint32_t bm_s = (uint32_t)__cvta_generic_to_shared(bm);
+    const uint32_t dummy_s = bm_s + (uint32_t)(WW + lane) * 4u;
+    for (int k = lane; k < WW; k += 32) bm[k] = 0u;
+    __syncwarp();
+
+    OutT *out = reinterpret_cast<OutT *>(a.out);
+    const int seg0 = lane * SPL;
+    const uint32_t seg_s = bm_s + (uint32_t)seg0 * 4u;
+    const int64_t stride = (int64_t)gridDim.x * RW_WARPS;
+    for (int64_t i = a.row_begin + (int64_t)blockIdx.x * RW_WARPS + warp; i < a.row_end;
+         i += stride) {
+        const int64_t lo = a.loff ? a.loff[i] : i * a.L;
+        const int Li = (int)((a.loff ? a.loff[i + 1] : lo + a.L) - lo);
+        for (int s = lane; s < Li; s += 32) {
+            const int c = a.lrel[lo + s];
+            const int m = a.bstart[c + 1] - a.bstart[c];
+            st[s] = 0;
+            sm[s] = m;
+            sb[s] = a.bpos[c];
+            sr[s] = a.maskoff[c] + (int64_t)a.posof[lo + s] * ((m + 31) >> 5);
+        }
+        __syncwarp();
+        int cnt = 0, cntu = 0;
+        int64_t outpos = FILL ? (a.rowoff[i] - a.out_base) : 0;
+        const int32_t self = (int32_t)i;
+        for (int32_t w0 = 0; w0 < a.n; w0 += a.window) {
+            const int32_t w1 = (int32_t)min((int64_t)a.n, (int64_t)w0 + a.window);
+            for (int sg = 0; sg < Li; sg += 32) {
+                const int s = sg + lane;
+                const bool act = s < Li;
+                int t = act ? st[s] : 0;
+                const int m = act ? sm[s] : 0;
+                const int32_t *mem = a.bmemp + (act ? sb[s] : 0);
+                const uint32_t *mrow = a.masks + (act ? sr[s] : 0);
+                bool go = act && t < m;
+                while (__any_sync(0xffffffffu, go)) {
+                    // 8 positions of an 8-aligned group (bucket starts are 4-aligned, padded)
+                    const int gs = t & ~(UNR - 1);
+                    int4 v0 = make_int4(INT_MAX, INT_MAX, INT_MAX, INT_MAX), v1 = v0;
+                    uint32_t mb = 0u;
+                    if (go) {
+                        v0 = __ldg(reinterpret_cast<const int4 *>(mem + gs));
+                        v1 = __ldg(reinterpret_cast<const int4 *>(mem + gs + 4));
+                        mb = __ldg(mrow + (gs >> 5)) >> (gs & 31);
+                    }
+                    const int v[UNR] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+                    uint32_t addr[UNR], bit[UNR];
+                    int k = 0;
+#pragma unroll
+                    for (int u = 0; u < UNR; ++u) {
+                        const bool in = (gs + u >= t) & (gs + u < m) & (v[u] < w1);
+                        k += in ? 1 : 0;
+                        const bool adm = in & ((mb >> u) & 1u);
+                        const uint32_t off = (uint32_t)(v[u] - w0);
+                        addr[u] = adm ? bm_s + ((off >> 5) << 2) : dummy_s;
+                        bit[u] = adm ? (1u << (off & 31)) : 0u;
+                    }
+                    t += k;
+                    go = go && t == gs + UNR && t < m;
+                    mark_round(addr, bit);
+                }
+                if (act) st[s] = t;
+            }
+            __syncwarp();
+            harvest<FILL, OutT>(seg_s, seg0, SPL, w0, self, lane, cnt, cntu, outpos, out, a.compact);
+            __syncwarp();
+        }
+        finish_row<FILL>(i, lane, cnt, cntu, a.deg, a.degu);
+        __syncwarp();
+    }
+}
+
+size_t gather_warp_bytes(const RowArgs &a) {
+    return (size_t)((a.window >> 5) + 32 + ((2 * a.slot_cap + 3) & ~3)) * 4;
+}
+size_t masked_warp_bytes(const RowArgs &a) {
+    const int off_r = (3 * a.slot_cap + 1) & ~1;
+    return (size_t)((a.window >> 5) + 32 + ((off_r + 2 * a.slot_cap + 3) & ~3)) * 4;
+}
+
+template <typename Kern>
+int launch_row_kernel(Kern k, const RowArgs &a, size_t per_warp, int sms, cudaStream_t s) {
     const size_t smem = per_warp * RW_WARPS;
-    cudaFuncSetAttribute(k_rows<KW, FILL, OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows<KW, FILL, OutT>,
-                                                  RW_WARPS * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, RW_WARPS * 32, smem);
     if (per_sm < 1) per_sm = 1;
     const int64_t rows = a.row_end - a.row_begin;
     int64_t grid = (int64_t)per_sm * sms;
     const int64_t need = (rows + RW_WARPS - 1) / RW_WARPS;
     if (grid > need) grid = need;
     if (grid < 1) grid = 1;
-    k_rows<KW, FILL, OutT><<<(unsigned)grid, RW_WARPS * 32, smem, s>>>(a);
+    k<<<(unsigned)grid, RW_WARPS * 32, smem, s>>>(a);
     return 1;
 }
 
 template <bool FILL, typename OutT>
-int dispatch_kw(const RowArgs &a, int sms, cudaStream_t s) {
+int dispatch_gather(const RowArgs &a, int sms, cudaStream_t s) {
+    const size_t pw = gather_warp_bytes(a);
     switch (a.kw) {
-        case 2: return run_rows<2, FILL, OutT>(a, sms, s);
-        case 4: return run_rows<4, FILL, OutT>(a, sms, s);
-        case 6: return run_rows<6, FILL, OutT>(a, sms, s);
-        case 8: return run_rows<8, FILL, OutT>(a, sms, s);
-        case 12: return run_rows<12, FILL, OutT>(a, sms, s);
-        default: return run_rows<0, FILL, OutT>(a, sms, s);
+        case 2: return launch_row_kernel(k_rows<2, FILL, OutT>, a, pw, sms, s);
+        case 4: return launch_row_kernel(k_rows<4, FILL, OutT>, a, pw, sms, s);
+        case 6: return launch_row_kernel(k_rows<6, FILL, OutT>, a, pw, sms, s);
+        case 8: return launch_row_kernel(k_rows<8, FILL, OutT>, a, pw, sms, s);
+        case 12: return launch_row_kernel(k_rows<12, FILL, OutT>, a, pw, sms, s);
+        default: return launch_row_kernel(k_rows<0, FILL, OutT>, a, pw, sms, s);
     }
+}
+
+template <bool FILL, typename OutT>
+int dispatch_rows(const RowArgs &a, int sms, cudaStream_t s) {
+    if (a.masks) return launch_row_kernel(k_rows_masked<FILL, OutT>, a, masked_warp_bytes(a), sms, s);
+    return dispatch_gather<FILL, OutT>(a, sms, s);
+}
+
+template <int KW>
+int run_masks(const BucketArgs &b, int sms, cudaStream_t s) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bucket_masks<KW>, MASK_WARPS * 32, 0);
+    if (per_sm < 1) per_sm = 1;
+    int64_t grid = (int64_t)per_sm * sms;
+    const int64_t need = (b.P + MASK_WARPS - 1) / MASK_WARPS;
+    if (grid > need) grid = need;
+    k_bucket_masks<KW><<<(unsigned)std::max<int64_t>(grid, 1), MASK_WARPS * 32, 0, s>>>(b);
+    return 1;
 }
 
 __global__ void k_compact(const int32_t *__restrict__ deg, int64_t n,
@@ -280,9 +522,27 @@ __global__ void k_compact(const int32_t *__restrict__ deg, int64_t n,
 
 int launch_rows(const RowArgs &a, bool fill, bool out64, int sms, cudaStream_t s) {
     if (a.row_end <= a.row_begin) return 0;
-    if (!fill) return dispatch_kw<false, int32_t>(a, sms, s);
-    if (out64) return dispatch_kw<true, int64_t>(a, sms, s);
-    return dispatch_kw<true, int32_t>(a, sms, s);
+    if (!fill) return dispatch_rows<false, int32_t>(a, sms, s);
+    if (out64) return dispatch_rows<true, int64_t>(a, sms, s);
+    return dispatch_rows<true, int32_t>(a, sms, s);
+}
+
+int launch_bucket_layout(const BucketArgs &b, int64_t entries, cudaStream_t s) {
+    if (entries == 0) return 0;
+    const int tb = 256;
+    k_bucket_layout<<<(unsigned)((entries + tb - 1) / tb), tb, 0, s>>>(b, entries);
+    return 1;
+}
+
+int launch_bucket_masks(const BucketArgs &b, int sms, cudaStream_t s) {
+    switch (b.kw) {
+        case 2: return run_masks<2>(b, sms, s);
+        case 4: return run_masks<4>(b, sms, s);
+        case 6: return run_masks<6>(b, sms, s);
+        case 8: return run_masks<8>(b, sms, s);
+        case 12: return run_masks<12>(b, sms, s);
+        default: return run_masks<0>(b, sms, s);
+    }
 }
 
 int launch_compact(const int32_t *deg, int64_t n, const int32_t *compact, const int64_t *rowoff,

@@ -24,7 +24,15 @@ def k1_algo(request):
     ctx.option("k1_algo", 0)
 
 
-def test_every_golden_build(golden_cases, k1_algo):
+@pytest.fixture(params=[1, 2], ids=["k2-gather", "k2-bucketmasks"])
+def k2_mode(request):
+    ctx = _native.context()
+    ctx.option("k2_mode", request.param)
+    yield request.param
+    ctx.option("k2_mode", 0)
+
+
+def test_every_golden_build(golden_cases, k1_algo, k2_mode):
     for case in golden_cases:
         case.check(b200.build(case.view, case.lists))
 
@@ -43,7 +51,7 @@ def test_hashed_q32_builds(golden_ref, n):
 
 
 @pytest.mark.parametrize("window", [4096, 8192, 32768])
-def test_window_geometry_does_not_change_rows(golden_ref, window):
+def test_window_geometry_does_not_change_rows(golden_ref, window, k2_mode):
     g = golden_ref["builds_hashed"]["q32_n10000"]
     ctx = _native.context()
     ctx.option("window", window)

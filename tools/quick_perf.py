@@ -17,6 +17,7 @@ ap.add_argument("--n", type=int, default=100_000)
 ap.add_argument("--q", type=int, default=32)
 ap.add_argument("--algo", type=int, default=0)
 ap.add_argument("--window", type=int, default=0)
+ap.add_argument("--k2", type=int, default=0)
 ap.add_argument("--reps", type=int, default=3)
 a = ap.parse_args()
 
@@ -28,17 +29,25 @@ print(f"inputs {time.time()-t:.1f}s  P={plan.palette_size} L={plan.list_size}", 
 ctx = _native.context()
 ctx.option("k1_algo", a.algo)
 ctx.option("window", a.window)
+ctx.option("k2_mode", a.k2)
 ctx.profiling(True)
 stage(v, lists, ctx)
 print("prep ms", ctx.kernel_times()[4])
 pairs = a.n * (a.n - 1) // 2
+import torch  # noqa: E402  (events only)
+
 for r in range(a.reps):
-    c, l1 = ctx.count_device()
-    l2 = ctx.fill_device()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0.record()
+    c, nl = ctx.build_device()
+    t1.record()
+    torch.cuda.synchronize()
     kt = ctx.kernel_times()
-    print(f"rep {r}: K1 {kt[0]:.3f} ms ({pairs/kt[0]/1e9:.1f} Gpair/s)  K2count {kt[1]:.3f} ms  "
-          f"compact {kt[3]:.3f} ms  K2fill {kt[2]:.3f} ms  |E_c|={c.deg_sum//2} |E|={c.pairs_in_shard-c.anticommuting}",
-          flush=True)
+    print(f"rep {r}: total {t0.elapsed_time(t1):.3f} ms  prep {kt[4]:.3f}  K1 {kt[0]:.3f} ms ({pairs/kt[0]/1e9:.1f} Gpair/s)  "
+          f"K2count {kt[1]:.3f}  compact {kt[3]:.3f}  K2fill {kt[2]:.3f}  launches {nl}  "
+          f"|E_c|={c.deg_sum//2} |E|={c.pairs_in_shard-c.anticommuting}", flush=True)
 t = time.time()
 gc = b200.build(v, lists)
 print(f"e2e build {time.time()-t:.3f} s")
