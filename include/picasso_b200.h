@@ -114,6 +114,8 @@ int pcg_build_device(pcg_ctx *ctx, pcg_counts *out, int32_t *launches);
  * [0] commute sweep (K1), [1] conflict-row count (K2c), [2] conflict-row fill (K2f),
  * [3] compaction/offsets, [4] input prep.  Requires pcg_set_profiling(ctx, 1). */
 int pcg_set_profiling(pcg_ctx *ctx, int32_t on);
+/* The context's CUDA stream (cudaStream_t), so callers can time it with their own events. */
+void *pcg_stream(pcg_ctx *ctx);
 int pcg_kernel_times(pcg_ctx *ctx, float *ms, int32_t n);
 /* Kernel configuration knobs (testing/tuning): 0 = auto.
  *   "k1_algo": 1 = direct LOP3/POPC tiles, 2 = four-Russians smem tables

@@ -72,6 +72,8 @@ def library():
         lib.pcg_set_profiling.argtypes = [_VP, _I32]
         lib.pcg_kernel_times.argtypes = [_VP, _VP, _I32]
         lib.pcg_set_option.argtypes = [_VP, ctypes.c_char_p, _I64]
+        lib.pcg_stream.argtypes = [_VP]
+        lib.pcg_stream.restype = _VP
         for name in ("pcg_create", "pcg_destroy", "pcg_set_inputs", "pcg_count",
                      "pcg_copy_degrees", "pcg_fill", "pcg_fill_rows", "pcg_count_device",
                      "pcg_fill_device", "pcg_build_device", "pcg_set_profiling",
@@ -84,7 +86,7 @@ def library():
 EXPORTED = (
     "pcg_version", "pcg_create", "pcg_destroy", "pcg_last_error", "pcg_set_inputs", "pcg_count",
     "pcg_copy_degrees", "pcg_fill", "pcg_fill_rows", "pcg_count_device", "pcg_fill_device",
-    "pcg_build_device", "pcg_set_profiling", "pcg_kernel_times", "pcg_set_option",
+    "pcg_build_device", "pcg_set_profiling", "pcg_kernel_times", "pcg_set_option", "pcg_stream",
 )
 
 
@@ -127,6 +129,9 @@ class Context:
         if rc == PCG_E_OOM:
             raise MemoryError(f"{what}: {msg}")
         raise DeviceError(f"{what} failed (code {rc}): {msg}")
+
+    def stream_handle(self) -> int:
+        return int(self.lib.pcg_stream(self.h) or 0)
 
     def option(self, key: str, value: int):
         self._check(self.lib.pcg_set_option(self.h, key.encode(), int(value)), "pcg_set_option")

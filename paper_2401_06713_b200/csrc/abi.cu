@@ -165,6 +165,8 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     return PCG_OK;
 }
 
+void *pcg_stream(pcg_ctx *ctx) { return ctx ? (void *)ctx->stream : nullptr; }
+
 int pcg_set_profiling(pcg_ctx *ctx, int32_t on) {
     if (!ctx) return PCG_E_ARG;
     ctx->prof = on != 0;
@@ -505,7 +507,7 @@ static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, 
 static int32_t pick_window(const pcg_ctx *ctx) {
     if (ctx->window > 0) return (int32_t)round_up(ctx->window, 4096);
     const int64_t w = round_up(std::max<int64_t>(ctx->n, 1), 4096);
-    return (int32_t)std::min<int64_t>(w, ctx->masked ? 65536 : 32768);
+    return (int32_t)std::min<int64_t>(w, 32768);
 }
 
 static RowArgs row_args(const pcg_ctx *ctx, int64_t r0, int64_t r1) {

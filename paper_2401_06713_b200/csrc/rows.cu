@@ -42,6 +42,7 @@ constexpr int RW_WARPS = 8;
 constexpr int UNR = 8;          // bucket members per lane per round
 constexpr int MASK_KG = 4;      // rows of one color per lane per pass in K2a (32*KG per pass)
 constexpr int MASK_WARPS = 8;
+constexpr int STAGE = 1024;     // fill-pass staging (ids per warp)
 
 template <int KW>
 struct RowVec {
@@ -134,20 +135,35 @@ __device__ __forceinline__ int upper_count(uint4 q, int32_t jlo, int32_t self) {
     return c;
 }
 
-// Marks UNR candidate bits per lane (addr = shared byte address of the word, bit = 0 for
-// "nothing": such lanes hit their private dummy word).  Plain load / or / store, then one
-// verify; lost bits (same word stored twice in this round) go through an atomic.
+__device__ __forceinline__ uint32_t lds_u32_if(bool p, uint32_t addr) {
+    uint32_t v = 0u;
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.shared.u32 %0, [%1];\n\t}"
+        : "+r"(v)
+        : "r"(addr), "r"((uint32_t)p)
+        : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_u32_if(bool p, uint32_t addr, uint32_t v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}" ::"r"(addr),
+                 "r"(v), "r"((uint32_t)p)
+                 : "memory");
+}
+
+// Marks up to UNR admitted bits per lane (bit == 0: nothing to mark; those accesses are
+// predicated off so they cost no shared-memory wavefronts).  Plain load / or / store, then
+// one verify; bits lost to a same-word store of this round go through an atomic.
 __device__ __forceinline__ void mark_round(const uint32_t (&addr)[UNR], const uint32_t (&bit)[UNR]) {
     uint32_t old[UNR];
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) old[u] = lds_u32(addr[u]);
+    for (int u = 0; u < UNR; ++u) old[u] = lds_u32_if(bit[u] != 0u, addr[u]);
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) sts_u32(addr[u], old[u] | bit[u]);
+    for (int u = 0; u < UNR; ++u) sts_u32_if(bit[u] != 0u, addr[u], old[u] | bit[u]);
     __syncwarp();
     uint32_t lost = 0u;
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-        old[u] = bit[u] & ~lds_u32(addr[u]);
+        old[u] = bit[u] & ~lds_u32_if(bit[u] != 0u, addr[u]);
         lost |= old[u];
     }
     if (__any_sync(0xffffffffu, lost != 0u)) {
@@ -159,47 +175,72 @@ __device__ __forceinline__ void mark_round(const uint32_t (&addr)[UNR], const ui
     __syncwarp();
 }
 
-// Harvest of one window: the count pass accumulates degree / upper degree; the fill pass
-// writes the admitted ids in ascending order.  Clears the lane's bitmap segment.
+// Harvest of one window.  Chunks are interleaved across lanes (lane l reads 16-byte chunk
+// it*32 + l), so every LDS.128 / STS.128 is conflict-free; ids keep ascending order because
+// chunk index grows with (it, lane).  Count pass: degree and upper degree.  Fill pass: per
+// chunk row a warp exclusive scan orders the ids; they are extracted into the warp's shared
+// staging buffer and stored to global memory coalesced.  Clears the bitmap.
 template <bool FILL, typename OutT>
-__device__ __forceinline__ void harvest(uint32_t seg_s, int seg0, int SPL, int32_t w0, int32_t self,
-                                        int lane, int &cnt, int &cntu, int64_t &outpos,
-                                        OutT *out, const int32_t *compact) {
+__device__ __forceinline__ void harvest(uint32_t bm_s, int WW, int32_t w0, int32_t self, int lane,
+                                        int &cnt, int &cntu, int64_t &outpos, OutT *out,
+                                        const int32_t *compact, int32_t *stage) {
+    const int rows = WW >> 7;  // 128 words (32 lanes x 4) per chunk row
     if constexpr (!FILL) {
-        for (int tt = 0; tt < SPL; tt += 4) {
-            const uint4 q4 = lds_u128(seg_s + tt * 4);
+        for (int it = 0; it < rows; ++it) {
+            const int c = it * 32 + lane;
+            const uint32_t addr = bm_s + (uint32_t)c * 16u;
+            const uint4 q4 = lds_u128(addr);
             if ((q4.x | q4.y | q4.z | q4.w) == 0u) continue;
-            sts_u128(seg_s + tt * 4, make_uint4(0u, 0u, 0u, 0u));
+            sts_u128(addr, make_uint4(0u, 0u, 0u, 0u));
             cnt += __popc(q4.x) + __popc(q4.y) + __popc(q4.z) + __popc(q4.w);
-            cntu += upper_count(q4, w0 + (seg0 + tt) * 32, self);
+            cntu += upper_count(q4, w0 + c * 128, self);
         }
     } else {
-        int mine = 0;
-        for (int tt = 0; tt < SPL; tt += 4) {
-            const uint4 q4 = lds_u128(seg_s + tt * 4);
-            mine += __popc(q4.x) + __popc(q4.y) + __popc(q4.z) + __popc(q4.w);
-        }
-        int total;
-        const int base = warp_excl_scan(mine, lane, total);
-        int64_t pos = outpos + base;
-        for (int tt = 0; tt < SPL; tt += 4) {
-            const uint4 q4 = lds_u128(seg_s + tt * 4);
-            if ((q4.x | q4.y | q4.z | q4.w) == 0u) continue;
-            sts_u128(seg_s + tt * 4, make_uint4(0u, 0u, 0u, 0u));
-            const uint32_t wv[4] = {q4.x, q4.y, q4.z, q4.w};
+        int fillv = 0;  // ids currently staged
+        for (int it = 0; it < rows; ++it) {
+            const int c = it * 32 + lane;
+            const uint32_t addr = bm_s + (uint32_t)c * 16u;
+            const uint4 q4 = lds_u128(addr);
+            const int nb = __popc(q4.x) + __popc(q4.y) + __popc(q4.z) + __popc(q4.w);
+            int total;
+            const int base = warp_excl_scan(nb, lane, total);
+            if (total == 0) continue;
+            const bool direct = total > STAGE;  // dense chunk row: store straight out
+            if (fillv > 0 && (direct || fillv + total > STAGE)) {
+                __syncwarp();
+                for (int k = lane; k < fillv; k += 32) out[outpos + k] = (OutT)stage[k];
+                outpos += fillv;
+                fillv = 0;
+                __syncwarp();
+            }
+            if (nb) {
+                sts_u128(addr, make_uint4(0u, 0u, 0u, 0u));
+                int64_t pos = direct ? outpos + base : fillv + base;
+                const uint32_t wv[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                uint32_t wd = wv[u];
-                const int32_t jb = w0 + ((seg0 + tt + u) << 5);
-                while (wd) {
-                    const int b = __ffs(wd) - 1;
-                    wd &= wd - 1u;
-                    const int32_t j = jb + b;
-                    out[pos++] = (OutT)(compact ? compact[j] : j);
+                for (int u = 0; u < 4; ++u) {
+                    uint32_t wd = wv[u];
+                    const int32_t jb = w0 + c * 128 + 32 * u;
+                    while (wd) {
+                        const int b = __ffs(wd) - 1;
+                        wd &= wd - 1u;
+                        const int32_t j = jb + b;
+                        const int32_t val = compact ? compact[j] : j;
+                        if (direct) out[pos++] = (OutT)val;
+                        else stage[pos++] = val;
+                    }
                 }
             }
+            if (direct) {
+                outpos += total;  // staging was flushed before this row
+            } else {
+                fillv += total;
+            }
         }
-        outpos += total;
+        __syncwarp();
+        for (int k = lane; k < fillv; k += 32) out[outpos + k] = (OutT)stage[k];
+        outpos += fillv;
+        __syncwarp();
     }
 }
 
@@ -227,10 +268,10 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_rows(RowArgs a) {
     extern __shared__ __align__(16) uint32_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int WW = a.window >> 5;
-    const int SPL = WW >> 5;
     const int slots = (2 * a.slot_cap + 3) & ~3;
-    uint32_t *bm = smem + (size_t)warp * (WW + 32 + slots);
-    int32_t *cur = reinterpret_cast<int32_t *>(bm + WW + 32);
+    uint32_t *bm = smem + (size_t)warp * (WW + 32 + STAGE + slots);
+    int32_t *stage = reinterpret_cast<int32_t *>(bm + WW + 32);
+    int32_t *cur = stage + STAGE;
     int32_t *cend = cur + a.slot_cap;
     const uint32_t bm_s = (uint32_t)__cvta_generic_to_shared(bm);
     const uint32_t dummy_s = bm_s + (uint32_t)(WW + lane) * 4u;
@@ -238,8 +279,6 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_rows(RowArgs a) {
     __syncwarp();
 
     OutT *out = reinterpret_cast<OutT *>(a.out);
-    const int seg0 = lane * SPL;
-    const uint32_t seg_s = bm_s + (uint32_t)seg0 * 4u;
     const int64_t stride = (int64_t)gridDim.x * RW_WARPS;
     for (int64_t i = a.row_begin + (int64_t)blockIdx.x * RW_WARPS + warp; i < a.row_end;
          i += stride) {
@@ -288,7 +327,7 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_rows(RowArgs a) {
                 if (act) cur[s] = p;
             }
             __syncwarp();
-            harvest<FILL, OutT>(seg_s, seg0, SPL, w0, self, lane, cnt, cntu, outpos, out, a.compact);
+            harvest<FILL, OutT>(bm_s, WW, w0, self, lane, cnt, cntu, outpos, out, a.compact, stage);
             __syncwarp();
         }
         finish_row<FILL>(i, lane, cnt, cntu, a.deg, a.degu);
@@ -367,12 +406,12 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_rows_masked(RowArgs a) {
     extern __shared__ __align__(16) uint32_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int WW = a.window >> 5;
-    const int SPL = WW >> 5;
     // per-warp region: bitmap (WW) | 32 dummy words | slot arrays (t, m, base | row int64)
     const int off_r = (3 * a.slot_cap + 1) & ~1;
     const int slot_words = (off_r + 2 * a.slot_cap + 3) & ~3;
-    uint32_t *bm = smem + (size_t)warp * (WW + 32 + slot_words);
-    int32_t *st = reinterpret_cast<int32_t *>(bm + WW + 32);
+    uint32_t *bm = smem + (size_t)warp * (WW + 32 + STAGE + slot_words);
+    int32_t *stage = reinterpret_cast<int32_t *>(bm + WW + 32);
+    int32_t *st = stage + STAGE;
     int32_t *sm = st + a.slot_cap;
     int32_t *sb = sm + a.slot_cap;
     int64_t *sr = reinterpret_cast<int64_t *>(st + off_r);
@@ -382,8 +421,6 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_rows_masked(RowArgs a) {
     __syncwarp();
 
     OutT *out = reinterpret_cast<OutT *>(a.out);
-    const int seg0 = lane * SPL;
-    const uint32_t seg_s = bm_s + (uint32_t)seg0 * 4u;
     const int64_t stride = (int64_t)gridDim.x * RW_WARPS;
     for (int64_t i = a.row_begin + (int64_t)blockIdx.x * RW_WARPS + warp; i < a.row_end;
          i += stride) {
@@ -440,7 +477,7 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_rows_masked(RowArgs a) {
                 if (act) st[s] = t;
             }
             __syncwarp();
-            harvest<FILL, OutT>(seg_s, seg0, SPL, w0, self, lane, cnt, cntu, outpos, out, a.compact);
+            harvest<FILL, OutT>(bm_s, WW, w0, self, lane, cnt, cntu, outpos, out, a.compact, stage);
             __syncwarp();
         }
         finish_row<FILL>(i, lane, cnt, cntu, a.deg, a.degu);
@@ -449,11 +486,11 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_rows_masked(RowArgs a) {
 }
 
 size_t gather_warp_bytes(const RowArgs &a) {
-    return (size_t)((a.window >> 5) + 32 + ((2 * a.slot_cap + 3) & ~3)) * 4;
+    return (size_t)((a.window >> 5) + 32 + STAGE + ((2 * a.slot_cap + 3) & ~3)) * 4;
 }
 size_t masked_warp_bytes(const RowArgs &a) {
     const int off_r = (3 * a.slot_cap + 1) & ~1;
-    return (size_t)((a.window >> 5) + 32 + ((off_r + 2 * a.slot_cap + 3) & ~3)) * 4;
+    return (size_t)((a.window >> 5) + 32 + STAGE + ((off_r + 2 * a.slot_cap + 3) & ~3)) * 4;
 }
 
 template <typename Kern>
