@@ -56,23 +56,27 @@ struct DegAt {
 
 __global__ void k_sum_degrees(const int32_t *__restrict__ deg, const int32_t *__restrict__ degu,
                               int64_t r0, int64_t r1, unsigned long long *out) {
-    unsigned long long s = 0, su = 0, m = 0;
+    unsigned long long s = 0, su = 0, m = 0, mx = 0;
     for (int64_t i = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r1;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int d = deg[i];
         s += d;
         su += degu[i];
         m += d > 0;
+        mx = d > (int)mx ? (unsigned long long)d : mx;
     }
     for (int o = 16; o > 0; o >>= 1) {
         s += __shfl_down_sync(0xffffffffu, s, o);
         su += __shfl_down_sync(0xffffffffu, su, o);
         m += __shfl_down_sync(0xffffffffu, m, o);
+        const unsigned long long y = __shfl_down_sync(0xffffffffu, mx, o);
+        mx = y > mx ? y : mx;
     }
     if ((threadIdx.x & 31) == 0) {
         atomicAdd(out + 1, s);
         atomicAdd(out + 2, su);
         atomicAdd(out + 3, m);
+        atomicMax(out + 4, mx);
     }
 }
 
@@ -161,6 +165,8 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "window")) ctx->window = (int)value;
     else if (!strcmp(key, "fr_ichunk")) ctx->fr_ichunk = (int)value;
     else if (!strcmp(key, "k2_mode")) ctx->k2_mode = (int)value;
+    else if (!strcmp(key, "merge_cap")) ctx->merge_cap = (int)value;
+    else if (!strcmp(key, "fill_algo")) ctx->fill_algo = (int)value;
     else return fail(ctx, PCG_E_ARG, std::string("unknown option ") + key);
     return PCG_OK;
 }
@@ -218,6 +224,14 @@ struct MaskWords {
         return m * ((m + 31) / 32);
     }
 };
+__global__ void k_bucket_max(const int32_t *bstart, int64_t P, int32_t *out) {
+    int32_t m = 0;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < P;
+         c += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, bstart[c + 1] - bstart[c]);
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
 __global__ void k_iota(int32_t *x, int64_t n) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) x[i] = (int32_t)i;
@@ -290,8 +304,13 @@ static int prep_device(pcg_ctx *ctx) {
                                                     ctx->bpos.as<int32_t>(), P + 1, s));
     PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->cubtmp.p, t2, mwords,
                                                     ctx->maskoff.as<int64_t>(), P + 1, s));
-    int32_t padded_total = 0;
+    PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->bad.as<int32_t>() + 2, 0, 4, s));
+    k_bucket_max<<<(unsigned)std::min<int64_t>((P + 255) / 256, 4 * ctx->sms), 256, 0, s>>>(
+        ctx->bstart.as<int32_t>(), P, ctx->bad.as<int32_t>() + 2);
+    int32_t padded_total = 0, m_max = 0;
     int64_t mask_total = 0;
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&m_max, ctx->bad.as<int32_t>() + 2, 4,
+                                      cudaMemcpyDeviceToHost, s));
     PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&padded_total, ctx->bpos.as<int32_t>() + P, 4,
                                       cudaMemcpyDeviceToHost, s));
     PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&mask_total, ctx->maskoff.as<int64_t>() + P, 8,
@@ -302,8 +321,11 @@ static int prep_device(pcg_ctx *ctx) {
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
     const size_t mask_bytes = (size_t)mask_total * 4;
-    ctx->masked = ctx->k2_mode == 2 ||
+    ctx->masked = ctx->k2_mode >= 2 ||
                   (ctx->k2_mode == 0 && mask_bytes <= std::min<size_t>(free_b / 4, 24ull << 30));
+    // ownership needs 12-bit member positions, 20-bit colors and <= 64 colors per list
+    ctx->owned = ctx->masked && ctx->k2_mode != 2 && m_max <= 4096 && P < (1 << 20) - 1 &&
+                 ctx->lmax <= 64 && ctx->kw <= 16;
 
     PCG_ALLOC(ctx, ctx->bmemp, (size_t)(padded_total + 16) * 4);
     PCG_ALLOC(ctx, ctx->posof, (size_t)entries * 4);
@@ -326,8 +348,30 @@ static int prep_device(pcg_ctx *ctx) {
     if (ctx->masked) {
         PCG_ALLOC(ctx, ctx->masks, std::max<size_t>(mask_bytes, 16));
         b.masks = ctx->masks.as<uint32_t>();
-        launch_bucket_masks(b, ctx->sms, s);
-        PCG_CHECK_LAUNCH(ctx);
+        if (ctx->owned) {
+            OwnArgs o{};
+            o.lrel = ctx->lrel.as<int32_t>();
+            o.loff = ctx->ragged ? ctx->loff.as<int64_t>() : nullptr;
+            o.L = ctx->L;
+            o.overflow = ctx->bad.as<int32_t>() + 3;
+            // table for the expected (c', k) entries of the largest bucket at load <= 1/2
+            int64_t want = (int64_t)m_max * std::max(1, ctx->lmax - 1);
+            int hs = 1024;
+            while (hs < want && hs < 32768) hs <<= 1;
+            o.hash_slots = hs;
+            o.m_cap = m_max;
+            PCG_TRY_CUDA(ctx, cudaMemsetAsync(o.overflow, 0, 4, s));
+            launch_owned_masks(b, o, ctx->sms, s);
+            PCG_CHECK_LAUNCH(ctx);
+            int32_t ovf = 0;
+            PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&ovf, o.overflow, 4, cudaMemcpyDeviceToHost, s));
+            PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+            if (ovf) ctx->owned = false;  // a color's ownership table overflowed: dedupe path
+        }
+        if (!ctx->owned) {
+            launch_bucket_masks(b, ctx->sms, s);
+            PCG_CHECK_LAUNCH(ctx);
+        }
     }
 
     // four-Russians row offsets
@@ -338,7 +382,7 @@ static int prep_device(pcg_ctx *ctx) {
     }
     PCG_ALLOC(ctx, ctx->deg, (size_t)n_active * 4);
     PCG_ALLOC(ctx, ctx->degu, (size_t)n_active * 4);
-    ctx->prep_launches = 5 + (bad[0] ? 1 : 0) + (ctx->masked ? 1 : 0) + (fr_supported(ctx->kw) ? 1 : 0);
+    ctx->prep_launches = 6 + (bad[0] ? 1 : 0) + (ctx->masked ? 1 : 0) + (fr_supported(ctx->kw) ? 1 : 0);
     if (ctx->prof) {
         cudaEventRecord(ctx->ev[11], s);
         cudaEventSynchronize(ctx->ev[11]);
@@ -510,6 +554,12 @@ static int32_t pick_window(const pcg_ctx *ctx) {
     return (int32_t)std::min<int64_t>(w, 32768);
 }
 
+static int32_t coop_window(const pcg_ctx *ctx) {
+    if (ctx->window > 0) return (int32_t)round_up(ctx->window, 4096);
+    const int64_t w = round_up(std::max<int64_t>(ctx->n, 1), 4096);
+    return (int32_t)std::min<int64_t>(w, 131072);
+}
+
 static RowArgs row_args(const pcg_ctx *ctx, int64_t r0, int64_t r1) {
     RowArgs a{};
     a.n = (int32_t)ctx->n;
@@ -561,14 +611,15 @@ static int count_impl(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t r0, 
         if (out) *out = c;
         return PCG_OK;
     }
-    PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->scal.p, 0, 32, s));
+    PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->scal.p, 0, 40, s));
     if (ctx->prof) cudaEventRecord(ctx->ev[0], s);
     int64_t pairs = 0;
     int rc = run_k1(ctx, shard, nshards, &pairs, launches);
     if (rc) return rc;
     if (ctx->prof) cudaEventRecord(ctx->ev[1], s);
     const RowArgs a = row_args(ctx, r0, r1);
-    *launches += launch_rows(a, false, false, ctx->sms, s);
+    *launches += ctx->owned ? launch_count_owned(a, ctx->sms, s)
+                            : launch_rows(a, false, false, ctx->sms, s);
     PCG_CHECK_LAUNCH(ctx);
     if (ctx->prof) cudaEventRecord(ctx->ev[2], s);
     if (r1 > r0) {
@@ -578,8 +629,8 @@ static int count_impl(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t r0, 
         *launches += 1;
         PCG_CHECK_LAUNCH(ctx);
     }
-    unsigned long long h[4];
-    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(h, ctx->scal.p, 32, cudaMemcpyDeviceToHost, s));
+    unsigned long long h[5];
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(h, ctx->scal.p, 40, cudaMemcpyDeviceToHost, s));
     PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
     if (ctx->prof) {
         cudaEventElapsedTime(&ctx->ktimes[0], ctx->ev[0], ctx->ev[1]);
@@ -590,6 +641,7 @@ static int count_impl(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t r0, 
     c.deg_sum = (int64_t)h[1];
     c.deg_upper_sum = (int64_t)h[2];
     c.members_in_range = (int64_t)h[3];
+    ctx->maxdeg = (int32_t)h[4];
     ctx->cnt_row_begin = r0;
     ctx->cnt_row_end = r1;
     ctx->last = c;
@@ -654,6 +706,61 @@ static int prefix_structures(pcg_ctx *ctx, const int32_t *deg, int64_t *n_member
     return PCG_OK;
 }
 
+
+// Fill pass for rows [r0, r1) into `out` (int64, entry index out_base at out[0]).  Owned
+// masks: warp merge of the disjoint runs, rows longer than the merge buffer go through the
+// bitmap row kernel; otherwise the bitmap row kernel for every row.
+static int fill_rows_device(pcg_ctx *ctx, int64_t r0, int64_t r1, const int32_t *deg,
+                            int32_t maxdeg, bool identity, void *out, int64_t out_base,
+                            int *launches) {
+    cudaStream_t s = ctx->stream;
+    RowArgs a = row_args(ctx, r0, r1);
+    a.deg = const_cast<int32_t *>(deg);
+    a.rowoff = ctx->rowoff.as<int64_t>();
+    a.compact = identity ? nullptr : ctx->compact.as<int32_t>();
+    a.out = out;
+    a.out_base = out_base;
+    if (!ctx->owned) {
+        *launches += launch_rows(a, true, true, ctx->sms, s);
+        PCG_CHECK_LAUNCH(ctx);
+        return PCG_OK;
+    }
+    if (ctx->fill_algo == 1) {  // cooperative bitmap fill (experimental)
+        a.window = coop_window(ctx);
+        *launches += launch_fill_coop(a, true, ctx->sms, s);
+        PCG_CHECK_LAUNCH(ctx);
+        return PCG_OK;
+    }
+    if (ctx->fill_algo != 2) {  // lane-per-bucket bitmap fill (default)
+        *launches += launch_rows(a, true, true, ctx->sms, s);
+        PCG_CHECK_LAUNCH(ctx);
+        return PCG_OK;
+    }
+    const int cap_max = ctx->merge_cap > 0 ? ctx->merge_cap : 6144;
+    MergeArgs g{};
+    g.cap = std::min(cap_max, std::max(32, (maxdeg + 31) & ~31));
+    PCG_ALLOC(ctx, ctx->heavy, (size_t)std::max<int64_t>(r1 - r0, 1) * 4);
+    g.heavy = ctx->heavy.as<int32_t>();
+    g.nheavy = reinterpret_cast<int32_t *>(ctx->scal.as<unsigned long long>() + 6);
+    PCG_TRY_CUDA(ctx, cudaMemsetAsync(g.nheavy, 0, 4, s));
+    *launches += launch_fill_merge(a, g, true, ctx->sms, s);
+    PCG_CHECK_LAUNCH(ctx);
+    if (maxdeg > g.cap) {
+        int32_t nh = 0;
+        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&nh, g.nheavy, 4, cudaMemcpyDeviceToHost, s));
+        PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+        if (nh > 0) {
+            RowArgs h = a;
+            h.rows_list = g.heavy;
+            h.row_begin = 0;
+            h.row_end = nh;
+            *launches += launch_rows(h, true, true, ctx->sms, s);
+            PCG_CHECK_LAUNCH(ctx);
+        }
+    }
+    return PCG_OK;
+}
+
 static int fill_impl(pcg_ctx *ctx, bool to_host, int64_t *members, int64_t *offsets,
                      int64_t *neighbors, int *launches) {
     if (!ctx->counted || ctx->cnt_row_begin != 0 || ctx->cnt_row_end != ctx->n)
@@ -681,13 +788,11 @@ static int fill_impl(pcg_ctx *ctx, bool to_host, int64_t *members, int64_t *offs
                                 ctx->members_o.as<int64_t>(), ctx->offsets_o.as<int64_t>(), s);
     PCG_CHECK_LAUNCH(ctx);
     if (ctx->prof) cudaEventRecord(ctx->ev[4], s);
-    RowArgs a = row_args(ctx, 0, n);
-    a.rowoff = ctx->rowoff.as<int64_t>();
-    a.compact = nm == n ? nullptr : ctx->compact.as<int32_t>();
-    a.out = ctx->nbr_o.p;
-    a.out_base = 0;
-    if (nnz > 0) *launches += launch_rows(a, true, true, ctx->sms, s);
-    PCG_CHECK_LAUNCH(ctx);
+    if (nnz > 0) {
+        rc = fill_rows_device(ctx, 0, n, ctx->deg.as<int32_t>(), ctx->maxdeg, nm == n,
+                              ctx->nbr_o.p, 0, launches);
+        if (rc) return rc;
+    }
     if (ctx->prof) cudaEventRecord(ctx->ev[5], s);
     if (to_host) {
         if (nm > 0 && members)
@@ -772,13 +877,12 @@ extern "C" int pcg_fill_rows(pcg_ctx *ctx, const int32_t *global_deg, int64_t *n
     const int64_t cnt = lohi[1] - lohi[0];
     if (cnt == 0) return PCG_OK;
     PCG_ALLOC(ctx, ctx->nbr_o, (size_t)cnt * 8);
-    RowArgs a = row_args(ctx, r0, r1);
-    a.rowoff = ctx->rowoff.as<int64_t>();
-    a.compact = nm == n ? nullptr : ctx->compact.as<int32_t>();
-    a.out = ctx->nbr_o.p;
-    a.out_base = lohi[0];
-    launch_rows(a, true, true, ctx->sms, s);
-    PCG_CHECK_LAUNCH(ctx);
+    int32_t gmax = 0;
+    for (int64_t r = r0; r < r1; ++r) gmax = std::max(gmax, global_deg[r]);
+    int l = 0;
+    rc = fill_rows_device(ctx, r0, r1, ctx->gdeg.as<int32_t>(), gmax, nm == n, ctx->nbr_o.p,
+                          lohi[0], &l);
+    if (rc) return rc;
     PCG_TRY_CUDA(ctx, cudaMemcpyAsync(neighbors, ctx->nbr_o.p, cnt * 8, cudaMemcpyDeviceToHost, s));
     PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
     return PCG_OK;

@@ -1,0 +1,583 @@
+// Owned bucket masks (K2a), popcount count pass (K2c) and merge fill pass (K2m).
+//
+// Ownership.  A conflict pair {u, v} is admitted through every color the two lists share;
+// k_owned_masks keeps it only in the commute mask of the SMALLEST shared color.  Then each
+// row's L mask rows are disjoint:
+//   deg[i]  = sum over i's colors c of popc(mask_c[k_c(i)])       (no dedupe, no bitmap)
+//   row i   = merge of L disjoint ascending runs                   (no duplicates)
+// A pair {v_k, v_t} of bucket c shares a smaller color iff some c' < c lies in both lists.
+// Per color, the CTA inserts (c', k) for every member k and every color c' < c of its list
+// into a shared-memory hash table keyed by c'; a key met twice marks the pairs of its group as
+// not owned by c, and their bits are cleared (a few per color: P(share >= 2 | share 1) is
+// ~(L-1)^2/P).  Exact; colors whose hash would overflow make the build use the dedupe path.
+#include <algorithm>
+#include <climits>
+
+#include "pcg_internal.cuh"
+
+namespace pcg {
+
+namespace {
+
+constexpr int OWN_THREADS = 128;
+constexpr int OWN_COLL = 4096;        // collision list capacity
+constexpr int MERGE_WARPS = 4;
+
+template <int KW>
+struct Vec {
+    uint32_t v[KW > 0 ? KW : 1];
+    __device__ __forceinline__ void load(const uint32_t *A, int64_t i, int kw) {
+#pragma unroll
+        for (int k = 0; k < KW; ++k) v[k] = __ldg(A + i * KW + k);
+    }
+    __device__ __forceinline__ uint32_t parity(const uint32_t *B, int32_t j, int kw) const {
+        uint32_t acc = 0;
+        const uint32_t *b = B + (int64_t)j * KW;
+#pragma unroll
+        for (int k = 0; k < KW; ++k) acc ^= v[k] & __ldg(b + k);
+        return __popc(acc) & 1u;
+    }
+};
+template <>
+struct Vec<0> {
+    const uint32_t *a;
+    __device__ __forceinline__ void load(const uint32_t *A, int64_t i, int kw) { a = A + i * kw; }
+    __device__ __forceinline__ uint32_t parity(const uint32_t *B, int32_t j, int kw) const {
+        uint32_t acc = 0;
+        const uint32_t *b = B + (int64_t)j * kw;
+        for (int k = 0; k < kw; ++k) acc ^= __ldg(a + k) & __ldg(b + k);
+        return __popc(acc) & 1u;
+    }
+};
+
+__device__ __forceinline__ uint32_t mix32(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    x ^= x >> 16;
+    return x;
+}
+
+// ---------------------------------------------------------------------------------------
+// K2a (owned): one CTA per color.
+// ---------------------------------------------------------------------------------------
+template <int KW>
+__global__ void __launch_bounds__(OWN_THREADS) k_owned_masks(BucketArgs b, OwnArgs o) {
+    extern __shared__ __align__(16) uint32_t osm[];
+    const int HS = o.hash_slots;
+    uint32_t *table = osm;                                   // HS: (c'+1)<<12 | first k
+    int32_t *head = reinterpret_cast<int32_t *>(osm + HS);   // HS: last collision + 1 per slot
+    uint32_t *coll = osm + 2 * HS;                           // OWN_COLL: slot<<12 | k
+    int32_t *link = reinterpret_cast<int32_t *>(coll + OWN_COLL);  // OWN_COLL: previous in slot
+    int32_t *sid = link + OWN_COLL;                          // member ids (m_cap)
+    uint32_t *sB = reinterpret_cast<uint32_t *>(sid + o.m_cap);   // partner vectors (m_cap * kw)
+    __shared__ int ncoll, overflow;
+    const int tid = threadIdx.x;
+    const int kw = b.kw;
+    for (int x = tid; x < 2 * HS; x += OWN_THREADS) osm[x] = 0u;
+    for (int64_t c = blockIdx.x; c < b.P; c += gridDim.x) {
+        const int m = b.bstart[c + 1] - b.bstart[c];
+        if (m < 2) {
+            if (m == 1 && tid == 0) b.masks[b.maskoff[c]] = 0u;
+            continue;
+        }
+        const int W = (m + 31) >> 5;
+        const int32_t *mem = b.bmemp + b.bpos[c];
+        uint32_t *out = b.masks + b.maskoff[c];
+        if (tid == 0) {
+            ncoll = 0;
+            overflow = 0;
+        }
+        for (int t = tid; t < m; t += OWN_THREADS) sid[t] = mem[t];
+        __syncthreads();
+        for (int x = tid; x < m * kw; x += OWN_THREADS) sB[x] = __ldg(b.B + (int64_t)sid[x / kw] * kw + x % kw);
+        __syncthreads();
+        // ---- commute masks: thread k owns row k
+        for (int k = tid; k < m; k += OWN_THREADS) {
+            uint32_t av[KW > 0 ? KW : 16];
+            for (int q = 0; q < kw; ++q) av[q] = __ldg(b.A + (int64_t)sid[k] * kw + q);
+            for (int w = 0; w < W; ++w) {
+                uint32_t bits = 0u;
+                const int tend = min(32, m - 32 * w);
+                for (int tt = 0; tt < tend; ++tt) {
+                    const uint32_t *bt = sB + (32 * w + tt) * kw;
+                    uint32_t acc = 0u;
+                    if constexpr (KW > 0) {
+#pragma unroll
+                        for (int q = 0; q < KW; ++q) acc ^= av[q] & bt[q];
+                    } else {
+                        for (int q = 0; q < kw; ++q) acc ^= av[q] & bt[q];
+                    }
+                    bits |= ((__popc(acc) & 1u) ^ 1u) << tt;
+                }
+                if (k >> 5 == w) bits &= ~(1u << (k & 31));  // no self pair
+                out[(int64_t)k * W + w] = bits;
+            }
+        }
+        // ---- ownership: (c', k) for every color c' < c of every member's list.  The first
+        // holder of c' stays in the table; later ones go to the collision list, chained per
+        // slot, so every pair of a group is produced exactly once (by its later member).
+        for (int k = tid; k < m; k += OWN_THREADS) {
+            const int32_t r = sid[k];
+            const int64_t lo = o.loff ? o.loff[r] : (int64_t)r * o.L;
+            const int64_t hi = o.loff ? o.loff[r + 1] : lo + o.L;
+            for (int64_t x = lo; x < hi; ++x) {
+                const int32_t cx = o.lrel[x];
+                if (cx >= c) continue;
+                const uint32_t cp = (uint32_t)cx + 1u;
+                const uint32_t key = (cp << 12) | (uint32_t)k;
+                uint32_t slot = mix32(cp) & (HS - 1);
+                for (int probe = 0;; ++probe) {
+                    if (probe == HS) {
+                        overflow = 1;
+                        break;
+                    }
+                    const uint32_t prev = atomicCAS(&table[slot], 0u, key);
+                    if (prev == 0u) break;
+                    if ((prev >> 12) == cp) {
+                        const int q = atomicAdd(&ncoll, 1);
+                        if (q < OWN_COLL) {
+                            coll[q] = (slot << 12) | (uint32_t)k;
+                            link[q] = atomicExch(&head[slot], q + 1) - 1;
+                        } else {
+                            overflow = 1;
+                        }
+                        break;
+                    }
+                    slot = (slot + 1) & (HS - 1);
+                }
+            }
+        }
+        __syncthreads();
+        const int nc = min(ncoll, OWN_COLL);
+        if (overflow && tid == 0) atomicExch(o.overflow, 1);
+        for (int q = tid; q < nc; q += OWN_THREADS) {
+            const uint32_t slot = coll[q] >> 12;
+            const int k2 = (int)(coll[q] & 0xfffu);
+            int k1 = (int)(table[slot] & 0xfffu);
+            for (int p = link[q];; p = link[p]) {
+                if (k1 != k2) {
+                    atomicAnd(&out[(int64_t)k1 * W + (k2 >> 5)], ~(1u << (k2 & 31)));
+                    atomicAnd(&out[(int64_t)k2 * W + (k1 >> 5)], ~(1u << (k1 & 31)));
+                }
+                if (p < 0) break;
+                k1 = (int)(coll[p] & 0xfffu);
+            }
+        }
+        __syncthreads();
+        // reset the table and the chain heads this color touched
+        for (int x = 4 * tid; x < HS; x += 4 * OWN_THREADS)
+            *reinterpret_cast<uint4 *>(table + x) = make_uint4(0u, 0u, 0u, 0u);
+        for (int q = tid; q < nc; q += OWN_THREADS) head[coll[q] >> 12] = 0;
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// K2c: degrees from owned masks (warp per row, lane per color slot)
+// ---------------------------------------------------------------------------------------
+__global__ void k_count_owned(RowArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = a.row_begin + gw; i < a.row_end; i += nw) {
+        const int64_t lo = a.loff ? a.loff[i] : i * a.L;
+        const int Li = (int)((a.loff ? a.loff[i + 1] : lo + a.L) - lo);
+        int cnt = 0, cntu = 0;
+        for (int s = lane; s < Li; s += 32) {
+            const int c = a.lrel[lo + s];
+            const int m = a.bstart[c + 1] - a.bstart[c];
+            const int W = (m + 31) >> 5;
+            const int k = a.posof[lo + s];
+            const uint32_t *row = a.masks + a.maskoff[c] + (int64_t)k * W;
+            for (int w = 0; w < W; ++w) {
+                const uint32_t x = __ldg(row + w);
+                cnt += __popc(x);
+                const int d = k - 32 * w;  // partners t > k are the ids > i (bucket ascends)
+                const uint32_t up = d < 0 ? 0xffffffffu : (d >= 31 ? 0u : ~((2u << d) - 1u));
+                cntu += __popc(x & up);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            cnt += __shfl_down_sync(0xffffffffu, cnt, o);
+            cntu += __shfl_down_sync(0xffffffffu, cntu, o);
+        }
+        if (lane == 0) {
+            a.deg[i] = cnt;
+            a.degu[i] = cntu;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// K2m: fill by merging the row's disjoint runs (warp per row, shared memory merge path)
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ int merge_split(const int32_t *A, int la, const int32_t *B, int lb,
+                                           int d) {
+    int lo = max(0, d - lb), hi = min(d, la);
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (A[mid] < B[d - 1 - mid]) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(MERGE_WARPS * 32) k_fill_merge(RowArgs a, MergeArgs g) {
+    extern __shared__ __align__(16) int32_t msm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int cap = g.cap;
+    int32_t *buf0 = msm + (size_t)warp * (2 * cap + 68);
+    int32_t *buf1 = buf0 + cap;
+    int32_t *roff = buf1 + cap;  // up to 33 run offsets (+ padding)
+    OutT *out = reinterpret_cast<OutT *>(a.out);
+    const int64_t gw = blockIdx.x * (int64_t)MERGE_WARPS + warp;
+    const int64_t nw = (int64_t)gridDim.x * MERGE_WARPS;
+    for (int64_t i = a.row_begin + gw; i < a.row_end; i += nw) {
+        const int deg = a.deg[i];
+        if (deg == 0) continue;
+        if (deg > cap) {  // too long for shared memory: the bitmap fill handles it
+            if (lane == 0) g.heavy[atomicAdd(g.nheavy, 1)] = (int32_t)i;
+            continue;
+        }
+        const int64_t lo = a.loff ? a.loff[i] : i * a.L;
+        const int Li = (int)((a.loff ? a.loff[i + 1] : lo + a.L) - lo);
+        // ---- decode: runs of the row's colors, ascending member ids where the owned bit is set
+        int fillv = 0;
+        for (int s = 0; s < Li; ++s) {
+            if (lane == 0) roff[s] = fillv;
+            const int c = a.lrel[lo + s];
+            const int m = a.bstart[c + 1] - a.bstart[c];
+            const int W = (m + 31) >> 5;
+            const uint32_t *row = a.masks + a.maskoff[c] + (int64_t)a.posof[lo + s] * W;
+            const int32_t *mem = a.bmemp + a.bpos[c];
+            for (int w0 = 0; w0 < W; w0 += 8) {
+                int32_t v[8];
+                uint32_t mw[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int w = w0 + u;
+                    mw[u] = w < W ? __ldg(row + w) : 0u;
+                    v[u] = (w < W && 32 * w + lane < m) ? __ldg(mem + 32 * w + lane) : 0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const bool adm = (mw[u] >> lane) & 1u;
+                    const uint32_t bal = __ballot_sync(0xffffffffu, adm);
+                    if (adm) buf0[fillv + __popc(bal & ((1u << lane) - 1u))] = v[u];
+                    fillv += __popc(bal);
+                }
+            }
+        }
+        if (lane == 0) roff[Li] = fillv;
+        __syncwarp();
+        // ---- merge tree: pairs of runs per level, merge path per lane
+        int R = Li;
+        int32_t *src = buf0, *dst = buf1;
+        while (R > 1) {
+            const int total = roff[R];
+            const int olo = (int)((int64_t)total * lane / 32);
+            const int ohi = (int)((int64_t)total * (lane + 1) / 32);
+            // each lane finds the pair(s) its output range falls in and merges on its own,
+            // so all lanes run their (equal-length) merge loops at the same time
+            int o = olo;
+            while (o < ohi) {
+                int p = 0;  // last pair whose output starts at or before o
+                for (int q = 1; 2 * q < R; ++q)
+                    if (roff[2 * q] <= o) p = q;
+                const int a0 = roff[2 * p], a1 = roff[min(2 * p + 1, R)];
+                const int e = roff[min(2 * p + 2, R)];
+                const int s1 = min(ohi, e);
+                const int32_t *A = src + a0, *B = src + a1;
+                const int la = a1 - a0, lb = e - a1;
+                int ia = merge_split(A, la, B, lb, o - a0);
+                int ib = (o - a0) - ia;
+                int32_t xa = ia < la ? A[ia] : INT_MAX;
+                int32_t xb = ib < lb ? B[ib] : INT_MAX;
+                for (; o < s1; ++o) {
+                    if (xa < xb) {
+                        dst[o] = xa;
+                        ++ia;
+                        xa = ia < la ? A[ia] : INT_MAX;
+                    } else {
+                        dst[o] = xb;
+                        ++ib;
+                        xb = ib < lb ? B[ib] : INT_MAX;
+                    }
+                }
+            }
+            __syncwarp();
+            const int R2 = (R + 1) >> 1;
+            int nr = 0;
+            if (lane <= R2) nr = roff[min(2 * lane, R)];
+            __syncwarp();
+            if (lane <= R2) roff[lane] = nr;
+            __syncwarp();
+            R = R2;
+            int32_t *t = src;
+            src = dst;
+            dst = t;
+        }
+        // ---- coalesced store (compact ids when some rows have no conflicts)
+        const int64_t base = a.rowoff[i] - a.out_base;
+        for (int k = lane; k < deg; k += 32) {
+            const int32_t j = src[k];
+            out[base + k] = (OutT)(a.compact ? a.compact[j] : j);
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// K2f: cooperative bitmap fill with owned masks (warp per row).  The warp walks one color
+// bucket at a time: 32 consecutive members per coalesced load (a whole bucket slice per
+// batch, all loads in flight), admitted members (owned-mask bit) compacted with a ballot, so
+// the ids in lanes 0..k-1 ascend.  Equal bitmap words can then only sit in neighbouring
+// lanes: two shuffles find them; unique words get a plain read-or-write, shared ones an
+// atomic.  Rows come out of the interleaved harvest in ascending order.
+// ---------------------------------------------------------------------------------------
+constexpr int COOP_WARPS = 8;
+constexpr int COOP_BATCH = 8;   // 32-member chunks per load batch
+constexpr int COOP_STAGE = 1024;
+
+__device__ __forceinline__ uint32_t c_lds(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void c_sts(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint4 c_lds4(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void c_sts4(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ int c_scan(int v, int lane, int &total) {
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    total = __shfl_sync(0xffffffffu, x, 31);
+    return x - v;
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(COOP_WARPS * 32) k_fill_coop(RowArgs a) {
+    extern __shared__ __align__(16) uint32_t csm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int WW = a.window >> 5;
+    uint32_t *bm = csm + (size_t)warp * (WW + COOP_STAGE + 4 * a.slot_cap);
+    int32_t *stage = reinterpret_cast<int32_t *>(bm + WW);
+    int32_t *st = stage + COOP_STAGE;       // cursor
+    int32_t *sm = st + a.slot_cap;          // bucket size
+    int32_t *sb = sm + a.slot_cap;          // bucket base in bmemp
+    int32_t *sw = sb + a.slot_cap;          // mask row offset (words) relative to masks
+    const uint32_t bm_s = (uint32_t)__cvta_generic_to_shared(bm);
+    for (int k = lane; k < WW; k += 32) bm[k] = 0u;
+    __syncwarp();
+    OutT *out = reinterpret_cast<OutT *>(a.out);
+    const uint32_t lt = (1u << lane) - 1u;
+    const int64_t stride = (int64_t)gridDim.x * COOP_WARPS;
+    for (int64_t ri = a.row_begin + (int64_t)blockIdx.x * COOP_WARPS + warp; ri < a.row_end;
+         ri += stride) {
+        const int64_t i = a.rows_list ? (int64_t)a.rows_list[ri] : ri;
+        if (a.deg[i] == 0) continue;
+        const int64_t lo = a.loff ? a.loff[i] : i * a.L;
+        const int Li = (int)((a.loff ? a.loff[i + 1] : lo + a.L) - lo);
+        for (int s = lane; s < Li; s += 32) {
+            const int c = a.lrel[lo + s];
+            const int m = a.bstart[c + 1] - a.bstart[c];
+            st[s] = 0;
+            sm[s] = m;
+            sb[s] = a.bpos[c];
+            sw[s] = (int32_t)(a.maskoff[c] + (int64_t)a.posof[lo + s] * ((m + 31) >> 5));
+        }
+        __syncwarp();
+        int64_t outpos = a.rowoff[i] - a.out_base;
+        for (int32_t w0 = 0; w0 < a.n; w0 += a.window) {
+            const int32_t w1 = (int32_t)min((int64_t)a.n, (int64_t)w0 + a.window);
+            for (int s = 0; s < Li; ++s) {
+                int t = st[s];
+                const int m = sm[s];
+                if (t >= m) continue;
+                const int32_t *mem = a.bmemp + sb[s];
+                const uint32_t *mrow = a.masks + sw[s];
+                bool more = true;
+                while (more) {
+                    int32_t v[COOP_BATCH];
+                    uint32_t mw[COOP_BATCH];
+#pragma unroll
+                    for (int u = 0; u < COOP_BATCH; ++u) {
+                        const int p = t + 32 * u + lane;
+                        const bool ok = p < m;
+                        v[u] = ok ? __ldg(mem + p) : INT_MAX;
+                        mw[u] = ok ? __ldg(mrow + (p >> 5)) : 0u;
+                    }
+#pragma unroll
+                    for (int u = 0; u < COOP_BATCH; ++u) {
+                        if (!more) break;
+                        const int p = t + lane;
+                        const bool in = v[u] < w1;
+                        const int k = __popc(__ballot_sync(0xffffffffu, in));
+                        const bool adm = in && ((mw[u] >> (p & 31)) & 1u);
+                        const uint32_t am = __ballot_sync(0xffffffffu, adm);
+                        const int na = __popc(am);
+                        // lane l < na takes the l-th admitted id (ascending)
+                        const int src = lane < na ? __fns(am, 0, lane + 1) : 0;
+                        const int32_t id = __shfl_sync(0xffffffffu, v[u], src);
+                        const bool act = lane < na;
+                        const uint32_t off = (uint32_t)(id - w0);
+                        const int32_t word = act ? (int32_t)(off >> 5) : -1 - lane;
+                        const int32_t up = __shfl_up_sync(0xffffffffu, word, 1);
+                        const int32_t dn = __shfl_down_sync(0xffffffffu, word, 1);
+                        const bool dup = act && ((lane > 0 && up == word) || (lane < 31 && dn == word));
+                        const uint32_t addr = bm_s + ((off >> 5) << 2);
+                        const uint32_t bit = 1u << (off & 31);
+                        if (act && !dup) c_sts(addr, c_lds(addr) | bit);
+                        if (__any_sync(0xffffffffu, dup)) {
+                            if (dup)
+                                atomicOr(reinterpret_cast<uint32_t *>(__cvta_shared_to_generic(addr)), bit);
+                        }
+                        t += k;
+                        more = (k == 32) && t < m;
+                    }
+                }
+                if (lane == 0) st[s] = t;
+                __syncwarp();
+            }
+            // ---- harvest: interleaved 16-byte chunks, ids staged then stored coalesced
+            const int rows = WW >> 7;
+            int fillv = 0;
+            for (int it = 0; it < rows; ++it) {
+                const int c = it * 32 + lane;
+                const uint32_t addr = bm_s + (uint32_t)c * 16u;
+                const uint4 q4 = c_lds4(addr);
+                const int nb = __popc(q4.x) + __popc(q4.y) + __popc(q4.z) + __popc(q4.w);
+                int total;
+                const int base = c_scan(nb, lane, total);
+                if (total == 0) continue;
+                const bool direct = total > COOP_STAGE;
+                if (fillv > 0 && (direct || fillv + total > COOP_STAGE)) {
+                    __syncwarp();
+                    for (int k = lane; k < fillv; k += 32) out[outpos + k] = (OutT)stage[k];
+                    outpos += fillv;
+                    fillv = 0;
+                    __syncwarp();
+                }
+                if (nb) {
+                    c_sts4(addr, make_uint4(0u, 0u, 0u, 0u));
+                    int64_t pos = direct ? outpos + base : fillv + base;
+                    const uint32_t wv[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        uint32_t wd = wv[u];
+                        const int32_t jb = w0 + c * 128 + 32 * u;
+                        while (wd) {
+                            const int bb = __ffs(wd) - 1;
+                            wd &= wd - 1u;
+                            const int32_t j = jb + bb;
+                            const int32_t val = a.compact ? a.compact[j] : j;
+                            if (direct) out[pos++] = (OutT)val;
+                            else stage[pos++] = val;
+                        }
+                    }
+                }
+                if (direct) outpos += total;
+                else fillv += total;
+            }
+            __syncwarp();
+            for (int k = lane; k < fillv; k += 32) out[outpos + k] = (OutT)stage[k];
+            outpos += fillv;
+            __syncwarp();
+        }
+    }
+}
+
+template <typename OutT>
+int run_coop(const RowArgs &a, int sms, cudaStream_t s) {
+    const size_t per_warp = (size_t)((a.window >> 5) + COOP_STAGE + 4 * a.slot_cap) * 4;
+    const size_t smem = per_warp * COOP_WARPS;
+    cudaFuncSetAttribute(k_fill_coop<OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fill_coop<OutT>, COOP_WARPS * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t rows = a.row_end - a.row_begin;
+    const int64_t grid = std::max<int64_t>(
+        1, std::min<int64_t>((int64_t)per_sm * sms, (rows + COOP_WARPS - 1) / COOP_WARPS));
+    k_fill_coop<OutT><<<(unsigned)grid, COOP_WARPS * 32, smem, s>>>(a);
+    return 1;
+}
+
+template <int KW>
+int run_owned(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s) {
+    int per_sm = 0;
+    const size_t smem = (size_t)(2 * o.hash_slots + 2 * OWN_COLL + o.m_cap + o.m_cap * b.kw) * 4;
+    cudaFuncSetAttribute(k_owned_masks<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_owned_masks<KW>, OWN_THREADS, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * sms * 4, b.P));
+    k_owned_masks<KW><<<(unsigned)grid, OWN_THREADS, smem, s>>>(b, o);
+    return 1;
+}
+
+template <typename OutT>
+int run_merge(const RowArgs &a, const MergeArgs &g, int sms, cudaStream_t s) {
+    const size_t smem = (size_t)MERGE_WARPS * (2 * g.cap + 68) * 4;
+    cudaFuncSetAttribute(k_fill_merge<OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fill_merge<OutT>, MERGE_WARPS * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t rows = a.row_end - a.row_begin;
+    const int64_t grid = std::max<int64_t>(
+        1, std::min<int64_t>((int64_t)per_sm * sms, (rows + MERGE_WARPS - 1) / MERGE_WARPS));
+    k_fill_merge<OutT><<<(unsigned)grid, MERGE_WARPS * 32, smem, s>>>(a, g);
+    return 1;
+}
+
+}  // namespace
+
+int launch_owned_masks(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s) {
+    switch (b.kw) {
+        case 2: return run_owned<2>(b, o, sms, s);
+        case 4: return run_owned<4>(b, o, sms, s);
+        case 6: return run_owned<6>(b, o, sms, s);
+        case 8: return run_owned<8>(b, o, sms, s);
+        case 12: return run_owned<12>(b, o, sms, s);
+        default: return run_owned<0>(b, o, sms, s);
+    }
+}
+
+int launch_count_owned(const RowArgs &a, int sms, cudaStream_t s) {
+    if (a.row_end <= a.row_begin) return 0;
+    const int64_t warps = a.row_end - a.row_begin;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, (int64_t)sms * 16));
+    k_count_owned<<<(unsigned)grid, 256, 0, s>>>(a);
+    return 1;
+}
+
+int launch_fill_merge(const RowArgs &a, const MergeArgs &g, bool out64, int sms, cudaStream_t s) {
+    if (a.row_end <= a.row_begin) return 0;
+    return out64 ? run_merge<int64_t>(a, g, sms, s) : run_merge<int32_t>(a, g, sms, s);
+}
+
+int merge_smem_bytes(int cap) { return MERGE_WARPS * (2 * cap + 68) * 4; }
+
+int launch_fill_coop(const RowArgs &a, bool out64, int sms, cudaStream_t s) {
+    if (a.row_end <= a.row_begin) return 0;
+    return out64 ? run_coop<int64_t>(a, sms, s) : run_coop<int32_t>(a, sms, s);
+}
+
+}  // namespace pcg

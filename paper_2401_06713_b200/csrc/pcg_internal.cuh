@@ -58,6 +58,22 @@ struct RowArgs {
     const int32_t *posof;   // per list entry: position of its row inside the color's bucket
     const int64_t *maskoff; // (P+1) word offset of each color's commute-mask matrix
     const uint32_t *masks;  // per color: m rows of ceil(m/32) words, bit t = commute(k, t)
+    const int32_t *rows_list; // if set: process rows rows_list[row_begin..row_end) instead
+};
+
+struct OwnArgs {
+    const int32_t *lrel;   // relative colors of every list entry
+    const int64_t *loff;   // ragged row offsets or null
+    int32_t L;
+    int32_t *overflow;     // set when a color's ownership table overflowed
+    int32_t hash_slots;    // power of two
+    int32_t m_cap;         // >= largest bucket
+};
+
+struct MergeArgs {
+    int32_t cap;           // ids per warp buffer; longer rows go to the bitmap fill
+    int32_t *heavy;        // out: rows longer than cap
+    int32_t *nheavy;       // out: their count
 };
 
 struct BucketArgs {
@@ -97,6 +113,11 @@ int launch_fr_prep(const uint32_t *A, int32_t kw, int64_t npad, uint32_t *H, cud
 int launch_rows(const RowArgs &a, bool fill, bool out64, int sms, cudaStream_t s);
 int launch_bucket_layout(const BucketArgs &b, int64_t entries, cudaStream_t s);
 int launch_bucket_masks(const BucketArgs &b, int sms, cudaStream_t s);
+int launch_owned_masks(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s);
+int launch_count_owned(const RowArgs &a, int sms, cudaStream_t s);
+int launch_fill_merge(const RowArgs &a, const MergeArgs &g, bool out64, int sms, cudaStream_t s);
+int merge_smem_bytes(int cap);
+int launch_fill_coop(const RowArgs &a, bool out64, int sms, cudaStream_t s);
 int launch_compact(const int32_t *deg, int64_t n, const int32_t *compact, const int64_t *rowoff,
                    const int64_t *active, int64_t *members_out, int64_t *offsets_out,
                    cudaStream_t s);
@@ -122,7 +143,9 @@ struct pcg_ctx {
     int k1_algo = 0;    // 0 auto, 1 direct, 2 four-Russians
     int window = 0;     // K2 window bits (0 auto)
     int fr_ichunk = 0;  // four-Russians i-chunk (0 auto)
-    int k2_mode = 0;    // 0 auto, 1 direct partner gathers, 2 bucket masks
+    int merge_cap = 0;  // fill-merge buffer cap (0 auto; testing knob)
+    int fill_algo = 0;  // owned masks: 0/3 lane-per-bucket bitmap fill, 1 cooperative bitmap, 2 merge
+    int k2_mode = 0;    // 0 auto, 1 partner gathers, 2 bucket masks + bitmap dedupe, 3 owned masks + merge
 
     // state of the last count
     bool counted = false;
@@ -137,7 +160,9 @@ struct pcg_ctx {
     // device buffers
     pcg::DevBuf words, active, lists64, loff, A, B, H, lrel, rowof, keys2, vals2, bstart,
         cubtmp, deg, degu, compact, rowoff, scal, bad, members_o, offsets_o, nbr_o, gdeg, items,
-        eidx, bpos, bmemp, posof, maskoff, masks;
+        eidx, bpos, bmemp, posof, maskoff, masks, heavy;
     int prep_launches = 0;
     bool masked = false;  // K2 uses bucket masks (K2a/K2b) instead of partner gathers
+    bool owned = false;   // masks keep each pair only in its smallest shared color
+    int32_t maxdeg = 0;
 };

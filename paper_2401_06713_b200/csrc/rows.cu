@@ -280,8 +280,9 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_rows(RowArgs a) {
 
     OutT *out = reinterpret_cast<OutT *>(a.out);
     const int64_t stride = (int64_t)gridDim.x * RW_WARPS;
-    for (int64_t i = a.row_begin + (int64_t)blockIdx.x * RW_WARPS + warp; i < a.row_end;
-         i += stride) {
+    for (int64_t ri = a.row_begin + (int64_t)blockIdx.x * RW_WARPS + warp; ri < a.row_end;
+         ri += stride) {
+        const int64_t i = a.rows_list ? (int64_t)a.rows_list[ri] : ri;
         const int64_t lo = a.loff ? a.loff[i] : i * a.L;
         const int Li = (int)((a.loff ? a.loff[i + 1] : lo + a.L) - lo);
         for (int s = lane; s < Li; s += 32) {
@@ -422,8 +423,9 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_rows_masked(RowArgs a) {
 
     OutT *out = reinterpret_cast<OutT *>(a.out);
     const int64_t stride = (int64_t)gridDim.x * RW_WARPS;
-    for (int64_t i = a.row_begin + (int64_t)blockIdx.x * RW_WARPS + warp; i < a.row_end;
-         i += stride) {
+    for (int64_t ri = a.row_begin + (int64_t)blockIdx.x * RW_WARPS + warp; ri < a.row_end;
+         ri += stride) {
+        const int64_t i = a.rows_list ? (int64_t)a.rows_list[ri] : ri;
         const int64_t lo = a.loff ? a.loff[i] : i * a.L;
         const int Li = (int)((a.loff ? a.loff[i + 1] : lo + a.L) - lo);
         for (int s = lane; s < Li; s += 32) {

@@ -24,7 +24,7 @@ def k1_algo(request):
     ctx.option("k1_algo", 0)
 
 
-@pytest.fixture(params=[1, 2], ids=["k2-gather", "k2-bucketmasks"])
+@pytest.fixture(params=[1, 2, 3], ids=["k2-gather", "k2-bucketmasks", "k2-owned-merge"])
 def k2_mode(request):
     ctx = _native.context()
     ctx.option("k2_mode", request.param)
@@ -35,6 +35,39 @@ def k2_mode(request):
 def test_every_golden_build(golden_cases, k1_algo, k2_mode):
     for case in golden_cases:
         case.check(b200.build(case.view, case.lists))
+
+
+@pytest.mark.parametrize("cap", [32, 96, 1024])
+def test_merge_heavy_rows_fallback(golden_cases, cap):
+    """Rows longer than the merge buffer take the bitmap fill; results must not change."""
+    ctx = _native.context()
+    ctx.option("k2_mode", 3)
+    ctx.option("fill_algo", 2)
+    ctx.option("merge_cap", cap)
+    try:
+        for case in golden_cases:
+            case.check(b200.build(case.view, case.lists))
+    finally:
+        ctx.option("merge_cap", 0)
+        ctx.option("fill_algo", 0)
+        ctx.option("k2_mode", 0)
+
+
+@pytest.mark.parametrize("window", [4096, 8192])
+def test_cooperative_fill_windows(golden_ref, window):
+    g = golden_ref["builds_hashed"]["q32_n20000"]
+    ctx = _native.context()
+    ctx.option("k2_mode", 3)
+    ctx.option("fill_algo", 1)
+    ctx.option("window", window)
+    try:
+        v = pauli_view(20000, 32, 0)
+        gc = b200.build(v, random_lists(v, seed=0))
+    finally:
+        ctx.option("window", 0)
+        ctx.option("fill_algo", 0)
+        ctx.option("k2_mode", 0)
+    assert sha(gc.graph.neighbors) == g["neighbors_sha"]
 
 
 @pytest.mark.parametrize("n", [5000, 10000, 20000])
