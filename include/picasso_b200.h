@@ -102,6 +102,16 @@ int pcg_fill(pcg_ctx *ctx, int64_t *members, int64_t *offsets, int64_t *neighbor
 int pcg_fill_rows(pcg_ctx *ctx, const int32_t *global_deg, int64_t *neighbors,
                   int64_t *slice_begin, int64_t *slice_end);
 
+/* Sharded build with device pointers (the NCCL merge operates on the caller's device
+ * buffers): degrees of the counted row range into deg_dev (int32, row_end-row_begin); the
+ * rows' CSR slice into neighbors_dev (int64; call with NULL first to learn the bounds). */
+int pcg_degrees_device(pcg_ctx *ctx, int32_t *deg_dev);
+/* Re-run the device input prep (bit planes, color buckets, bucket masks) on the staged raw
+ * inputs — the per-step replicated work of a sharded build. */
+int pcg_prep_device(pcg_ctx *ctx);
+int pcg_fill_rows_device(pcg_ctx *ctx, const int32_t *global_deg_dev, int32_t maxdeg,
+                         int64_t *neighbors_dev, int64_t *slice_begin, int64_t *slice_end);
+
 /* Device-resident timing hooks for the benchmark (no host traffic): re-run count and fill
  * on the inputs already staged; outputs stay in HBM.  *launches receives the number of
  * kernels this call launched. */

@@ -72,12 +72,17 @@ def library():
         lib.pcg_set_profiling.argtypes = [_VP, _I32]
         lib.pcg_kernel_times.argtypes = [_VP, _VP, _I32]
         lib.pcg_set_option.argtypes = [_VP, ctypes.c_char_p, _I64]
+        lib.pcg_degrees_device.argtypes = [_VP, _VP]
+        lib.pcg_prep_device.argtypes = [_VP]
+        lib.pcg_fill_rows_device.argtypes = [_VP, _VP, _I32, _VP, ctypes.POINTER(_I64),
+                                             ctypes.POINTER(_I64)]
         lib.pcg_stream.argtypes = [_VP]
         lib.pcg_stream.restype = _VP
         for name in ("pcg_create", "pcg_destroy", "pcg_set_inputs", "pcg_count",
                      "pcg_copy_degrees", "pcg_fill", "pcg_fill_rows", "pcg_count_device",
                      "pcg_fill_device", "pcg_build_device", "pcg_set_profiling",
-                     "pcg_kernel_times", "pcg_set_option"):
+                     "pcg_kernel_times", "pcg_set_option", "pcg_degrees_device",
+                     "pcg_fill_rows_device", "pcg_prep_device"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
         return lib
@@ -87,6 +92,7 @@ EXPORTED = (
     "pcg_version", "pcg_create", "pcg_destroy", "pcg_last_error", "pcg_set_inputs", "pcg_count",
     "pcg_copy_degrees", "pcg_fill", "pcg_fill_rows", "pcg_count_device", "pcg_fill_device",
     "pcg_build_device", "pcg_set_profiling", "pcg_kernel_times", "pcg_set_option", "pcg_stream",
+    "pcg_degrees_device", "pcg_fill_rows_device", "pcg_prep_device",
 )
 
 
@@ -178,6 +184,20 @@ class Context:
         g = np.ascontiguousarray(global_deg, dtype=np.int32)
         self._check(self.lib.pcg_fill_rows(self.h, _ptr(g), _ptr(neighbors), ctypes.byref(lo),
                                            ctypes.byref(hi)), "pcg_fill_rows")
+        return int(lo.value), int(hi.value)
+
+    def prep_device(self):
+        self._check(self.lib.pcg_prep_device(self.h), "pcg_prep_device")
+
+    def degrees_device(self, deg_ptr: int):
+        self._check(self.lib.pcg_degrees_device(self.h, _VP(deg_ptr)), "pcg_degrees_device")
+
+    def fill_rows_device(self, gdeg_ptr: int, maxdeg: int, out_ptr: int | None) -> tuple:
+        lo, hi = _I64(0), _I64(0)
+        self._check(self.lib.pcg_fill_rows_device(self.h, _VP(gdeg_ptr), int(maxdeg),
+                                                  _VP(out_ptr) if out_ptr else None,
+                                                  ctypes.byref(lo), ctypes.byref(hi)),
+                    "pcg_fill_rows_device")
         return int(lo.value), int(hi.value)
 
     def count_device(self) -> tuple:

@@ -887,3 +887,60 @@ extern "C" int pcg_fill_rows(pcg_ctx *ctx, const int32_t *global_deg, int64_t *n
     PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
     return PCG_OK;
 }
+
+// Device-pointer variants for the sharded build (NCCL collectives operate on the caller's
+// device tensors; nothing crosses PCIe).
+extern "C" int pcg_degrees_device(pcg_ctx *ctx, int32_t *deg_dev) {
+    if (!ctx || !deg_dev) return PCG_E_ARG;
+    if (!ctx->counted) return fail(ctx, PCG_E_STATE, "pcg_degrees_device before pcg_count");
+    PCG_TRY_CUDA(ctx, cudaSetDevice(ctx->device));
+    const int64_t r0 = ctx->cnt_row_begin, r1 = ctx->cnt_row_end;
+    if (r1 > r0)
+        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(deg_dev, ctx->deg.as<int32_t>() + r0, (r1 - r0) * 4,
+                                          cudaMemcpyDeviceToDevice, ctx->stream));
+    PCG_TRY_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return PCG_OK;
+}
+
+extern "C" int pcg_fill_rows_device(pcg_ctx *ctx, const int32_t *global_deg_dev, int32_t maxdeg,
+                                    int64_t *neighbors_dev, int64_t *slice_begin,
+                                    int64_t *slice_end) {
+    if (!ctx || !global_deg_dev || !slice_begin || !slice_end) return PCG_E_ARG;
+    if (!ctx->counted) return fail(ctx, PCG_E_STATE, "pcg_fill_rows_device before pcg_count");
+    PCG_TRY_CUDA(ctx, cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const int64_t n = ctx->n, r0 = ctx->cnt_row_begin, r1 = ctx->cnt_row_end;
+    if (n < 2) {
+        *slice_begin = *slice_end = 0;
+        return PCG_OK;
+    }
+    PCG_ALLOC(ctx, ctx->gdeg, (size_t)n * 4);
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->gdeg.p, global_deg_dev, n * 4,
+                                      cudaMemcpyDeviceToDevice, s));
+    int64_t nm = 0;
+    int rc = prefix_structures(ctx, ctx->gdeg.as<int32_t>(), &nm);
+    if (rc) return rc;
+    int64_t lohi[2];
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&lohi[0], ctx->rowoff.as<int64_t>() + r0, 8,
+                                      cudaMemcpyDeviceToHost, s));
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&lohi[1], ctx->rowoff.as<int64_t>() + r1, 8,
+                                      cudaMemcpyDeviceToHost, s));
+    PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+    *slice_begin = lohi[0];
+    *slice_end = lohi[1];
+    if (!neighbors_dev || lohi[1] == lohi[0]) return PCG_OK;
+    int l = 0;
+    rc = fill_rows_device(ctx, r0, r1, ctx->gdeg.as<int32_t>(), maxdeg, nm == n, neighbors_dev,
+                          lohi[0], &l);
+    if (rc) return rc;
+    PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+    return PCG_OK;
+}
+
+extern "C" int pcg_prep_device(pcg_ctx *ctx) {
+    if (!ctx) return PCG_E_ARG;
+    if (!ctx->staged) return fail(ctx, PCG_E_STATE, "pcg_prep_device before pcg_set_inputs");
+    PCG_TRY_CUDA(ctx, cudaSetDevice(ctx->device));
+    ctx->counted = false;
+    return prep_device(ctx);
+}

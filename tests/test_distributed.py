@@ -1,0 +1,147 @@
+"""Multi-rank host logic of the sharded build (distributed.py) on CPU: gloo process group,
+world size 2 and 3, with an oracle-backed engine standing in for each rank's GPU.  The
+assembled CSR must equal the reference golden CSR on every rank, and budget errors must be
+raised identically everywhere."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+class OracleEngine:
+    """Per-rank engine computing on the CPU oracle (test infrastructure only)."""
+
+    def set_inputs(self, words, num_qubits, active, data, off, L, base, P):
+        from oracle.oracle import OracleInstance
+        from paper_2401_06713_b200.driver import ColorLists
+
+        n = active.size
+        if off is None:
+            lists = ColorLists.from_array(active, data.reshape(n, L), base, P)
+        else:
+            lists = ColorLists(active, [data[off[k]:off[k + 1]] for k in range(n)], base, P)
+        self.inst = OracleInstance(words, active, lists, threads=2)
+        self.csr = self.inst.build()
+        self.n = n
+        deg = np.zeros(n, dtype=np.int64)
+        local = np.searchsorted(active, self.csr.members)
+        deg[local] = np.diff(self.csr.offsets)
+        self.deg = deg
+        self.degu = self.csr.deg_upper
+        # commuting partners j > i per row (row-wise K1 shard stand-in)
+        w = words[active]
+        self.comm_upper = np.zeros(n, dtype=np.int64)
+        for i in range(n):
+            acc = np.bitwise_xor.reduce(w[i + 1:] & w[i], axis=1) if i + 1 < n else np.zeros(0, np.uint64)
+            self.comm_upper[i] = int((np.bitwise_count(acc) & 1 == 0).sum())
+
+    def count(self, shard, nshards, r0, r1):
+        a, b = self.n * shard // nshards, self.n * (shard + 1) // nshards
+        rows = np.arange(a, b)
+        pairs = int((self.n - 1 - rows).sum())
+        return dict(anticommuting=pairs - int(self.comm_upper[a:b].sum()), pairs=pairs,
+                    deg_sum=int(self.deg[r0:r1].sum()), members=int((self.deg[r0:r1] > 0).sum()))
+
+    def degrees(self, rows):
+        self.r = (self._r0, self._r0 + rows)
+        return self.deg[self.r[0]:self.r[1]].astype(np.int32), self.degu[self.r[0]:self.r[1]].astype(np.int32)
+
+    def fill_rows(self, gdeg, want):
+        off = np.concatenate([[0], np.cumsum(np.asarray(gdeg, dtype=np.int64))])
+        lo, hi = int(off[self.r[0]]), int(off[self.r[1]])
+        return lo, hi, (self.csr.neighbors[lo:hi].copy() if want else None)
+
+
+def _worker(rank, world, port, name, budget, two_phase, q, native=False):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from conftest import GoldenCase
+        from test_distributed import OracleEngine
+        from paper_2401_06713_b200 import distributed as dmod
+        from paper_2401_06713_b200.errors import EdgeBudgetExceededError
+        import json
+
+        with open(os.path.join(ROOT, "tests", "golden", "reference.json")) as f:
+            meta = next(m for m in json.load(f)["cases"] if m["name"] == name)
+        arrays = dict(np.load(os.path.join(ROOT, "tests", "golden", "builds_small.npz")))
+        case = GoldenCase(meta, arrays)
+        if native:
+            eng = dmod.NativeEngine(0)
+        else:
+            eng = OracleEngine()
+            eng._r0 = dmod.row_ranges(case.view.n_active, world)[rank][0]
+        try:
+            gc = dmod.build_sharded(case.view, case.lists, engine=eng, edge_budget=budget,
+                                    two_phase=two_phase)
+            case.check(gc)
+            q.put((rank, "ok", None))
+        except EdgeBudgetExceededError as e:
+            q.put((rank, "budget", e.projected))
+    except Exception as e:  # report, don't hang the other ranks
+        q.put((rank, "error", repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, name, budget=None, two_phase=True, native=False):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, budget, two_phase, q, native))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    return sorted(out)
+
+
+@pytest.mark.parametrize("world,name", [(2, "tc_all_modes_pauli"), (2, "ragged_lists"),
+                                        (3, "induced_subset"), (3, "two_vertices")])
+def test_sharded_build_matches_golden(world, name):
+    res = _run(world, name)
+    assert [r[1] for r in res] == ["ok"] * world, res
+
+
+def test_sharded_budget_error_on_every_rank(golden_ref):
+    meta = next(m for m in golden_ref["cases"] if m["name"] == "tc_determinism")
+    res = _run(2, "tc_determinism", budget=meta["edge_count"] - 1)
+    assert [r[1] for r in res] == ["budget", "budget"]
+    assert res[0][2] == res[1][2] == meta["edge_count"]
+
+
+def test_row_ranges_cover_rows():
+    from paper_2401_06713_b200.distributed import row_ranges
+
+    for n, w in ((0, 2), (1, 3), (10, 3), (1_000_003, 8)):
+        rr = row_ranges(n, w)
+        assert rr[0][0] == 0 and rr[-1][1] == n
+        assert all(a[1] == b[0] for a, b in zip(rr, rr[1:]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,name", [(2, "c1_iter1"), (3, "induced_subset"), (2, "ragged_lists")])
+def test_sharded_native_engine_on_one_gpu(world, name):
+    """Each rank runs the CUDA K1 tile shard + K2 row shard + sharded fill (all ranks share
+    cuda:0); the gathered CSR must equal the reference."""
+    res = _run(world, name, native=True)
+    assert [r[1] for r in res] == ["ok"] * world, res
