@@ -5,6 +5,8 @@
 // the budget, then fill (compaction + K2 fill) straight into the caller's buffers.
 #include <cub/cub.cuh>
 
+#include <omp.h>
+
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -152,6 +154,8 @@ int pcg_destroy(pcg_ctx *ctx) {
     for (DevBuf *b : bufs) release(*b);
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
+    for (auto &h : ctx->stage)
+        if (h) cudaFreeHost(h);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
     return PCG_OK;
@@ -707,6 +711,51 @@ static int prefix_structures(pcg_ctx *ctx, const int32_t *deg, int64_t *n_member
 }
 
 
+
+// Device -> pageable host copy of a large result: double-buffered pinned staging chunks, the
+// DMA of chunk k overlapping the (OpenMP-parallel) host copy of chunk k-1.  A plain
+// cudaMemcpy into pageable memory runs at a fraction of PCIe bandwidth.
+static int d2h_pipelined(pcg_ctx *ctx, void *dst, const void *src, size_t bytes) {
+    cudaStream_t s = ctx->stream;
+    const size_t CH = 32ull << 20;
+    if (bytes <= CH) {
+        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+        PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+        return PCG_OK;
+    }
+    for (int k = 0; k < 2; ++k)
+        if (!ctx->stage[k]) PCG_TRY_CUDA(ctx, cudaHostAlloc(&ctx->stage[k], CH, cudaHostAllocDefault));
+    const size_t nch = (bytes + CH - 1) / CH;
+    auto issue = [&](size_t k) -> cudaError_t {
+        const size_t off = k * CH, len = std::min(CH, bytes - off);
+        cudaError_t e = cudaMemcpyAsync(ctx->stage[k & 1], static_cast<const char *>(src) + off,
+                                        len, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaEventRecord(ctx->ev[6 + (k & 1)], s);
+        return e;
+    };
+    auto drain = [&](size_t k) -> cudaError_t {
+        cudaError_t e = cudaEventSynchronize(ctx->ev[6 + (k & 1)]);
+        if (e != cudaSuccess) return e;
+        const size_t off = k * CH, len = std::min(CH, bytes - off);
+        const char *from = static_cast<const char *>(ctx->stage[k & 1]);
+        char *to = static_cast<char *>(dst) + off;
+        const int parts = 16;
+#pragma omp parallel for num_threads(std::min(16, omp_get_num_procs())) schedule(static)
+        for (int t = 0; t < parts; ++t) {
+            const size_t a = len * t / parts, b = len * (t + 1) / parts;
+            std::memcpy(to + a, from + a, b - a);
+        }
+        return cudaSuccess;
+    };
+    PCG_TRY_CUDA(ctx, issue(0));
+    for (size_t k = 1; k < nch; ++k) {
+        PCG_TRY_CUDA(ctx, issue(k));
+        PCG_TRY_CUDA(ctx, drain(k - 1));
+    }
+    PCG_TRY_CUDA(ctx, drain(nch - 1));
+    return PCG_OK;
+}
+
 // Fill pass for rows [r0, r1) into `out` (int64, entry index out_base at out[0]).  Owned
 // masks: warp merge of the disjoint runs, rows longer than the merge buffer go through the
 // bitmap row kernel; otherwise the bitmap row kernel for every row.
@@ -801,11 +850,12 @@ static int fill_impl(pcg_ctx *ctx, bool to_host, int64_t *members, int64_t *offs
         if (offsets)
             PCG_TRY_CUDA(ctx, cudaMemcpyAsync(offsets, ctx->offsets_o.p, (nm + 1) * 8,
                                               cudaMemcpyDeviceToHost, s));
-        if (nnz > 0 && neighbors)
-            PCG_TRY_CUDA(ctx, cudaMemcpyAsync(neighbors, ctx->nbr_o.p, nnz * 8,
-                                              cudaMemcpyDeviceToHost, s));
     }
     PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+    if (to_host && nnz > 0 && neighbors) {
+        rc = d2h_pipelined(ctx, neighbors, ctx->nbr_o.p, (size_t)nnz * 8);
+        if (rc) return rc;
+    }
     if (ctx->prof) {
         cudaEventElapsedTime(&ctx->ktimes[3], ctx->ev[3], ctx->ev[4]);
         cudaEventElapsedTime(&ctx->ktimes[2], ctx->ev[4], ctx->ev[5]);
@@ -883,9 +933,8 @@ extern "C" int pcg_fill_rows(pcg_ctx *ctx, const int32_t *global_deg, int64_t *n
     rc = fill_rows_device(ctx, r0, r1, ctx->gdeg.as<int32_t>(), gmax, nm == n, ctx->nbr_o.p,
                           lohi[0], &l);
     if (rc) return rc;
-    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(neighbors, ctx->nbr_o.p, cnt * 8, cudaMemcpyDeviceToHost, s));
     PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
-    return PCG_OK;
+    return d2h_pipelined(ctx, neighbors, ctx->nbr_o.p, (size_t)cnt * 8);
 }
 
 // Device-pointer variants for the sharded build (NCCL collectives operate on the caller's

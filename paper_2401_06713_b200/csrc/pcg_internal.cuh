@@ -156,6 +156,7 @@ struct pcg_ctx {
     bool prof = false;
     cudaEvent_t ev[12] = {};
     float ktimes[5] = {0, 0, 0, 0, 0};
+    void *stage[2] = {nullptr, nullptr};  // pinned D2H staging (32 MiB each)
 
     // device buffers
     pcg::DevBuf words, active, lists64, loff, A, B, H, lrel, rowof, keys2, vals2, bstart,
