@@ -278,7 +278,8 @@ def bench_gpu(args) -> None:
     hbm = peaks.get("hbm_gbs", 6650.0)
     fill_ms = float(kt[2])
     words_b = n * view.backing.words.shape[1] * 8
-    fill_bytes = (2 * edges) * 8 + (members + 1) * 8 + members * 8 + n * plan.list_size * 4 + words_b
+    # device CSR ids are int32 (widened to the API's int64 on the host during the D2H copy)
+    fill_bytes = (2 * edges) * 4 + (members + 1) * 8 + members * 8 + n * plan.list_size * 4 + words_b
     achieved = fill_bytes / (fill_ms * 1e-3) / 1e9
     # the commuting-pair sweep against the survey's POPC-issue bound (1 POPC / pair / clk)
     sm_mhz = (clocks.summary().get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0))

@@ -756,12 +756,51 @@ static int d2h_pipelined(pcg_ctx *ctx, void *dst, const void *src, size_t bytes)
     return PCG_OK;
 }
 
+// Same pipeline, int32 device ids widened to the API's int64 during the host-side copy, so
+// only half the bytes cross PCIe.
+static int d2h_widen(pcg_ctx *ctx, int64_t *dst, const int32_t *src, size_t count) {
+    cudaStream_t s = ctx->stream;
+    const size_t CH = 8ull << 20;  // ids per chunk (32 MiB of int32)
+    for (int k = 0; k < 2; ++k)
+        if (!ctx->stage[k]) PCG_TRY_CUDA(ctx, cudaHostAlloc(&ctx->stage[k], 32ull << 20, cudaHostAllocDefault));
+    const size_t nch = (count + CH - 1) / CH;
+    if (nch == 0) return PCG_OK;
+    auto issue = [&](size_t k) -> cudaError_t {
+        const size_t off = k * CH, len = std::min(CH, count - off);
+        cudaError_t e = cudaMemcpyAsync(ctx->stage[k & 1], src + off, len * 4,
+                                        cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaEventRecord(ctx->ev[6 + (k & 1)], s);
+        return e;
+    };
+    auto drain = [&](size_t k) -> cudaError_t {
+        cudaError_t e = cudaEventSynchronize(ctx->ev[6 + (k & 1)]);
+        if (e != cudaSuccess) return e;
+        const size_t off = k * CH, len = std::min(CH, count - off);
+        const int32_t *from = static_cast<const int32_t *>(ctx->stage[k & 1]);
+        int64_t *to = dst + off;
+        const int parts = 16;
+#pragma omp parallel for num_threads(std::min(16, omp_get_num_procs())) schedule(static)
+        for (int t = 0; t < parts; ++t) {
+            const size_t a = len * t / parts, b = len * (t + 1) / parts;
+            for (size_t x = a; x < b; ++x) to[x] = from[x];
+        }
+        return cudaSuccess;
+    };
+    PCG_TRY_CUDA(ctx, issue(0));
+    for (size_t k = 1; k < nch; ++k) {
+        PCG_TRY_CUDA(ctx, issue(k));
+        PCG_TRY_CUDA(ctx, drain(k - 1));
+    }
+    PCG_TRY_CUDA(ctx, drain(nch - 1));
+    return PCG_OK;
+}
+
 // Fill pass for rows [r0, r1) into `out` (int64, entry index out_base at out[0]).  Owned
 // masks: warp merge of the disjoint runs, rows longer than the merge buffer go through the
 // bitmap row kernel; otherwise the bitmap row kernel for every row.
 static int fill_rows_device(pcg_ctx *ctx, int64_t r0, int64_t r1, const int32_t *deg,
                             int32_t maxdeg, bool identity, void *out, int64_t out_base,
-                            int *launches) {
+                            int *launches, bool out64 = true) {
     cudaStream_t s = ctx->stream;
     RowArgs a = row_args(ctx, r0, r1);
     a.deg = const_cast<int32_t *>(deg);
@@ -770,18 +809,18 @@ static int fill_rows_device(pcg_ctx *ctx, int64_t r0, int64_t r1, const int32_t 
     a.out = out;
     a.out_base = out_base;
     if (!ctx->owned) {
-        *launches += launch_rows(a, true, true, ctx->sms, s);
+        *launches += launch_rows(a, true, out64, ctx->sms, s);
         PCG_CHECK_LAUNCH(ctx);
         return PCG_OK;
     }
     if (ctx->fill_algo == 1) {  // cooperative bitmap fill (experimental)
         a.window = coop_window(ctx);
-        *launches += launch_fill_coop(a, true, ctx->sms, s);
+        *launches += launch_fill_coop(a, out64, ctx->sms, s);
         PCG_CHECK_LAUNCH(ctx);
         return PCG_OK;
     }
     if (ctx->fill_algo != 2) {  // lane-per-bucket bitmap fill (default)
-        *launches += launch_rows(a, true, true, ctx->sms, s);
+        *launches += launch_rows(a, true, out64, ctx->sms, s);
         PCG_CHECK_LAUNCH(ctx);
         return PCG_OK;
     }
@@ -792,7 +831,7 @@ static int fill_rows_device(pcg_ctx *ctx, int64_t r0, int64_t r1, const int32_t 
     g.heavy = ctx->heavy.as<int32_t>();
     g.nheavy = reinterpret_cast<int32_t *>(ctx->scal.as<unsigned long long>() + 6);
     PCG_TRY_CUDA(ctx, cudaMemsetAsync(g.nheavy, 0, 4, s));
-    *launches += launch_fill_merge(a, g, true, ctx->sms, s);
+    *launches += launch_fill_merge(a, g, out64, ctx->sms, s);
     PCG_CHECK_LAUNCH(ctx);
     if (maxdeg > g.cap) {
         int32_t nh = 0;
@@ -803,7 +842,7 @@ static int fill_rows_device(pcg_ctx *ctx, int64_t r0, int64_t r1, const int32_t 
             h.rows_list = g.heavy;
             h.row_begin = 0;
             h.row_end = nh;
-            *launches += launch_rows(h, true, true, ctx->sms, s);
+            *launches += launch_rows(h, true, out64, ctx->sms, s);
             PCG_CHECK_LAUNCH(ctx);
         }
     }
@@ -830,7 +869,7 @@ static int fill_impl(pcg_ctx *ctx, bool to_host, int64_t *members, int64_t *offs
     if (nm2 != nm) return fail(ctx, PCG_E_STATE, "member count mismatch");
     PCG_ALLOC(ctx, ctx->members_o, (size_t)std::max<int64_t>(nm, 1) * 8);
     PCG_ALLOC(ctx, ctx->offsets_o, (size_t)(nm + 1) * 8);
-    PCG_ALLOC(ctx, ctx->nbr_o, (size_t)std::max<int64_t>(nnz, 1) * 8);
+    PCG_ALLOC(ctx, ctx->nbr_o, (size_t)std::max<int64_t>(nnz, 1) * 4);
     *launches += launch_compact(ctx->deg.as<int32_t>(), n,
                                 nm == n ? nullptr : ctx->compact.as<int32_t>(),
                                 ctx->rowoff.as<int64_t>(), ctx->active.as<int64_t>(),
@@ -839,7 +878,7 @@ static int fill_impl(pcg_ctx *ctx, bool to_host, int64_t *members, int64_t *offs
     if (ctx->prof) cudaEventRecord(ctx->ev[4], s);
     if (nnz > 0) {
         rc = fill_rows_device(ctx, 0, n, ctx->deg.as<int32_t>(), ctx->maxdeg, nm == n,
-                              ctx->nbr_o.p, 0, launches);
+                              ctx->nbr_o.p, 0, launches, /*out64=*/false);
         if (rc) return rc;
     }
     if (ctx->prof) cudaEventRecord(ctx->ev[5], s);
@@ -853,7 +892,7 @@ static int fill_impl(pcg_ctx *ctx, bool to_host, int64_t *members, int64_t *offs
     }
     PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
     if (to_host && nnz > 0 && neighbors) {
-        rc = d2h_pipelined(ctx, neighbors, ctx->nbr_o.p, (size_t)nnz * 8);
+        rc = d2h_widen(ctx, neighbors, ctx->nbr_o.as<int32_t>(), (size_t)nnz);
         if (rc) return rc;
     }
     if (ctx->prof) {
