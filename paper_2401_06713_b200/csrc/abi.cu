@@ -150,7 +150,8 @@ int pcg_destroy(pcg_ctx *ctx) {
                       &ctx->cubtmp, &ctx->deg, &ctx->degu, &ctx->compact, &ctx->rowoff,
                       &ctx->scal, &ctx->bad, &ctx->members_o, &ctx->offsets_o, &ctx->nbr_o,
                       &ctx->gdeg, &ctx->items, &ctx->eidx, &ctx->bpos, &ctx->bmemp,
-                      &ctx->posof, &ctx->maskoff, &ctx->masks};
+                      &ctx->posof, &ctx->maskoff, &ctx->masks, &ctx->heavy, &ctx->runlen,
+                      &ctx->runoff, &ctx->runs};
     for (DevBuf *b : bufs) release(*b);
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
@@ -226,6 +227,13 @@ struct MaskWords {
         if (c >= P) return 0;
         const int64_t m = bstart[c + 1] - bstart[c];
         return m * ((m + 31) / 32);
+    }
+};
+struct PaddedRun {
+    const int32_t *len;
+    int64_t n;
+    __host__ __device__ int64_t operator()(int64_t e) const {
+        return e < n ? (int64_t)((len[e] + 3) & ~3) : 0;
     }
 };
 __global__ void k_bucket_max(const int32_t *bstart, int64_t P, int32_t *out) {
@@ -365,12 +373,40 @@ static int prep_device(pcg_ctx *ctx) {
             o.hash_slots = hs;
             o.m_cap = m_max;
             PCG_TRY_CUDA(ctx, cudaMemsetAsync(o.overflow, 0, 4, s));
+            PCG_ALLOC(ctx, ctx->runlen, (size_t)entries * 4);
+            PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->runlen.p, 0, (size_t)entries * 4, s));
+            b.runlen = ctx->runlen.as<int32_t>();
             launch_owned_masks(b, o, ctx->sms, s);
             PCG_CHECK_LAUNCH(ctx);
+            // owned partner runs (padded to 4 ids) for the TMA-staged fill
+            PCG_ALLOC(ctx, ctx->runoff, (size_t)(entries + 1) * 8);
+            cub::TransformInputIterator<int64_t, PaddedRun, cub::CountingInputIterator<int64_t>> plen(
+                cidx, PaddedRun{ctx->runlen.as<int32_t>(), entries});
+            size_t t3 = 0;
+            PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, t3, plen,
+                                                            ctx->runoff.as<int64_t>(), entries + 1, s));
+            PCG_ALLOC(ctx, ctx->cubtmp, t3);
+            PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->cubtmp.p, t3, plen,
+                                                            ctx->runoff.as<int64_t>(), entries + 1, s));
             int32_t ovf = 0;
+            int64_t runs_total = 0;
             PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&ovf, o.overflow, 4, cudaMemcpyDeviceToHost, s));
+            PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&runs_total, ctx->runoff.as<int64_t>() + entries, 8,
+                                              cudaMemcpyDeviceToHost, s));
             PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
             if (ovf) ctx->owned = false;  // a color's ownership table overflowed: dedupe path
+            ctx->runs_ready = false;
+            if (ctx->owned && ctx->fill_algo == 4 &&
+                (size_t)runs_total * 4 < free_b / 3) {
+                PCG_ALLOC(ctx, ctx->runs, (size_t)(runs_total + 4) * 4);
+                RunArgs ra{};
+                ra.runlen = ctx->runlen.as<int32_t>();
+                ra.runoff = ctx->runoff.as<int64_t>();
+                ra.runs = ctx->runs.as<int32_t>();
+                launch_write_runs(b, ra, ctx->sms, s);
+                PCG_CHECK_LAUNCH(ctx);
+                ctx->runs_ready = true;
+            }
         }
         if (!ctx->owned) {
             launch_bucket_masks(b, ctx->sms, s);
@@ -811,6 +847,34 @@ static int fill_rows_device(pcg_ctx *ctx, int64_t r0, int64_t r1, const int32_t 
     if (!ctx->owned) {
         *launches += launch_rows(a, true, out64, ctx->sms, s);
         PCG_CHECK_LAUNCH(ctx);
+        return PCG_OK;
+    }
+    if (ctx->runs_ready) {  // TMA-staged owned runs (default)
+        RunArgs r{};
+        r.runlen = ctx->runlen.as<int32_t>();
+        r.runoff = ctx->runoff.as<int64_t>();
+        r.runs = ctx->runs.as<int32_t>();
+        const int capmax = ctx->merge_cap > 0 ? ctx->merge_cap : 4096;
+        r.cap = std::min(capmax, (maxdeg + 3 * ctx->lmax + 31) & ~31);
+        PCG_ALLOC(ctx, ctx->heavy, (size_t)std::max<int64_t>(r1 - r0, 1) * 4);
+        r.heavy = ctx->heavy.as<int32_t>();
+        r.nheavy = reinterpret_cast<int32_t *>(ctx->scal.as<unsigned long long>() + 6);
+        PCG_TRY_CUDA(ctx, cudaMemsetAsync(r.nheavy, 0, 4, s));
+        RowArgs fa = a;
+        fa.window = 16384;
+        *launches += launch_fill_runs(fa, r, out64, ctx->sms, s);
+        PCG_CHECK_LAUNCH(ctx);
+        int32_t nh = 0;
+        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&nh, r.nheavy, 4, cudaMemcpyDeviceToHost, s));
+        PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+        if (nh > 0) {
+            RowArgs h = a;
+            h.rows_list = r.heavy;
+            h.row_begin = 0;
+            h.row_end = nh;
+            *launches += launch_rows(h, true, out64, ctx->sms, s);
+            PCG_CHECK_LAUNCH(ctx);
+        }
         return PCG_OK;
     }
     if (ctx->fill_algo == 1) {  // cooperative bitmap fill (experimental)

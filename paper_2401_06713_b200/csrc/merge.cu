@@ -19,8 +19,8 @@ namespace pcg {
 
 namespace {
 
-constexpr int OWN_THREADS = 128;
-constexpr int OWN_COLL = 4096;        // collision list capacity
+constexpr int OWN_THREADS = 256;
+constexpr int OWN_COLL = 2048;        // collision list capacity
 constexpr int MERGE_WARPS = 4;
 
 template <int KW>
@@ -66,16 +66,16 @@ template <int KW>
 __global__ void __launch_bounds__(OWN_THREADS) k_owned_masks(BucketArgs b, OwnArgs o) {
     extern __shared__ __align__(16) uint32_t osm[];
     const int HS = o.hash_slots;
-    uint32_t *table = osm;                                   // HS: (c'+1)<<12 | first k
-    int32_t *head = reinterpret_cast<int32_t *>(osm + HS);   // HS: last collision + 1 per slot
-    uint32_t *coll = osm + 2 * HS;                           // OWN_COLL: slot<<12 | k
-    int32_t *link = reinterpret_cast<int32_t *>(coll + OWN_COLL);  // OWN_COLL: previous in slot
-    int32_t *sid = link + OWN_COLL;                          // member ids (m_cap)
+    uint32_t *table = osm;                                        // HS: (c'+1)<<12 | first k
+    unsigned short *head = reinterpret_cast<unsigned short *>(osm + HS);  // HS: last coll + 1
+    uint32_t *coll = osm + HS + HS / 2;                           // OWN_COLL: slot<<12 | k
+    int32_t *link = reinterpret_cast<int32_t *>(coll + OWN_COLL); // OWN_COLL: previous in slot
+    int32_t *sid = link + OWN_COLL;                               // member ids (m_cap)
     uint32_t *sB = reinterpret_cast<uint32_t *>(sid + o.m_cap);   // partner vectors (m_cap * kw)
     __shared__ int ncoll, overflow;
     const int tid = threadIdx.x;
     const int kw = b.kw;
-    for (int x = tid; x < 2 * HS; x += OWN_THREADS) osm[x] = 0u;
+    for (int x = tid; x < HS + HS / 2; x += OWN_THREADS) osm[x] = 0u;
     for (int64_t c = blockIdx.x; c < b.P; c += gridDim.x) {
         const int m = b.bstart[c + 1] - b.bstart[c];
         if (m < 2) {
@@ -139,7 +139,16 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_masks(BucketArgs b, OwnAr
                         const int q = atomicAdd(&ncoll, 1);
                         if (q < OWN_COLL) {
                             coll[q] = (slot << 12) | (uint32_t)k;
-                            link[q] = atomicExch(&head[slot], q + 1) - 1;
+                            // 16-bit chain head: swap through the containing 32-bit word
+                            uint32_t *hw = reinterpret_cast<uint32_t *>(head) + (slot >> 1);
+                            const int sh = (slot & 1) * 16;
+                            uint32_t old = *hw, assumed;
+                            do {
+                                assumed = old;
+                                const uint32_t nv = (assumed & ~(0xffffu << sh)) | ((uint32_t)(q + 1) << sh);
+                                old = atomicCAS(hw, assumed, nv);
+                            } while (old != assumed);
+                            link[q] = (int)((old >> sh) & 0xffffu) - 1;
                         } else {
                             overflow = 1;
                         }
@@ -166,10 +175,17 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_masks(BucketArgs b, OwnAr
             }
         }
         __syncthreads();
+        if (b.runlen) {  // owned partners per member: the run lengths of the fill pass
+            for (int k = tid; k < m; k += OWN_THREADS) {
+                int cnt = 0;
+                for (int w = 0; w < W; ++w) cnt += __popc(out[(int64_t)k * W + w]);
+                b.runlen[b.bstart[c] + k] = cnt;
+            }
+        }
         // reset the table and the chain heads this color touched
         for (int x = 4 * tid; x < HS; x += 4 * OWN_THREADS)
             *reinterpret_cast<uint4 *>(table + x) = make_uint4(0u, 0u, 0u, 0u);
-        for (int q = tid; q < nc; q += OWN_THREADS) head[coll[q] >> 12] = 0;
+        for (int q = tid; q < nc; q += OWN_THREADS) head[coll[q] >> 12] = 0;  // (16-bit store)
         __syncthreads();
     }
 }
@@ -341,6 +357,7 @@ __global__ void __launch_bounds__(MERGE_WARPS * 32) k_fill_merge(RowArgs a, Merg
 constexpr int COOP_WARPS = 8;
 constexpr int COOP_BATCH = 8;   // 32-member chunks per load batch
 constexpr int COOP_STAGE = 1024;
+constexpr int UNR_F = 8;    // run elements per lane per round (runs fill)
 
 __device__ __forceinline__ uint32_t c_lds(uint32_t addr) {
     uint32_t v;
@@ -521,10 +538,269 @@ int run_coop(const RowArgs &a, int sms, cudaStream_t s) {
     return 1;
 }
 
+
+// ---------------------------------------------------------------------------------------
+// Owned partner runs: for every bucket entry (color c, member k) the ascending ids of its
+// owned admitted partners, at a 16-byte aligned offset (TMA bulk copies need it).  Warp per
+// color; 32 bucket positions per step, ballot-compacted, coalesced stores.
+// ---------------------------------------------------------------------------------------
+constexpr int RUN_WARPS = 8;
+
+__global__ void __launch_bounds__(RUN_WARPS * 32) k_write_runs(BucketArgs b, RunArgs r) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = blockIdx.x * (int64_t)RUN_WARPS + (threadIdx.x >> 5);
+    const int64_t nw = (int64_t)gridDim.x * RUN_WARPS;
+    for (int64_t c = gw; c < b.P; c += nw) {
+        const int m = b.bstart[c + 1] - b.bstart[c];
+        if (m < 2) continue;
+        const int W = (m + 31) >> 5;
+        const int32_t *mem = b.bmemp + b.bpos[c];
+        const uint32_t *mk = b.masks + b.maskoff[c];
+        for (int k = 0; k < m; ++k) {
+            const int64_t pos = b.bstart[c] + k;
+            int32_t *dst = r.runs + r.runoff[pos];
+            int cnt = 0;
+            for (int w = 0; w < W; ++w) {
+                const uint32_t word = __ldg(mk + (int64_t)k * W + w);  // broadcast
+                if (word == 0u) continue;
+                const int t = 32 * w + lane;
+                const bool keep = (word >> lane) & 1u;
+                const int32_t id = keep ? __ldg(mem + t) : 0;
+                if (keep) dst[cnt + __popc(word & ((1u << lane) - 1u))] = id;
+                cnt += __popc(word);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Fill from owned runs (warp per row).  Lanes s < L issue one TMA bulk copy each (their
+// run) into the warp's shared staging buffer, completing on an mbarrier; the next row is
+// staged into the other buffer while this one is sorted.  Lanes then walk their run in
+// shared memory and mark partners in the window bitmap; the interleaved harvest emits the
+// row in ascending order (runs are disjoint: no dedupe needed).
+// ---------------------------------------------------------------------------------------
+constexpr int FR_W = 4;  // warps per block
+
+__device__ __forceinline__ void mbar_init(uint32_t mbar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint32_t mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "\t@!p bra W%=;\n\t}" ::"r"(mbar),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(mbar)
+        : "memory");
+}
+
+struct RowStage {
+    int off, len;     // this lane's run inside the buffer (ids)
+    int deg;          // row total (warp-uniform)
+};
+
+// Issue the TMA copies of row i into buffer `buf_s` (shared byte address).  Returns the
+// lane's run geometry.  deg == -1 marks a row too long for the buffer.
+__device__ __forceinline__ RowStage stage_row(const RowArgs &a, const RunArgs &r, int64_t i,
+                                              uint32_t buf_s, uint32_t mbar, int lane) {
+    RowStage g{0, 0, 0};
+    const int64_t lo = a.loff ? a.loff[i] : i * a.L;
+    const int Li = (int)((a.loff ? a.loff[i + 1] : lo + a.L) - lo);
+    int64_t src = 0;
+    int len = 0;
+    if (lane < Li) {
+        const int c = a.lrel[lo + lane];
+        const int64_t pos = a.bstart[c] + a.posof[lo + lane];
+        len = r.runlen[pos];
+        src = r.runoff[pos];
+    }
+    const int padded = (len + 3) & ~3;
+    int total;
+    int x = padded;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    total = __shfl_sync(0xffffffffu, x, 31);
+    const int off = x - padded;
+    g.off = off;
+    g.len = len;
+    g.deg = total > r.cap ? -1 : total;
+    if (g.deg > 0) {
+        if (lane == 0) mbar_expect(mbar, (uint32_t)total * 4u);
+        __syncwarp();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (padded > 0) tma_load(buf_s + (uint32_t)off * 4u, r.runs + src, (uint32_t)padded * 4u, mbar);
+    }
+    return g;
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(FR_W * 32) k_fill_runs(RowArgs a, RunArgs r) {
+    extern __shared__ __align__(16) uint32_t fsm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int WW = a.window >> 5;
+    const size_t per_warp = (size_t)2 * r.cap + WW + 32 + COOP_STAGE + 4;
+    uint32_t *base = fsm + (size_t)warp * per_warp;
+    int32_t *buf0 = reinterpret_cast<int32_t *>(base);
+    uint32_t *bm = base + 2 * r.cap;
+    int32_t *stage = reinterpret_cast<int32_t *>(bm + WW + 32);
+    uint64_t *mb = reinterpret_cast<uint64_t *>(stage + COOP_STAGE);
+    const uint32_t bufs_s = (uint32_t)__cvta_generic_to_shared(buf0);
+    const uint32_t bm_s = (uint32_t)__cvta_generic_to_shared(bm);
+    const uint32_t dummy_s = bm_s + (uint32_t)(WW + lane) * 4u;
+    const uint32_t mb_s = (uint32_t)__cvta_generic_to_shared(mb);
+    for (int k = lane; k < WW; k += 32) bm[k] = 0u;
+    if (lane == 0) {
+        mbar_init(mb_s);
+        mbar_init(mb_s + 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    OutT *out = reinterpret_cast<OutT *>(a.out);
+    const int64_t stride = (int64_t)gridDim.x * FR_W;
+    int64_t ri = a.row_begin + (int64_t)blockIdx.x * FR_W + warp;
+    uint32_t phase[2] = {0u, 0u};
+    int b = 0;
+    RowStage cur{0, 0, 0};
+    if (ri < a.row_end) cur = stage_row(a, r, ri, bufs_s, mb_s, lane);
+    for (; ri < a.row_end; ri += stride) {
+        const int64_t i = ri;
+        // prefetch the next row into the other buffer
+        RowStage nxt{0, 0, 0};
+        const int64_t rn = ri + stride;
+        if (rn < a.row_end)
+            nxt = stage_row(a, r, rn, bufs_s + (uint32_t)((b ^ 1) * r.cap) * 4u, mb_s + 8 * (b ^ 1), lane);
+        if (cur.deg < 0) {  // too long for the staging buffer: bitmap fallback pass
+            if (lane == 0) r.heavy[atomicAdd(r.nheavy, 1)] = (int32_t)i;
+        } else if (cur.deg > 0) {
+            mbar_wait(mb_s + 8 * b, phase[b]);
+            phase[b] ^= 1u;
+            const int32_t *buf = buf0 + b * r.cap;
+            int t = 0;
+            int64_t outpos = a.rowoff[i] - a.out_base;
+            for (int32_t w0 = 0; w0 < a.n; w0 += a.window) {
+                const int32_t w1 = (int32_t)min((int64_t)a.n, (int64_t)w0 + a.window);
+                bool go = t < cur.len;
+                while (__any_sync(0xffffffffu, go)) {
+                    uint32_t addr[UNR_F], bit[UNR_F];
+                    int k = 0;
+#pragma unroll
+                    for (int u = 0; u < UNR_F; ++u) {
+                        const int32_t v = (go && t + u < cur.len) ? buf[cur.off + t + u] : INT_MAX;
+                        const bool in = v < w1;
+                        k += in ? 1 : 0;
+                        const uint32_t off = (uint32_t)(v - w0);
+                        addr[u] = in ? bm_s + ((off >> 5) << 2) : dummy_s;
+                        bit[u] = in ? (1u << (off & 31)) : 0u;
+                    }
+                    t += k;
+                    go = go && k == UNR_F && t < cur.len;
+                    // mark (plain RMW + verify; atomics only for lost bits)
+                    uint32_t old[UNR_F];
+#pragma unroll
+                    for (int u = 0; u < UNR_F; ++u) old[u] = bit[u] ? c_lds(addr[u]) : 0u;
+#pragma unroll
+                    for (int u = 0; u < UNR_F; ++u)
+                        if (bit[u]) c_sts(addr[u], old[u] | bit[u]);
+                    __syncwarp();
+                    uint32_t lost = 0u;
+#pragma unroll
+                    for (int u = 0; u < UNR_F; ++u) {
+                        old[u] = bit[u] ? (bit[u] & ~c_lds(addr[u])) : 0u;
+                        lost |= old[u];
+                    }
+                    if (__any_sync(0xffffffffu, lost != 0u)) {
+#pragma unroll
+                        for (int u = 0; u < UNR_F; ++u)
+                            if (old[u])
+                                atomicOr(reinterpret_cast<uint32_t *>(__cvta_shared_to_generic(addr[u])), old[u]);
+                    }
+                    __syncwarp();
+                }
+                // harvest: interleaved chunks, staged, coalesced stores
+                const int rows = WW >> 7;
+                int fillv = 0;
+                for (int it = 0; it < rows; ++it) {
+                    const int cc = it * 32 + lane;
+                    const uint32_t ad = bm_s + (uint32_t)cc * 16u;
+                    const uint4 q4 = c_lds4(ad);
+                    const int nb = __popc(q4.x) + __popc(q4.y) + __popc(q4.z) + __popc(q4.w);
+                    int total;
+                    const int bse = c_scan(nb, lane, total);
+                    if (total == 0) continue;
+                    const bool direct = total > COOP_STAGE;
+                    if (fillv > 0 && (direct || fillv + total > COOP_STAGE)) {
+                        __syncwarp();
+                        for (int q = lane; q < fillv; q += 32) out[outpos + q] = (OutT)stage[q];
+                        outpos += fillv;
+                        fillv = 0;
+                        __syncwarp();
+                    }
+                    if (nb) {
+                        c_sts4(ad, make_uint4(0u, 0u, 0u, 0u));
+                        int64_t pos = direct ? outpos + bse : fillv + bse;
+                        const uint32_t wv[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            uint32_t wd = wv[u];
+                            const int32_t jb = w0 + cc * 128 + 32 * u;
+                            while (wd) {
+                                const int bb = __ffs(wd) - 1;
+                                wd &= wd - 1u;
+                                const int32_t j = jb + bb;
+                                const int32_t val = a.compact ? a.compact[j] : j;
+                                if (direct) out[pos++] = (OutT)val;
+                                else stage[pos++] = val;
+                            }
+                        }
+                    }
+                    if (direct) outpos += total;
+                    else fillv += total;
+                }
+                __syncwarp();
+                for (int q = lane; q < fillv; q += 32) out[outpos + q] = (OutT)stage[q];
+                outpos += fillv;
+                __syncwarp();
+                if (!__any_sync(0xffffffffu, t < cur.len)) break;  // row done before n
+            }
+        }
+        __syncwarp();
+        cur = nxt;
+        b ^= 1;
+    }
+}
+
+template <typename OutT>
+int run_fill_runs(const RowArgs &a, const RunArgs &r, int sms, cudaStream_t s) {
+    const size_t per_warp = ((size_t)2 * r.cap + (a.window >> 5) + 32 + COOP_STAGE + 4) * 4;
+    const size_t smem = per_warp * FR_W;
+    cudaFuncSetAttribute(k_fill_runs<OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fill_runs<OutT>, FR_W * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t rows = a.row_end - a.row_begin;
+    const int64_t grid = std::max<int64_t>(
+        1, std::min<int64_t>((int64_t)per_sm * sms, (rows + FR_W - 1) / FR_W));
+    k_fill_runs<OutT><<<(unsigned)grid, FR_W * 32, smem, s>>>(a, r);
+    return 1;
+}
+
 template <int KW>
 int run_owned(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s) {
     int per_sm = 0;
-    const size_t smem = (size_t)(2 * o.hash_slots + 2 * OWN_COLL + o.m_cap + o.m_cap * b.kw) * 4;
+    const size_t smem = (size_t)(o.hash_slots + o.hash_slots / 2 + 2 * OWN_COLL + o.m_cap + o.m_cap * b.kw) * 4;
     cudaFuncSetAttribute(k_owned_masks<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_owned_masks<KW>, OWN_THREADS, smem);
     if (per_sm < 1) per_sm = 1;
@@ -574,6 +850,18 @@ int launch_fill_merge(const RowArgs &a, const MergeArgs &g, bool out64, int sms,
 }
 
 int merge_smem_bytes(int cap) { return MERGE_WARPS * (2 * cap + 68) * 4; }
+
+int launch_write_runs(const BucketArgs &b, const RunArgs &r, int sms, cudaStream_t s) {
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((b.P + RUN_WARPS - 1) / RUN_WARPS,
+                                                                (int64_t)sms * 8));
+    k_write_runs<<<(unsigned)grid, RUN_WARPS * 32, 0, s>>>(b, r);
+    return 1;
+}
+
+int launch_fill_runs(const RowArgs &a, const RunArgs &r, bool out64, int sms, cudaStream_t s) {
+    if (a.row_end <= a.row_begin) return 0;
+    return out64 ? run_fill_runs<int64_t>(a, r, sms, s) : run_fill_runs<int32_t>(a, r, sms, s);
+}
 
 int launch_fill_coop(const RowArgs &a, bool out64, int sms, cudaStream_t s) {
     if (a.row_end <= a.row_begin) return 0;

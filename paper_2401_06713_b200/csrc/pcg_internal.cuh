@@ -70,6 +70,15 @@ struct OwnArgs {
     int32_t m_cap;         // >= largest bucket
 };
 
+struct RunArgs {
+    const int32_t *runlen;    // owned partners per sorted position (bucket entry)
+    const int64_t *runoff;    // 4-aligned offset of each entry's run in `runs`
+    int32_t *runs;            // out of k_write_runs: ascending partner ids per entry
+    int32_t cap;              // fill: ids per staging buffer (per warp, x2)
+    int32_t *heavy;           // fill: rows whose runs do not fit the staging buffer
+    int32_t *nheavy;
+};
+
 struct MergeArgs {
     int32_t cap;           // ids per warp buffer; longer rows go to the bitmap fill
     int32_t *heavy;        // out: rows longer than cap
@@ -87,6 +96,7 @@ struct BucketArgs {
     int32_t *bmem;            // out: unpadded members (direct mode), may be null
     int32_t *posof;           // out: position of each entry in its bucket
     uint32_t *masks;          // out: commute masks
+    int32_t *runlen;          // out (owned mode): popcount of every mask row, by sorted position
     const uint32_t *A;
     const uint32_t *B;
     int32_t kw;
@@ -117,6 +127,8 @@ int launch_owned_masks(const BucketArgs &b, const OwnArgs &o, int sms, cudaStrea
 int launch_count_owned(const RowArgs &a, int sms, cudaStream_t s);
 int launch_fill_merge(const RowArgs &a, const MergeArgs &g, bool out64, int sms, cudaStream_t s);
 int merge_smem_bytes(int cap);
+int launch_write_runs(const BucketArgs &b, const RunArgs &r, int sms, cudaStream_t s);
+int launch_fill_runs(const RowArgs &a, const RunArgs &r, bool out64, int sms, cudaStream_t s);
 int launch_fill_coop(const RowArgs &a, bool out64, int sms, cudaStream_t s);
 int launch_compact(const int32_t *deg, int64_t n, const int32_t *compact, const int64_t *rowoff,
                    const int64_t *active, int64_t *members_out, int64_t *offsets_out,
@@ -144,7 +156,8 @@ struct pcg_ctx {
     int window = 0;     // K2 window bits (0 auto)
     int fr_ichunk = 0;  // four-Russians i-chunk (0 auto)
     int merge_cap = 0;  // fill-merge buffer cap (0 auto; testing knob)
-    int fill_algo = 0;  // owned masks: 0/3 lane-per-bucket bitmap fill, 1 cooperative bitmap, 2 merge
+    int fill_algo = 0;  // owned masks: 0/3 lane-per-bucket bitmap fill, 1 cooperative bitmap,
+                        // 2 merge, 4 TMA-staged owned runs
     int k2_mode = 0;    // 0 auto, 1 partner gathers, 2 bucket masks + bitmap dedupe, 3 owned masks + merge
 
     // state of the last count
@@ -161,9 +174,10 @@ struct pcg_ctx {
     // device buffers
     pcg::DevBuf words, active, lists64, loff, A, B, H, lrel, rowof, keys2, vals2, bstart,
         cubtmp, deg, degu, compact, rowoff, scal, bad, members_o, offsets_o, nbr_o, gdeg, items,
-        eidx, bpos, bmemp, posof, maskoff, masks, heavy;
+        eidx, bpos, bmemp, posof, maskoff, masks, heavy, runlen, runoff, runs;
     int prep_launches = 0;
     bool masked = false;  // K2 uses bucket masks (K2a/K2b) instead of partner gathers
     bool owned = false;   // masks keep each pair only in its smallest shared color
+    bool runs_ready = false;  // owned partner runs materialised (TMA-staged fill)
     int32_t maxdeg = 0;
 };

@@ -53,6 +53,36 @@ def test_merge_heavy_rows_fallback(golden_cases, cap):
         ctx.option("k2_mode", 0)
 
 
+@pytest.mark.parametrize("fill_algo", [0, 1, 2, 4], ids=["bitmap", "coop", "merge", "runs-tma"])
+def test_owned_fill_variants(golden_cases, fill_algo):
+    ctx = _native.context()
+    ctx.option("k2_mode", 3)
+    ctx.option("fill_algo", fill_algo)
+    try:
+        for case in golden_cases:
+            case.check(b200.build(case.view, case.lists))
+    finally:
+        ctx.option("fill_algo", 0)
+        ctx.option("k2_mode", 0)
+
+
+@pytest.mark.parametrize("cap", [32, 256])
+def test_runs_fill_heavy_rows(golden_cases, golden_ref, cap):
+    """Rows whose runs exceed the TMA staging buffer take the bitmap pass."""
+    ctx = _native.context()
+    ctx.option("merge_cap", cap)
+    ctx.option("fill_algo", 4)
+    try:
+        for case in golden_cases:
+            case.check(b200.build(case.view, case.lists))
+        g = golden_ref["builds_hashed"]["q32_n10000"]
+        v = pauli_view(10000, 32, 0)
+        assert sha(b200.build(v, random_lists(v, seed=0)).graph.neighbors) == g["neighbors_sha"]
+    finally:
+        ctx.option("merge_cap", 0)
+        ctx.option("fill_algo", 0)
+
+
 @pytest.mark.parametrize("window", [4096, 8192])
 def test_cooperative_fill_windows(golden_ref, window):
     g = golden_ref["builds_hashed"]["q32_n20000"]

@@ -18,6 +18,7 @@ ap.add_argument("--q", type=int, default=32)
 ap.add_argument("--algo", type=int, default=0)
 ap.add_argument("--window", type=int, default=0)
 ap.add_argument("--k2", type=int, default=0)
+ap.add_argument("--fill", type=int, default=0)
 ap.add_argument("--reps", type=int, default=3)
 a = ap.parse_args()
 
@@ -30,6 +31,7 @@ ctx = _native.context()
 ctx.option("k1_algo", a.algo)
 ctx.option("window", a.window)
 ctx.option("k2_mode", a.k2)
+ctx.option("fill_algo", a.fill)
 ctx.profiling(True)
 stage(v, lists, ctx)
 print("prep ms", ctx.kernel_times()[4])
