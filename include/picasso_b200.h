@@ -133,6 +133,16 @@ int pcg_kernel_times(pcg_ctx *ctx, float *ms, int32_t n);
  *   "window": bitmap window of the row pass (ids), "fr_ichunk": rows per K1 work item */
 int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value);
 
+/*
+ * Host list coloring of a conflict CSR, dynamic bucket scheme (list_coloring.py:53-139),
+ * draw-for-draw identical to numpy's Generator(PCG64).  rng6 = {state_hi, state_lo, inc_hi,
+ * inc_lo, has_uint32, uinteger} (numpy's PCG64 state), advanced in place.  color_of[k] =
+ * chosen color of member k, or INT64_MIN for the uncolored residue.
+ */
+int pcg_color_dynamic(int64_t nm, const int64_t *offsets, const int64_t *neighbors,
+                      const int64_t *list_data, const int64_t *list_off, uint64_t *rng6,
+                      int64_t *color_of, int64_t *removal_ops);
+
 #ifdef __cplusplus
 }
 #endif

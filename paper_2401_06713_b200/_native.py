@@ -76,6 +76,8 @@ def library():
         lib.pcg_prep_device.argtypes = [_VP]
         lib.pcg_fill_rows_device.argtypes = [_VP, _VP, _I32, _VP, ctypes.POINTER(_I64),
                                              ctypes.POINTER(_I64)]
+        lib.pcg_color_dynamic.argtypes = [ctypes.c_int64, _VP, _VP, _VP, _VP, _VP, _VP, _VP]
+        lib.pcg_color_dynamic.restype = ctypes.c_int
         lib.pcg_stream.argtypes = [_VP]
         lib.pcg_stream.restype = _VP
         for name in ("pcg_create", "pcg_destroy", "pcg_set_inputs", "pcg_count",
@@ -92,7 +94,7 @@ EXPORTED = (
     "pcg_version", "pcg_create", "pcg_destroy", "pcg_last_error", "pcg_set_inputs", "pcg_count",
     "pcg_copy_degrees", "pcg_fill", "pcg_fill_rows", "pcg_count_device", "pcg_fill_device",
     "pcg_build_device", "pcg_set_profiling", "pcg_kernel_times", "pcg_set_option", "pcg_stream",
-    "pcg_degrees_device", "pcg_fill_rows_device", "pcg_prep_device",
+    "pcg_degrees_device", "pcg_fill_rows_device", "pcg_prep_device", "pcg_color_dynamic",
 )
 
 
