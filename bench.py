@@ -315,6 +315,14 @@ def bench_gpu(args) -> None:
                          "frac": k1_rate / popc_bound},
         "clocks": clocks.summary(),
     }
+    if not args.no_run:
+        # the whole Picasso run on this workload (GPU builds + GPU palette lists + native
+        # host list coloring): end-to-end coloring time and #colors (BASELINE.json metric)
+        t0 = time.perf_counter()
+        res = b200.run(view, b200.PaletteParams(*WORKLOADS[args.workload][3:6]))
+        line["run"] = {"seconds": time.perf_counter() - t0, "colors": res.total_colors,
+                       "iterations": len(res.iterations), "oracle_edges": res.oracle_edges,
+                       "peak_conflict_edges": res.peak_conflict_edges}
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(view, lists, seconds=args.cpu_seconds)
     print(json.dumps(line), flush=True)
@@ -331,6 +339,7 @@ def main() -> None:
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true", help="skip the nvidia-smi sampler")
+    ap.add_argument("--no-run", action="store_true", help="skip the whole-run report")
     args = ap.parse_args()
     if args.impl == "reference":
         bench_reference(args)

@@ -134,6 +134,15 @@ int pcg_kernel_times(pcg_ctx *ctx, float *ms, int32_t n);
 int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value);
 
 /*
+ * Palette lists on the device (rng.py:22-70 + driver.py:175-188, bit-identical): for each
+ * active id v, list_size distinct colors of [0, palette_size) by Floyd sampling on the
+ * splitmix64 stream mix64(v*phi + base_key), sorted, + palette_base.  base_key =
+ * mix64(seed + phi*iteration) (rng.stream_keys).  out: (n, list_size) int64, host.
+ */
+int pcg_assign_lists(pcg_ctx *ctx, const int64_t *active, int64_t n, uint64_t base_key,
+                     int64_t palette_size, int32_t list_size, int64_t palette_base, int64_t *out);
+
+/*
  * Host list coloring of a conflict CSR, dynamic bucket scheme (list_coloring.py:53-139),
  * draw-for-draw identical to numpy's Generator(PCG64).  rng6 = {state_hi, state_lo, inc_hi,
  * inc_lo, has_uint32, uinteger} (numpy's PCG64 state), advanced in place.  color_of[k] =

@@ -76,6 +76,8 @@ def library():
         lib.pcg_prep_device.argtypes = [_VP]
         lib.pcg_fill_rows_device.argtypes = [_VP, _VP, _I32, _VP, ctypes.POINTER(_I64),
                                              ctypes.POINTER(_I64)]
+        lib.pcg_assign_lists.argtypes = [_VP, _VP, _I64, ctypes.c_uint64, _I64, _I32, _I64, _VP]
+        lib.pcg_assign_lists.restype = ctypes.c_int
         lib.pcg_color_dynamic.argtypes = [ctypes.c_int64, _VP, _VP, _VP, _VP, _VP, _VP, _VP]
         lib.pcg_color_dynamic.restype = ctypes.c_int
         lib.pcg_stream.argtypes = [_VP]
@@ -95,6 +97,7 @@ EXPORTED = (
     "pcg_copy_degrees", "pcg_fill", "pcg_fill_rows", "pcg_count_device", "pcg_fill_device",
     "pcg_build_device", "pcg_set_profiling", "pcg_kernel_times", "pcg_set_option", "pcg_stream",
     "pcg_degrees_device", "pcg_fill_rows_device", "pcg_prep_device", "pcg_color_dynamic",
+    "pcg_assign_lists",
 )
 
 
@@ -201,6 +204,14 @@ class Context:
                                                   ctypes.byref(lo), ctypes.byref(hi)),
                     "pcg_fill_rows_device")
         return int(lo.value), int(hi.value)
+
+    def assign_lists(self, active: np.ndarray, base_key: int, P: int, L: int, base: int) -> np.ndarray:
+        active = np.ascontiguousarray(active, dtype=np.int64)
+        out = np.empty((active.size, L), dtype=np.int64)
+        self._check(self.lib.pcg_assign_lists(self.h, _ptr(active), int(active.size),
+                                              ctypes.c_uint64(base_key), int(P), int(L), int(base),
+                                              _ptr(out)), "pcg_assign_lists")
+        return out
 
     def count_device(self) -> tuple:
         c = Counts()

@@ -1096,3 +1096,26 @@ extern "C" int pcg_prep_device(pcg_ctx *ctx) {
     ctx->counted = false;
     return prep_device(ctx);
 }
+
+// Palette lists on the device (rng.py:22-70, driver.py:175-188): active ids in, (n, L) int64
+// colors out (host pointers); base_key = mix64(seed + phi * iteration), computed by the caller
+// exactly like rng.stream_keys.
+extern "C" int pcg_assign_lists(pcg_ctx *ctx, const int64_t *active, int64_t n, uint64_t base_key,
+                                int64_t palette_size, int32_t list_size, int64_t palette_base,
+                                int64_t *out) {
+    if (!ctx || (n > 0 && (!active || !out))) return PCG_E_ARG;
+    if (list_size < 1 || list_size > 1024 || palette_size < list_size)
+        return fail(ctx, PCG_E_ARG, "need 0 < list_size <= palette_size, list_size <= 1024");
+    if (n == 0) return PCG_OK;
+    PCG_TRY_CUDA(ctx, cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    PCG_ALLOC(ctx, ctx->active, (size_t)n * 8);
+    PCG_ALLOC(ctx, ctx->lists64, (size_t)n * list_size * 8);
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->active.p, active, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+    launch_assign_lists(ctx->active.as<int64_t>(), n, base_key, palette_size, list_size, palette_base,
+                        ctx->lists64.as<int64_t>(), s);
+    PCG_CHECK_LAUNCH(ctx);
+    int rc = d2h_pipelined(ctx, out, ctx->lists64.p, (size_t)n * list_size * 8);
+    ctx->staged = false;  // the staging buffers now hold lists, not a build's inputs
+    return rc;
+}

@@ -127,6 +127,8 @@ int launch_owned_masks(const BucketArgs &b, const OwnArgs &o, int sms, cudaStrea
 int launch_count_owned(const RowArgs &a, int sms, cudaStream_t s);
 int launch_fill_merge(const RowArgs &a, const MergeArgs &g, bool out64, int sms, cudaStream_t s);
 int merge_smem_bytes(int cap);
+int launch_assign_lists(const int64_t *active, int64_t n, uint64_t base_key, int64_t P, int L,
+                        int64_t palette_base, int64_t *out, cudaStream_t s);
 int launch_write_runs(const BucketArgs &b, const RunArgs &r, int sms, cudaStream_t s);
 int launch_fill_runs(const RowArgs &a, const RunArgs &r, bool out64, int sms, cudaStream_t s);
 int launch_fill_coop(const RowArgs &a, bool out64, int sms, cudaStream_t s);

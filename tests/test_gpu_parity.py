@@ -260,3 +260,40 @@ def test_full_size_config2_properties():
         assert np.array_equal(got, row)
         for j in got[:5]:  # symmetry
             assert i in nb[off[j]:off[j + 1]]
+
+
+@pytest.mark.parametrize("n,P,L,it,seed,base", [(2000, 250, 15, 1, 0, 0), (500, 40, 7, 2, 3, 100),
+                                                 (3000, 125000, 28, 1, 9, 0), (10, 5, 5, 4, 1, 7),
+                                                 (10, 17, 1, 1, 0, 0), (4000, 5000, 59, 3, -5, 11),
+                                                 (300, 400, 394, 1, 2, 0)])
+def test_gpu_palette_lists_bit_identical(n, P, L, it, seed, base):
+    """csrc/rng.cu draws exactly the host splitmix64/Floyd lists (rng.py:22-70)."""
+    if L > P:
+        pytest.skip("L <= P")
+    rs = np.random.default_rng(n)
+    active = np.sort(rs.choice(10 * n, size=n, replace=False)).astype(np.int64)
+    plan = b200.IterationPlan(iteration=it, palette_size=P, palette_base=base, list_size=L)
+    host = b200.assign_random_lists(plan, active, seed, device=False)
+    dev = b200.assign_random_lists(plan, active, seed, device=True)
+    assert np.array_equal(host.array, dev.array)
+
+
+def test_gpu_palette_lists_golden(golden_ref):
+    plan = b200.plan_iteration(1, 2000, b200.PaletteParams(12.5, 2.0, 0))
+    dev = b200.assign_random_lists(plan, np.arange(2000), 0, device=True)
+    want = next(b for b in golden_ref["runs"]["c1"]["builds"] if b["n_active"] == 2000)
+    assert sha(dev.array) == want["lists_sha"]
+
+
+def test_whole_run_50k_recorded_golden(golden_ref):
+    """The largest run the reference could finish on the survey host (50,000 x 32q, 8
+    iterations, 503 s there): identical coloring (sha of the color array), color count,
+    iteration count, |E| and peak |E_c|."""
+    r = golden_ref["runs_recorded"]["q32_n50000"]
+    v = pauli_view(r["n"], r["q"], r["gen_seed"])
+    res = b200.run(v, b200.PaletteParams(r["palette_pct"], r["alpha"], seed=r["seed"]))
+    assert res.total_colors == r["colors"]
+    assert len(res.iterations) == r["iterations"]
+    assert res.oracle_edges == r["oracle_edges"]
+    assert res.peak_conflict_edges == r["peak_conflict_edges"]
+    assert sha(res.color) == r["color_sha"]
