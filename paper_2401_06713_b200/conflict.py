@@ -31,7 +31,7 @@ from typing import Optional
 
 import numpy as np
 
-from . import _native
+from . import _native, hostpool
 from .errors import EdgeBudgetExceededError
 from .graph import ExplicitGraph, pair_chunks
 
@@ -165,7 +165,7 @@ def build(view, lists, *, edge_budget: Optional[int] = None, threads: int = 1,
     nm = int(c.members_in_range)
     members = np.empty(nm, dtype=np.int64)
     offsets = np.empty(nm + 1, dtype=np.int64)
-    neighbors = np.empty(2 * total, dtype=np.int64)
+    neighbors = hostpool.empty_int64(2 * total)
     ctx.fill(members, offsets, neighbors)
     if nm == 0:
         offsets[0] = 0

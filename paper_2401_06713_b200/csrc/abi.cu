@@ -7,6 +7,8 @@
 
 #include <omp.h>
 
+#include <immintrin.h>
+
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -792,6 +794,32 @@ static int d2h_pipelined(pcg_ctx *ctx, void *dst, const void *src, size_t bytes)
     return PCG_OK;
 }
 
+// int32 -> int64 widening of one host range.  AVX-512 with non-temporal stores when the CPU
+// has it: the destination is written once and never read back here, so streaming stores
+// skip the read-for-ownership of every output line (1/3 less host memory traffic).
+__attribute__((target("avx512f"))) static void widen_avx512(int64_t *to, const int32_t *from,
+                                                              size_t len) {
+    size_t x = 0;
+    for (; x < len && (reinterpret_cast<uintptr_t>(to + x) & 63); ++x) to[x] = from[x];
+    for (; x + 16 <= len; x += 16) {
+        const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(from + x));
+        const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(from + x + 8));
+        _mm512_stream_si512(reinterpret_cast<__m512i *>(to + x), _mm512_cvtepi32_epi64(a));
+        _mm512_stream_si512(reinterpret_cast<__m512i *>(to + x + 8), _mm512_cvtepi32_epi64(b));
+    }
+    for (; x < len; ++x) to[x] = from[x];
+    _mm_sfence();
+}
+
+static void widen_range(int64_t *to, const int32_t *from, size_t len) {
+    static const bool avx512 = __builtin_cpu_supports("avx512f");
+    if (avx512) {
+        widen_avx512(to, from, len);
+        return;
+    }
+    for (size_t x = 0; x < len; ++x) to[x] = from[x];
+}
+
 // Same pipeline, int32 device ids widened to the API's int64 during the host-side copy, so
 // only half the bytes cross PCIe.
 static int d2h_widen(pcg_ctx *ctx, int64_t *dst, const int32_t *src, size_t count) {
@@ -818,7 +846,7 @@ static int d2h_widen(pcg_ctx *ctx, int64_t *dst, const int32_t *src, size_t coun
 #pragma omp parallel for num_threads(std::min(16, omp_get_num_procs())) schedule(static)
         for (int t = 0; t < parts; ++t) {
             const size_t a = len * t / parts, b = len * (t + 1) / parts;
-            for (size_t x = a; x < b; ++x) to[x] = from[x];
+            widen_range(to + a, from + a, b - a);
         }
         return cudaSuccess;
     };

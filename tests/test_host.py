@@ -162,3 +162,26 @@ def test_native_list_coloring_ragged_lists(golden_cases):
     a = lc.color_dynamic(gc, case.lists, np.random.default_rng(5))
     b = lc.color_dynamic_py(gc, case.lists, np.random.default_rng(5))
     assert a.colored == b.colored and np.array_equal(a.uncolored, b.uncolored)
+
+
+def test_hostpool_never_hands_out_a_live_buffer():
+    from paper_2401_06713_b200 import hostpool as hp
+
+    hp.release()
+    n = hp.MIN_POOLED_BYTES // 8 + 1000
+    a = hp.empty_int64(n)
+    b = hp.empty_int64(n - 10)          # a is alive -> fresh memory
+    assert not np.shares_memory(a, b)
+    view_of_b = b[5:]                   # keeps b's memory alive through .base
+    del b
+    c = hp.empty_int64(n - 20)
+    assert not np.shares_memory(c, view_of_b)
+    del view_of_b, a
+    addr = c.__array_interface__["data"][0]
+    del c
+    d = hp.empty_int64(n - 30)          # the pooled buffer is free again -> reused
+    assert d.__array_interface__["data"][0] == addr
+    small = hp.empty_int64(10)
+    assert not np.shares_memory(small, d)
+    hp.release()
+    assert hp.cached_bytes() == 0
