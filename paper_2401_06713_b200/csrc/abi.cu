@@ -10,6 +10,7 @@
 #include <immintrin.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -174,6 +175,8 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "k2_mode")) ctx->k2_mode = (int)value;
     else if (!strcmp(key, "merge_cap")) ctx->merge_cap = (int)value;
     else if (!strcmp(key, "fill_algo")) ctx->fill_algo = (int)value;
+    else if (!strcmp(key, "seg_bits")) ctx->seg_bits = (int)value;
+    else if (!strcmp(key, "seg_warps")) ctx->seg_warps = (int)value;
     else return fail(ctx, PCG_E_ARG, std::string("unknown option ") + key);
     return PCG_OK;
 }
@@ -341,9 +344,12 @@ static int prep_device(pcg_ctx *ctx) {
     ctx->owned = ctx->masked && ctx->k2_mode != 2 && m_max <= 4096 && P < (1 << 20) - 1 &&
                  ctx->lmax <= 64 && ctx->kw <= 16;
 
-    PCG_ALLOC(ctx, ctx->bmemp, (size_t)(padded_total + 16) * 4);
+    ctx->m_max = m_max;
+    ctx->mask_words = mask_total;
+    // +64 sentinel ids: the segmented fill loads whole 32-position words past a bucket's end
+    PCG_ALLOC(ctx, ctx->bmemp, (size_t)(padded_total + 64) * 4);
     PCG_ALLOC(ctx, ctx->posof, (size_t)entries * 4);
-    PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->bmemp.p, 0x7f, (size_t)(padded_total + 16) * 4, s));
+    PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->bmemp.p, 0x7f, (size_t)(padded_total + 64) * 4, s));
     BucketArgs b{};
     b.P = P;
     b.bstart = ctx->bstart.as<int32_t>();
@@ -904,6 +910,30 @@ static int fill_rows_device(pcg_ctx *ctx, int64_t r0, int64_t r1, const int32_t 
             PCG_CHECK_LAUNCH(ctx);
         }
         return PCG_OK;
+    }
+    if (ctx->fill_algo == 0 && ctx->mask_words < (1LL << 32) && ctx->lmax <= 64 && maxdeg < 65535) {
+        // segmented fill (default): warp-decoded mask words, lane-segment harvest
+        SegArgs g{};
+        // measured: small windows (more warps per SM) win at config 2; at 1M ids fewer,
+        // larger windows win (each window re-decodes the words that straddle its edges)
+        const int64_t max_bits = ctx->seg_bits > 0 ? ctx->seg_bits : (ctx->n <= 131072 ? 28672 : 61440);
+        seg_geometry(ctx->n, max_bits, &g.wb, &g.nwin, &g.seg);
+        const int wpm = (ctx->m_max + 31) / 32;
+        g.desc_cap = (ctx->lmax * (wpm + (g.nwin > 1 ? 1 : 0)) + 3) & ~3;
+        g.warp_words = ((g.wb >> 5) + 32 + 2 * g.desc_cap + 3) & ~3;
+        g.warps = ctx->seg_warps > 0 ? ctx->seg_warps : 4;
+        if ((size_t)g.warp_words * 4 * g.warps <= 227u * 1024u) {
+            if (g.nwin > 1) {
+                PCG_ALLOC(ctx, ctx->bnd, (size_t)ctx->P * (g.nwin + 1) * 4);
+                *launches += launch_window_bounds(ctx->bstart.as<int32_t>(), ctx->bpos.as<int32_t>(),
+                                                  ctx->bmemp.as<int32_t>(), ctx->P, g.nwin, g.wb,
+                                                  ctx->bnd.as<int32_t>(), s);
+                g.bnd = ctx->bnd.as<int32_t>();
+            }
+            *launches += launch_fill_seg(a, g, out64, ctx->sms, s);
+            PCG_CHECK_LAUNCH(ctx);
+            return PCG_OK;
+        }
     }
     if (ctx->fill_algo == 1) {  // cooperative bitmap fill (experimental)
         a.window = coop_window(ctx);

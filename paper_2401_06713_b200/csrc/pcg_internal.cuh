@@ -79,6 +79,16 @@ struct RunArgs {
     int32_t *nheavy;
 };
 
+struct SegArgs {
+    int32_t wb;            // window bits per warp bitmap (1024 * S)
+    int32_t nwin;          // windows per row
+    int32_t seg;           // bitmap words per lane segment (wb / 1024, odd)
+    int32_t warp_words;    // shared words per warp (see k_fill_seg)
+    int32_t desc_cap;      // descriptor slots (mask words per window)
+    int32_t warps;         // warps per block
+    const int32_t *bnd;    // (P, nwin+1) members of each bucket below each window start
+};
+
 struct MergeArgs {
     int32_t cap;           // ids per warp buffer; longer rows go to the bitmap fill
     int32_t *heavy;        // out: rows longer than cap
@@ -132,6 +142,10 @@ int launch_assign_lists(const int64_t *active, int64_t n, uint64_t base_key, int
 int launch_write_runs(const BucketArgs &b, const RunArgs &r, int sms, cudaStream_t s);
 int launch_fill_runs(const RowArgs &a, const RunArgs &r, bool out64, int sms, cudaStream_t s);
 int launch_fill_coop(const RowArgs &a, bool out64, int sms, cudaStream_t s);
+void seg_geometry(int64_t n, int64_t max_bits, int32_t *wb, int32_t *nwin, int32_t *seg);
+int launch_window_bounds(const int32_t *bstart, const int32_t *bpos, const int32_t *bmemp,
+                         int64_t P, int nwin, int32_t wb, int32_t *bnd, cudaStream_t s);
+int launch_fill_seg(const RowArgs &a, const SegArgs &g, bool out64, int sms, cudaStream_t s);
 int launch_compact(const int32_t *deg, int64_t n, const int32_t *compact, const int64_t *rowoff,
                    const int64_t *active, int64_t *members_out, int64_t *offsets_out,
                    cudaStream_t s);
@@ -158,8 +172,11 @@ struct pcg_ctx {
     int window = 0;     // K2 window bits (0 auto)
     int fr_ichunk = 0;  // four-Russians i-chunk (0 auto)
     int merge_cap = 0;  // fill-merge buffer cap (0 auto; testing knob)
-    int fill_algo = 0;  // owned masks: 0/3 lane-per-bucket bitmap fill, 1 cooperative bitmap,
+    int fill_algo = 0;  // owned masks: 0 segmented fill (warp-decoded words, lane-segment
+                        // harvest), 3 lane-per-bucket bitmap fill, 1 cooperative bitmap,
                         // 2 merge, 4 TMA-staged owned runs
+    int seg_bits = 0;   // segmented fill: max window bits per warp (0 auto)
+    int seg_warps = 0;  // segmented fill: warps per block (0 auto)
     int k2_mode = 0;    // 0 auto, 1 partner gathers, 2 bucket masks + bitmap dedupe, 3 owned masks + merge
 
     // state of the last count
@@ -182,4 +199,7 @@ struct pcg_ctx {
     bool owned = false;   // masks keep each pair only in its smallest shared color
     bool runs_ready = false;  // owned partner runs materialised (TMA-staged fill)
     int32_t maxdeg = 0;
+    int32_t m_max = 0;        // largest color bucket of the staged build
+    int64_t mask_words = 0;   // owned/bucket mask words of the staged build
+    pcg::DevBuf bnd;          // segmented fill window bounds
 };

@@ -53,7 +53,8 @@ def test_merge_heavy_rows_fallback(golden_cases, cap):
         ctx.option("k2_mode", 0)
 
 
-@pytest.mark.parametrize("fill_algo", [0, 1, 2, 4], ids=["bitmap", "coop", "merge", "runs-tma"])
+@pytest.mark.parametrize("fill_algo", [0, 1, 2, 3, 4],
+                         ids=["segmented", "coop", "merge", "lane-bitmap", "runs-tma"])
 def test_owned_fill_variants(golden_cases, fill_algo):
     ctx = _native.context()
     ctx.option("k2_mode", 3)
@@ -81,6 +82,28 @@ def test_runs_fill_heavy_rows(golden_cases, golden_ref, cap):
     finally:
         ctx.option("merge_cap", 0)
         ctx.option("fill_algo", 0)
+
+
+@pytest.mark.parametrize("bits,warps", [(1024, 1), (3072, 2), (12288, 2), (20480, 4),
+                                        (131072, 3), (131072, 4)])
+def test_segmented_fill_geometry(golden_cases, golden_ref, bits, warps):
+    """Window size (1..many windows per row) and warps per block must not change a single
+    entry."""
+    ctx = _native.context()
+    ctx.option("seg_bits", bits)
+    ctx.option("seg_warps", warps)
+    try:
+        for case in golden_cases:
+            case.check(b200.build(case.view, case.lists))
+        for n in (10000, 20000):
+            g = golden_ref["builds_hashed"][f"q32_n{n}"]
+            v = pauli_view(n, 32, 0)
+            gc = b200.build(v, random_lists(v, seed=0))
+            assert (sha(gc.graph.offsets), sha(gc.graph.neighbors)) == (
+                g["offsets_sha"], g["neighbors_sha"])
+    finally:
+        ctx.option("seg_bits", 0)
+        ctx.option("seg_warps", 0)
 
 
 @pytest.mark.parametrize("window", [4096, 8192])
