@@ -176,6 +176,7 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "merge_cap")) ctx->merge_cap = (int)value;
     else if (!strcmp(key, "fill_algo")) ctx->fill_algo = (int)value;
     else if (!strcmp(key, "seg_bits")) ctx->seg_bits = (int)value;
+    else if (!strcmp(key, "own_algo")) ctx->own_algo = (int)value;
     else if (!strcmp(key, "seg_warps")) ctx->seg_warps = (int)value;
     else return fail(ctx, PCG_E_ARG, std::string("unknown option ") + key);
     return PCG_OK;
@@ -380,31 +381,40 @@ static int prep_device(pcg_ctx *ctx) {
             while (hs < want && hs < 32768) hs <<= 1;
             o.hash_slots = hs;
             o.m_cap = m_max;
+            o.fr = ctx->own_algo == 0 ? 1 : 0;
+            o.l_magic = (uint32_t)(((1ull << 32) + (uint64_t)std::max(1, ctx->L) - 1) /
+                                   (uint64_t)std::max(1, ctx->L));
+            if ((int64_t)m_max * std::max(1, ctx->L) >= (1 << 20)) o.fr = 0;  // umulhi range
             PCG_TRY_CUDA(ctx, cudaMemsetAsync(o.overflow, 0, 4, s));
-            PCG_ALLOC(ctx, ctx->runlen, (size_t)entries * 4);
-            PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->runlen.p, 0, (size_t)entries * 4, s));
-            b.runlen = ctx->runlen.as<int32_t>();
+            const bool want_runs = ctx->fill_algo == 4;  // run lengths only feed the runs fill
+            b.runlen = nullptr;
+            if (want_runs) {
+                PCG_ALLOC(ctx, ctx->runlen, (size_t)entries * 4);
+                PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->runlen.p, 0, (size_t)entries * 4, s));
+                b.runlen = ctx->runlen.as<int32_t>();
+            }
             launch_owned_masks(b, o, ctx->sms, s);
             PCG_CHECK_LAUNCH(ctx);
-            // owned partner runs (padded to 4 ids) for the TMA-staged fill
-            PCG_ALLOC(ctx, ctx->runoff, (size_t)(entries + 1) * 8);
-            cub::TransformInputIterator<int64_t, PaddedRun, cub::CountingInputIterator<int64_t>> plen(
-                cidx, PaddedRun{ctx->runlen.as<int32_t>(), entries});
-            size_t t3 = 0;
-            PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, t3, plen,
-                                                            ctx->runoff.as<int64_t>(), entries + 1, s));
-            PCG_ALLOC(ctx, ctx->cubtmp, t3);
-            PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->cubtmp.p, t3, plen,
-                                                            ctx->runoff.as<int64_t>(), entries + 1, s));
-            int32_t ovf = 0;
             int64_t runs_total = 0;
+            if (want_runs) {  // owned partner runs (padded to 4 ids) for the TMA-staged fill
+                PCG_ALLOC(ctx, ctx->runoff, (size_t)(entries + 1) * 8);
+                cub::TransformInputIterator<int64_t, PaddedRun, cub::CountingInputIterator<int64_t>> plen(
+                    cidx, PaddedRun{ctx->runlen.as<int32_t>(), entries});
+                size_t t3 = 0;
+                PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, t3, plen,
+                                                                ctx->runoff.as<int64_t>(), entries + 1, s));
+                PCG_ALLOC(ctx, ctx->cubtmp, t3);
+                PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->cubtmp.p, t3, plen,
+                                                                ctx->runoff.as<int64_t>(), entries + 1, s));
+                PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&runs_total, ctx->runoff.as<int64_t>() + entries, 8,
+                                                  cudaMemcpyDeviceToHost, s));
+            }
+            int32_t ovf = 0;
             PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&ovf, o.overflow, 4, cudaMemcpyDeviceToHost, s));
-            PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&runs_total, ctx->runoff.as<int64_t>() + entries, 8,
-                                              cudaMemcpyDeviceToHost, s));
             PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
             if (ovf) ctx->owned = false;  // a color's ownership table overflowed: dedupe path
             ctx->runs_ready = false;
-            if (ctx->owned && ctx->fill_algo == 4 &&
+            if (ctx->owned && want_runs &&
                 (size_t)runs_total * 4 < free_b / 3) {
                 PCG_ALLOC(ctx, ctx->runs, (size_t)(runs_total + 4) * 4);
                 RunArgs ra{};

@@ -191,6 +191,182 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_masks(BucketArgs b, OwnAr
 }
 
 // ---------------------------------------------------------------------------------------
+// K2a (owned, four-Russians): one CTA per color, same output as k_owned_masks.  The m x m
+// commute matrix of a bucket is a GF(2) product A_k . B_t: for each 32-partner word w the
+// CTA transposes the partners' bits with ballots (BT[p] bit tt = bit p of B_{32w+tt}) and
+// tabulates, for every 4-bit slice g of the K = 32*KW bits, the 16 XOR-combinations of
+// BT[4g..4g+3].  Row k's mask word is then the XOR of NIB = 8*KW table entries picked by its
+// own nibbles (addresses precomputed once per color): 32 pairs per NIB LDS + NIB/2 LOP3,
+// instead of one AND/POPC chain per pair.  Ownership inserts run warp-per-member with the
+// lanes over the member's (sorted) list, colors below c only.
+// ---------------------------------------------------------------------------------------
+template <int KW>
+__global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs o) {
+    constexpr int NIB = 8 * KW;
+    extern __shared__ __align__(16) uint32_t osm[];
+    const int HS = o.hash_slots;
+    uint32_t *table = osm;                                        // HS: (c'+1)<<12 | first k
+    unsigned short *head = reinterpret_cast<unsigned short *>(osm + HS);  // HS: last coll + 1
+    uint32_t *coll = osm + HS + HS / 2;                           // OWN_COLL: slot<<12 | k
+    int32_t *link = reinterpret_cast<int32_t *>(coll + OWN_COLL); // OWN_COLL: previous in slot
+    int32_t *sid = link + OWN_COLL;                               // member ids (m_cap)
+    uint32_t *T = reinterpret_cast<uint32_t *>(sid + ((o.m_cap + 3) & ~3));  // NIB*16 table
+    uint32_t *BT = T + NIB * 16;                                  // 32*KW transposed bits
+    __shared__ int ncoll, overflow;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NWARPS = OWN_THREADS / 32;
+    const uint32_t T_s = (uint32_t)__cvta_generic_to_shared(T);
+    for (int x = tid; x < HS + HS / 2; x += OWN_THREADS) osm[x] = 0u;
+    for (int64_t c = blockIdx.x; c < b.P; c += gridDim.x) {
+        const int m = b.bstart[c + 1] - b.bstart[c];
+        if (m < 2) {
+            if (m == 1 && tid == 0) b.masks[b.maskoff[c]] = 0u;
+            continue;
+        }
+        const int W = (m + 31) >> 5;
+        const int32_t *mem = b.bmemp + b.bpos[c];
+        uint32_t *out = b.masks + b.maskoff[c];
+        if (tid == 0) {
+            ncoll = 0;
+            overflow = 0;
+        }
+        for (int t = tid; t < m; t += OWN_THREADS) sid[t] = mem[t];
+        __syncthreads();
+        // ---- commute masks
+        for (int k0 = 0; k0 < m; k0 += OWN_THREADS) {
+            const int k = k0 + tid;
+            uint32_t naddr[NIB];
+            {
+                uint32_t av[KW];
+#pragma unroll
+                for (int q = 0; q < KW; ++q) av[q] = k < m ? __ldg(b.A + (int64_t)sid[k] * KW + q) : 0u;
+#pragma unroll
+                for (int g = 0; g < NIB; ++g)
+                    naddr[g] = T_s + (uint32_t)(g * 16 + ((av[g >> 3] >> (4 * (g & 7))) & 15u)) * 4u;
+            }
+            for (int w = 0; w < W; ++w) {
+                // transposed partner bits: warp j takes bit positions [j*4*KW, (j+1)*4*KW)
+                {
+                    const int t = 32 * w + lane;
+                    constexpr int PER = 4 * KW;  // bits per warp (32*KW / 8 warps)
+#pragma unroll
+                    for (int pp = 0; pp < PER; ++pp) {
+                        const int p = warp * PER + pp;
+                        const uint32_t word = t < m ? __ldg(b.B + (int64_t)sid[t] * KW + (p >> 5)) : 0u;
+                        const uint32_t bal = __ballot_sync(0xffffffffu, (word >> (p & 31)) & 1u);
+                        if (lane == 0) BT[p] = bal;
+                    }
+                }
+                __syncthreads();
+                for (int x = tid; x < NIB * 16; x += OWN_THREADS) {
+                    const int g = x >> 4, v = x & 15;
+                    uint32_t e = 0u;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if ((v >> q) & 1) e ^= BT[4 * g + q];
+                    T[x] = e;
+                }
+                __syncthreads();
+                if (k < m) {
+                    uint32_t acc = 0u;
+#pragma unroll
+                    for (int g = 0; g < NIB; ++g) {
+                        uint32_t e;
+                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(naddr[g]));
+                        acc ^= e;
+                    }
+                    const int tend = min(32, m - 32 * w);
+                    uint32_t bits = ~acc & (tend == 32 ? 0xffffffffu : ((1u << tend) - 1u));
+                    if (k >> 5 == w) bits &= ~(1u << (k & 31));  // no self pair
+                    out[(int64_t)k * W + w] = bits;
+                }
+                __syncthreads();
+            }
+        }
+        // ---- ownership: (c', k) for every color c' < c of every member's list.  Rectangular
+        // lists: one thread per (member, slot) item, consecutive threads on consecutive slots
+        // of a member (coalesced loads); ragged lists: warp per member.
+        auto insert = [&](uint32_t cp, int k) {
+            const uint32_t key = (cp << 12) | (uint32_t)k;
+            uint32_t slot = mix32(cp) & (HS - 1);
+            for (int probe = 0;; ++probe) {
+                if (probe == HS) {
+                    overflow = 1;
+                    return;
+                }
+                const uint32_t prev = atomicCAS(&table[slot], 0u, key);
+                if (prev == 0u) return;
+                if ((prev >> 12) == cp) {
+                    const int q = atomicAdd(&ncoll, 1);
+                    if (q < OWN_COLL) {
+                        coll[q] = (slot << 12) | (uint32_t)k;
+                        uint32_t *hw = reinterpret_cast<uint32_t *>(head) + (slot >> 1);
+                        const int sh = (slot & 1) * 16;
+                        uint32_t old = *hw, assumed;
+                        do {
+                            assumed = old;
+                            const uint32_t nv = (assumed & ~(0xffffu << sh)) | ((uint32_t)(q + 1) << sh);
+                            old = atomicCAS(hw, assumed, nv);
+                        } while (old != assumed);
+                        link[q] = (int)((old >> sh) & 0xffffu) - 1;
+                    } else {
+                        overflow = 1;
+                    }
+                    return;
+                }
+                slot = (slot + 1) & (HS - 1);
+            }
+        };
+        if (!o.loff) {
+            const uint32_t items = (uint32_t)m * (uint32_t)o.L;
+            for (uint32_t e = tid; e < items; e += OWN_THREADS) {
+                const int k = (int)__umulhi(e, o.l_magic);  // e / L (exact for e < 2^20)
+                const int x = (int)(e - (uint32_t)k * (uint32_t)o.L);
+                const int32_t cx = o.lrel[(int64_t)sid[k] * o.L + x];
+                if (cx < c) insert((uint32_t)cx + 1u, k);
+            }
+        } else {
+            for (int k = warp; k < m; k += NWARPS) {
+                const int32_t r = sid[k];
+                for (int64_t x = o.loff[r] + lane; x < o.loff[r + 1]; x += 32) {
+                    const int32_t cx = o.lrel[x];
+                    if (cx < c) insert((uint32_t)cx + 1u, k);
+                }
+            }
+        }
+        __syncthreads();
+        const int nc = min(ncoll, OWN_COLL);
+        if (overflow && tid == 0) atomicExch(o.overflow, 1);
+        for (int q = tid; q < nc; q += OWN_THREADS) {
+            const uint32_t slot = coll[q] >> 12;
+            const int k2 = (int)(coll[q] & 0xfffu);
+            int k1 = (int)(table[slot] & 0xfffu);
+            for (int p = link[q];; p = link[p]) {
+                if (k1 != k2) {
+                    atomicAnd(&out[(int64_t)k1 * W + (k2 >> 5)], ~(1u << (k2 & 31)));
+                    atomicAnd(&out[(int64_t)k2 * W + (k1 >> 5)], ~(1u << (k1 & 31)));
+                }
+                if (p < 0) break;
+                k1 = (int)(coll[p] & 0xfffu);
+            }
+        }
+        __syncthreads();
+        if (b.runlen) {  // owned partners per member: the run lengths of the runs fill
+            for (int k = tid; k < m; k += OWN_THREADS) {
+                int cnt = 0;
+                for (int w = 0; w < W; ++w) cnt += __popc(out[(int64_t)k * W + w]);
+                b.runlen[b.bstart[c] + k] = cnt;
+            }
+        }
+        // reset the table and the chain heads this color touched
+        for (int x = 4 * tid; x < HS; x += 4 * OWN_THREADS)
+            *reinterpret_cast<uint4 *>(table + x) = make_uint4(0u, 0u, 0u, 0u);
+        for (int q = tid; q < nc; q += OWN_THREADS) head[coll[q] >> 12] = 0;  // (16-bit store)
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------------------
 // K2c: degrees from owned masks (warp per row, lane per color slot)
 // ---------------------------------------------------------------------------------------
 __global__ void k_count_owned(RowArgs a) {
@@ -809,6 +985,19 @@ int run_owned(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s) {
     return 1;
 }
 
+template <int KW>
+int run_owned_fr(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s) {
+    int per_sm = 0;
+    const size_t smem = (size_t)(o.hash_slots + o.hash_slots / 2 + 2 * OWN_COLL +
+                                 ((o.m_cap + 3) & ~3) + 8 * KW * 16 + 32 * KW) * 4;
+    cudaFuncSetAttribute(k_owned_fr<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_owned_fr<KW>, OWN_THREADS, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * sms * 4, b.P));
+    k_owned_fr<KW><<<(unsigned)grid, OWN_THREADS, smem, s>>>(b, o);
+    return 1;
+}
+
 template <typename OutT>
 int run_merge(const RowArgs &a, const MergeArgs &g, int sms, cudaStream_t s) {
     const size_t smem = (size_t)MERGE_WARPS * (2 * g.cap + 68) * 4;
@@ -826,6 +1015,15 @@ int run_merge(const RowArgs &a, const MergeArgs &g, int sms, cudaStream_t s) {
 }  // namespace
 
 int launch_owned_masks(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s) {
+    if (o.fr) {
+        switch (b.kw) {
+            case 2: return run_owned_fr<2>(b, o, sms, s);
+            case 4: return run_owned_fr<4>(b, o, sms, s);
+            case 6: return run_owned_fr<6>(b, o, sms, s);
+            case 8: return run_owned_fr<8>(b, o, sms, s);
+            default: break;
+        }
+    }
     switch (b.kw) {
         case 2: return run_owned<2>(b, o, sms, s);
         case 4: return run_owned<4>(b, o, sms, s);

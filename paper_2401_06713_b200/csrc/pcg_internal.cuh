@@ -68,6 +68,8 @@ struct OwnArgs {
     int32_t *overflow;     // set when a color's ownership table overflowed
     int32_t hash_slots;    // power of two
     int32_t m_cap;         // >= largest bucket
+    int32_t fr;            // 1: four-Russians mask kernel (kw in {2,4,6,8})
+    uint32_t l_magic;      // ceil(2^32 / L): item -> member by umulhi
 };
 
 struct RunArgs {
@@ -177,6 +179,7 @@ struct pcg_ctx {
                         // 2 merge, 4 TMA-staged owned runs
     int seg_bits = 0;   // segmented fill: max window bits per warp (0 auto)
     int seg_warps = 0;  // segmented fill: warps per block (0 auto)
+    int own_algo = 0;   // owned masks: 0 four-Russians tables (when kw allows), 1 per-pair
     int k2_mode = 0;    // 0 auto, 1 partner gathers, 2 bucket masks + bitmap dedupe, 3 owned masks + merge
 
     // state of the last count

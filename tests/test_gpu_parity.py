@@ -24,7 +24,7 @@ def k1_algo(request):
     ctx.option("k1_algo", 0)
 
 
-@pytest.fixture(params=[1, 2, 3], ids=["k2-gather", "k2-bucketmasks", "k2-owned-merge"])
+@pytest.fixture(params=[1, 2, 3], ids=["k2-gather", "k2-bucketmasks", "k2-owned"])
 def k2_mode(request):
     ctx = _native.context()
     ctx.option("k2_mode", request.param)
@@ -35,6 +35,26 @@ def k2_mode(request):
 def test_every_golden_build(golden_cases, k1_algo, k2_mode):
     for case in golden_cases:
         case.check(b200.build(case.view, case.lists))
+
+
+@pytest.mark.parametrize("own_algo", [0, 1], ids=["own-fourrussians", "own-perpair"])
+def test_owned_mask_kernels(golden_cases, golden_ref, own_algo):
+    """Both owned-mask kernels (table-driven and per-pair) give the reference CSR."""
+    ctx = _native.context()
+    ctx.option("k2_mode", 3)
+    ctx.option("own_algo", own_algo)
+    try:
+        for case in golden_cases:
+            case.check(b200.build(case.view, case.lists))
+        for n in (5000, 20000):
+            g = golden_ref["builds_hashed"][f"q32_n{n}"]
+            v = pauli_view(n, 32, 0)
+            gc = b200.build(v, random_lists(v, seed=0))
+            assert (sha(gc.graph.offsets), sha(gc.graph.neighbors)) == (
+                g["offsets_sha"], g["neighbors_sha"])
+    finally:
+        ctx.option("own_algo", 0)
+        ctx.option("k2_mode", 0)
 
 
 @pytest.mark.parametrize("cap", [32, 96, 1024])
