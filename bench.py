@@ -71,60 +71,60 @@ def make_inputs(name: str, pinned: bool = False):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region, in-process through NVML
+    (a 50 ms polling thread; no nvidia-smi child process competing with the host thread that
+    drives the GPU)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
-    def __init__(self, device: int):
+    def __init__(self, device):
         self.device = device
-        self.proc = None
+        self.samples = []
+        self._stop = threading.Event()
+        self._thread = None
+
+    def _run(self, nvml, h):
+        while not self._stop.is_set():
+            try:
+                sm = nvml.nvmlDeviceGetClockInfo(h, nvml.NVML_CLOCK_SM)
+                mx = nvml.nvmlDeviceGetMaxClockInfo(h, nvml.NVML_CLOCK_SM)
+                rs = nvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((float(sm), float(mx), int(rs)))
+            except Exception:  # noqa: BLE001 - sampling is best effort
+                pass
+            self._stop.wait(0.05)
 
     def __enter__(self):
         if self.device is None:
             return self
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except (FileNotFoundError, OSError):
-            self.proc = None
-        time.sleep(0.25)
+            import pynvml as nvml
+
+            nvml.nvmlInit()
+            h = nvml.nvmlDeviceGetHandleByIndex(self.device)
+            self._thread = threading.Thread(target=self._run, args=(nvml, h), daemon=True)
+            self._thread.start()
+        except Exception:  # noqa: BLE001 - no NVML: report "unsampled"
+            self._thread = None
+        time.sleep(0.1)
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
-        if self.proc is not None:
-            time.sleep(0.15)
-            self.proc.terminate()
-            try:
-                out, _ = self.proc.communicate(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
-                out = ""
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        if self._thread is not None:
+            time.sleep(0.1)
+            self._stop.set()
+            self._thread.join(timeout=2)
 
     def summary(self) -> dict:
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in getattr(self, "lines", []):
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for name, val in zip(names, parts[2:6]):
-                if val.lower().startswith("active"):
-                    reasons.add(name)
-        if not sm:
+        if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        mx = max(s[1] for s in self.samples)
+        sm = [s[0] for s in self.samples]
         busy = [x for x in sm if x > 0.5 * mx] or sm
-        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": mx, "reasons": sorted(reasons)}
+        reasons = sorted({name for _, _, r in self.samples
+                          for name, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": mx, "reasons": reasons}
 
 
 def measured_peaks() -> dict:

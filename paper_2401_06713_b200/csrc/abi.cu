@@ -257,6 +257,24 @@ __global__ void k_iota(int32_t *x, int64_t n) {
 }  // namespace pcg_prep
 using namespace pcg_prep;
 
+static BucketArgs bucket_args(const pcg_ctx *ctx) {
+    BucketArgs b{};
+    b.P = ctx->P;
+    b.bstart = ctx->bstart.as<int32_t>();
+    b.sorted_e = ctx->vals2.as<int32_t>();
+    b.row_of = ctx->rowof.as<int32_t>();
+    b.bpos = ctx->bpos.as<int32_t>();
+    b.maskoff = ctx->maskoff.as<int64_t>();
+    b.bmemp = ctx->bmemp.as<int32_t>();
+    b.bmem = ctx->masked ? nullptr : ctx->keys2.as<int32_t>();  // keys are dead after bounds
+    b.posof = ctx->posof.as<int32_t>();
+    b.masks = ctx->masked ? ctx->masks.as<uint32_t>() : nullptr;
+    b.A = ctx->A.as<uint32_t>();
+    b.B = ctx->B.as<uint32_t>();
+    b.kw = ctx->kw;
+    return b;
+}
+
 // K0 on the device-resident raw inputs: vectors, relative lists, color buckets, bucket
 // commute masks (K2a), four-Russians offsets.  Everything a build computes besides the count
 // and fill passes; the benchmark times it as part of every step.
@@ -273,14 +291,8 @@ static int prep_device(pcg_ctx *ctx) {
                  n_active, ctx->L, entries, ctx->base, P, ctx->lrel.as<int32_t>(),
                  ctx->rowof.as<int32_t>(), ctx->bad.as<int32_t>() + 1, s);
     PCG_CHECK_LAUNCH(ctx);
-    int32_t bad[2] = {0, 0};
-    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(bad, ctx->bad.p, 8, cudaMemcpyDeviceToHost, s));
-    PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
-    if (bad[1]) return fail(ctx, PCG_E_COLOR, "a list color lies outside the palette");
-    if (bad[0]) {
-        rc = encode_vectors(ctx, true);
-        if (rc) return rc;
-    }
+    // (the invalid-code / invalid-color flags are read back with the bucket sizes below:
+    // invalid colors are clamped to 0 until then, and the bit planes are not consumed before)
 
     // color buckets: stable radix sort of (color, entry) in row-major entry order, so each
     // bucket lists its rows ascending
@@ -327,6 +339,8 @@ static int prep_device(pcg_ctx *ctx) {
         ctx->bstart.as<int32_t>(), P, ctx->bad.as<int32_t>() + 2);
     int32_t padded_total = 0, m_max = 0;
     int64_t mask_total = 0;
+    int32_t bad[2] = {0, 0};
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(bad, ctx->bad.p, 8, cudaMemcpyDeviceToHost, s));
     PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&m_max, ctx->bad.as<int32_t>() + 2, 4,
                                       cudaMemcpyDeviceToHost, s));
     PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&padded_total, ctx->bpos.as<int32_t>() + P, 4,
@@ -334,11 +348,20 @@ static int prep_device(pcg_ctx *ctx) {
     PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&mask_total, ctx->maskoff.as<int64_t>() + P, 8,
                                       cudaMemcpyDeviceToHost, s));
     PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+    if (bad[1]) return fail(ctx, PCG_E_COLOR, "a list color lies outside the palette");
+    if (bad[0]) {  // invalid 3-bit codes: exact raw-word predicate
+        rc = encode_vectors(ctx, true);
+        if (rc) return rc;
+    }
     // bucket masks when they fit comfortably (dense corners with huge buckets use the
-    // partner-gather row kernel instead; both are exact)
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
+    // partner-gather row kernel instead; both are exact).  Free memory is queried once per
+    // context (and again only when a decision is close), not on every build.
     const size_t mask_bytes = (size_t)mask_total * 4;
+    if (ctx->free_mem == 0 || mask_bytes > ctx->free_mem / 8) {
+        size_t total_b = 0;
+        cudaMemGetInfo(&ctx->free_mem, &total_b);
+    }
+    const size_t free_b = ctx->free_mem;
     ctx->masked = ctx->k2_mode >= 2 ||
                   (ctx->k2_mode == 0 && mask_bytes <= std::min<size_t>(free_b / 4, 24ull << 30));
     // ownership needs 12-bit member positions, 20-bit colors and <= 64 colors per list
@@ -351,19 +374,7 @@ static int prep_device(pcg_ctx *ctx) {
     PCG_ALLOC(ctx, ctx->bmemp, (size_t)(padded_total + 64) * 4);
     PCG_ALLOC(ctx, ctx->posof, (size_t)entries * 4);
     PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->bmemp.p, 0x7f, (size_t)(padded_total + 64) * 4, s));
-    BucketArgs b{};
-    b.P = P;
-    b.bstart = ctx->bstart.as<int32_t>();
-    b.sorted_e = ctx->vals2.as<int32_t>();
-    b.row_of = ctx->rowof.as<int32_t>();
-    b.bpos = ctx->bpos.as<int32_t>();
-    b.maskoff = ctx->maskoff.as<int64_t>();
-    b.bmemp = ctx->bmemp.as<int32_t>();
-    b.bmem = ctx->masked ? nullptr : ctx->keys2.as<int32_t>();  // keys are dead after bounds
-    b.posof = ctx->posof.as<int32_t>();
-    b.A = ctx->A.as<uint32_t>();
-    b.B = ctx->B.as<uint32_t>();
-    b.kw = ctx->kw;
+    BucketArgs b = bucket_args(ctx);
     launch_bucket_layout(b, entries, s);
     PCG_CHECK_LAUNCH(ctx);
     if (ctx->masked) {
@@ -409,11 +420,15 @@ static int prep_device(pcg_ctx *ctx) {
                 PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&runs_total, ctx->runoff.as<int64_t>() + entries, 8,
                                                   cudaMemcpyDeviceToHost, s));
             }
-            int32_t ovf = 0;
-            PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&ovf, o.overflow, 4, cudaMemcpyDeviceToHost, s));
-            PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
-            if (ovf) ctx->owned = false;  // a color's ownership table overflowed: dedupe path
             ctx->runs_ready = false;
+            ctx->own_check = true;  // the overflow flag is read back with the count totals
+            if (want_runs) {
+                int32_t ovf = 0;
+                PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&ovf, o.overflow, 4, cudaMemcpyDeviceToHost, s));
+                PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+                ctx->own_check = false;
+                if (ovf) ctx->owned = false;  // a color's table overflowed: dedupe path
+            }
             if (ctx->owned && want_runs &&
                 (size_t)runs_total * 4 < free_b / 3) {
                 PCG_ALLOC(ctx, ctx->runs, (size_t)(runs_total + 4) * 4);
@@ -443,8 +458,7 @@ static int prep_device(pcg_ctx *ctx) {
     ctx->prep_launches = 6 + (bad[0] ? 1 : 0) + (ctx->masked ? 1 : 0) + (fr_supported(ctx->kw) ? 1 : 0);
     if (ctx->prof) {
         cudaEventRecord(ctx->ev[11], s);
-        cudaEventSynchronize(ctx->ev[11]);
-        cudaEventElapsedTime(&ctx->ktimes[4], ctx->ev[10], ctx->ev[11]);
+        ctx->prep_timed = true;  // elapsed time read at the next host sync (count pass)
     }
     return PCG_OK;
 }
@@ -688,11 +702,27 @@ static int count_impl(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t r0, 
         PCG_CHECK_LAUNCH(ctx);
     }
     unsigned long long h[5];
+    int32_t ovf = 0;
     PCG_TRY_CUDA(ctx, cudaMemcpyAsync(h, ctx->scal.p, 40, cudaMemcpyDeviceToHost, s));
+    if (ctx->own_check)
+        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&ovf, ctx->bad.as<int32_t>() + 3, 4,
+                                          cudaMemcpyDeviceToHost, s));
     PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
     if (ctx->prof) {
+        if (ctx->prep_timed) cudaEventElapsedTime(&ctx->ktimes[4], ctx->ev[10], ctx->ev[11]);
+        ctx->prep_timed = false;
         cudaEventElapsedTime(&ctx->ktimes[0], ctx->ev[0], ctx->ev[1]);
         cudaEventElapsedTime(&ctx->ktimes[1], ctx->ev[1], ctx->ev[2]);
+    }
+    if (ctx->own_check) {
+        ctx->own_check = false;
+        if (ovf && ctx->owned) {  // a color's ownership table overflowed: plain bucket masks
+            ctx->owned = false;   // (pairs deduplicated by the row bitmap) and count again
+            BucketArgs b = bucket_args(ctx);
+            launch_bucket_masks(b, ctx->sms, s);
+            PCG_CHECK_LAUNCH(ctx);
+            return count_impl(ctx, shard, nshards, r0, r1, out, launches);
+        }
     }
     c.anticommuting = (int64_t)h[0];
     c.pairs_in_shard = pairs;
@@ -756,6 +786,7 @@ static int prefix_structures(pcg_ctx *ctx, const int32_t *deg, int64_t *n_member
                                                     ctx->compact.as<int32_t>(), n + 1, s));
     PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->cubtmp.p, t2, dv,
                                                     ctx->rowoff.as<int64_t>(), n + 1, s));
+    if (!n_members) return PCG_OK;  // caller knows the member count (no host round trip)
     int32_t nm = 0;
     PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&nm, ctx->compact.as<int32_t>() + n, 4,
                                       cudaMemcpyDeviceToHost, s));
@@ -995,10 +1026,9 @@ static int fill_impl(pcg_ctx *ctx, bool to_host, int64_t *members, int64_t *offs
     }
     if (n < 2) return PCG_OK;
     if (ctx->prof) cudaEventRecord(ctx->ev[3], s);
-    int64_t nm2 = 0;
-    int rc = prefix_structures(ctx, ctx->deg.as<int32_t>(), &nm2);
+    // the member count is the count pass's (rows with degree > 0), no readback needed
+    int rc = prefix_structures(ctx, ctx->deg.as<int32_t>(), nullptr);
     if (rc) return rc;
-    if (nm2 != nm) return fail(ctx, PCG_E_STATE, "member count mismatch");
     PCG_ALLOC(ctx, ctx->members_o, (size_t)std::max<int64_t>(nm, 1) * 8);
     PCG_ALLOC(ctx, ctx->offsets_o, (size_t)(nm + 1) * 8);
     PCG_ALLOC(ctx, ctx->nbr_o, (size_t)std::max<int64_t>(nnz, 1) * 4);

@@ -203,6 +203,9 @@ struct pcg_ctx {
     bool runs_ready = false;  // owned partner runs materialised (TMA-staged fill)
     int32_t maxdeg = 0;
     int32_t m_max = 0;        // largest color bucket of the staged build
+    size_t free_mem = 0;      // device free memory, queried once per context
+    bool own_check = false;   // ownership overflow flag still to be read (count pass)
+    bool prep_timed = false;  // prep events recorded, elapsed time pending
     int64_t mask_words = 0;   // owned/bucket mask words of the staged build
     pcg::DevBuf bnd;          // segmented fill window bounds
 };
