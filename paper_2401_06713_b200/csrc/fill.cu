@@ -14,7 +14,7 @@
 //     them; a warp exclusive scan gives every lane the output position of its segment.
 //     S is odd, so the loads of the 32 lanes hit 32 distinct banks.
 //  3. extract: uniform steps over the segment's words; in each step every lane emits the ids
-//     of its word (two unrolled, a rarely taken loop for more) into its own contiguous run of
+//     of its word (three unrolled, a rarely taken loop for more) into its own contiguous run of
 //     the row's output slice, and clears the word.
 //
 // Windows: n <= wb is one window (config 2: 100k ids = 12.8 KB of bitmap).  Larger n uses
@@ -169,14 +169,16 @@ __global__ void __launch_bounds__(SEG_MAX_WARPS * 32) k_fill_seg(RowArgs a, SegA
             for (int q = 0; q < n1; ++q)
                 desc[T0 + off1 + q] = make_int2(s1.b + 32 * (lo1 + q), (int)__ldg(masks + s1.r + (uint32_t)(lo1 + q)));
             const int T = T0 + T1;
+            const int T8 = (T + SEG_CH - 1) & ~(SEG_CH - 1);  // padded: unpredicated loads
+            if (T + lane < T8) desc[T + lane] = make_int2(0, 0);  // (mask 0: nothing admitted)
             __syncwarp();
             // ---- decode: mark admitted ids in the bitmap (plain load/or/store; non-admitted
             // lanes touch their own dummy word: no predicates to keep alive across phases)
-            for (int f0 = 0; f0 < T; f0 += SEG_CH) {
+            for (int f0 = 0; f0 < T8; f0 += SEG_CH) {
                 uint32_t addr[SEG_CH], bit[SEG_CH];
 #pragma unroll
                 for (int u = 0; u < SEG_CH; ++u) {
-                    const int2 d = f0 + u < T ? desc[f0 + u] : make_int2(0, 0);
+                    const int2 d = desc[f0 + u];
                     const int32_t x = __ldg(bmem_l + (uint32_t)d.x);
                     const uint32_t off = MULTI ? (uint32_t)(x - w0) : (uint32_t)x;
                     bool adm = ((uint32_t)d.y & lanebit) != 0u;
@@ -192,13 +194,14 @@ __global__ void __launch_bounds__(SEG_MAX_WARPS * 32) k_fill_seg(RowArgs a, SegA
                 __syncwarp();
                 uint32_t lost = 0u;
 #pragma unroll
-                for (int u = 0; u < SEG_CH; ++u) lost |= bit[u] & ~s_lds(addr[u]);
-                if (__any_sync(0xffffffffu, lost != 0u)) {  // same-word stores of this step
+                for (int u = 0; u < SEG_CH; ++u) {
+                    old[u] = bit[u] & ~s_lds(addr[u]);  // bits lost to a same-word store
+                    lost |= old[u];
+                }
+                if (__any_sync(0xffffffffu, lost != 0u)) {
 #pragma unroll
-                    for (int u = 0; u < SEG_CH; ++u) {
-                        const uint32_t l = bit[u] & ~s_lds(addr[u]);
-                        if (l) atomicOr(reinterpret_cast<uint32_t *>(__cvta_shared_to_generic(addr[u])), l);
-                    }
+                    for (int u = 0; u < SEG_CH; ++u)
+                        if (old[u]) atomicOr(reinterpret_cast<uint32_t *>(__cvta_shared_to_generic(addr[u])), old[u]);
                 }
                 __syncwarp();
             }
@@ -228,7 +231,12 @@ __global__ void __launch_bounds__(SEG_MAX_WARPS * 32) k_fill_seg(RowArgs a, SegA
                     v &= v - 1u;
                     *op++ = (OutT)(COMPACT ? __ldg(compact + j) : j);
                 }
-                while (__any_sync(0xffffffffu, v != 0u)) {  // words with 3+ ids
+                if (v) {
+                    const int32_t j = cb + __ffs(v) - 1;
+                    v &= v - 1u;
+                    *op++ = (OutT)(COMPACT ? __ldg(compact + j) : j);
+                }
+                while (__any_sync(0xffffffffu, v != 0u)) {  // words with 4+ ids
                     if (v) {
                         const int32_t j = cb + __ffs(v) - 1;
                         v &= v - 1u;
