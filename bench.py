@@ -127,6 +127,18 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(busy), "sm_max_mhz": mx, "reasons": reasons}
 
 
+def measured_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`, from the committed
+    ncu --set full capture of this bench command (profiles/roofline_traffic.json, written by
+    tools/profile_summary.py); None when no capture is committed."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
+            rec = json.load(f).get(kernel)
+        return None if rec is None else {"bytes": rec["dram_bytes_per_launch"], "source": rec["source"]}
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def measured_peaks() -> dict:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -307,9 +319,9 @@ def bench_gpu(args) -> None:
         "kernel_ms": {"commute_sweep_k1": float(kt[0]), "conflict_rows_count_k2b": float(kt[1]),
                       "conflict_rows_fill_k2b": float(kt[2]), "compaction": float(kt[3]),
                       "prep_incl_bucket_masks_k2a": float(kt[4])},
-        "roofline": {"bound": "hbm", "kernel": "conflict-row fill (k_rows_masked<fill>)",
+        "roofline": {"bound": "hbm", "kernel": "conflict-row fill (k_fill_seg)",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": None,
+                     "traffic": measured_traffic("k_fill_seg"),
                      "bytes_per_launch": int(fill_bytes),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
         "int_roofline": {"kernel": "commuting-pair sweep (k_commute_fr)", "achieved": k1_rate,
