@@ -134,7 +134,7 @@ def measured_traffic(kernel: str):
     try:
         with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
             rec = json.load(f).get(kernel)
-        return None if rec is None else {"bytes": rec["dram_bytes_per_launch"], "source": rec["source"]}
+        return None if rec is None else (float(rec["dram_bytes_per_launch"]), "profiles/" + rec["source"])
     except (OSError, ValueError, KeyError):
         return None
 
@@ -321,7 +321,8 @@ def bench_gpu(args) -> None:
                       "prep_incl_bucket_masks_k2a": float(kt[4])},
         "roofline": {"bound": "hbm", "kernel": "conflict-row fill (k_fill_seg)",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": measured_traffic("k_fill_seg"),
+                     "traffic": (measured_traffic("k_fill_seg") or (None, None))[0],
+                     "traffic_source": (measured_traffic("k_fill_seg") or (None, None))[1],
                      "bytes_per_launch": int(fill_bytes),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
         "int_roofline": {"kernel": "commuting-pair sweep (k_commute_fr)", "achieved": k1_rate,
