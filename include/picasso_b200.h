@@ -152,6 +152,20 @@ int pcg_color_dynamic(int64_t nm, const int64_t *offsets, const int64_t *neighbo
                       const int64_t *list_data, const int64_t *list_off, uint64_t *rng6,
                       int64_t *color_of, int64_t *removal_ops);
 
+/*
+ * Exhaustive properness check of a coloring (validation.py:41-131, exhaustive mode; the
+ * reference enumerates all pairs in Python and stops at 20,000 vertices, graph.py:34).
+ * words / active as in pcg_set_inputs; color (n_active,) int64: the color of each active
+ * vertex, INT64_MIN for uncolored (never a violation).  Outputs: *edges = commuting pairs
+ * (|E|, oracle_edges), *violations = commuting pairs with equal colors, and the first
+ * min(cap, *violations) of them in the reference's enumeration order (i ascending, then j)
+ * as local index pairs into pairs_out (2*cap int64).  Invalidates a staged build.
+ */
+int pcg_validate(pcg_ctx *ctx, const uint64_t *words, int64_t n_total, int32_t nwords,
+                 int32_t num_qubits, const int64_t *active, int64_t n_active,
+                 const int64_t *color, int32_t cap, int64_t *pairs_out, int64_t *violations,
+                 int64_t *edges);
+
 #ifdef __cplusplus
 }
 #endif

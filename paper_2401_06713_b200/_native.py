@@ -80,6 +80,9 @@ def library():
         lib.pcg_assign_lists.restype = ctypes.c_int
         lib.pcg_color_dynamic.argtypes = [ctypes.c_int64, _VP, _VP, _VP, _VP, _VP, _VP, _VP]
         lib.pcg_color_dynamic.restype = ctypes.c_int
+        lib.pcg_validate.argtypes = [_VP, _VP, _I64, _I32, _I32, _VP, _I64, _VP, _I32, _VP,
+                                     ctypes.POINTER(_I64), ctypes.POINTER(_I64)]
+        lib.pcg_validate.restype = ctypes.c_int
         lib.pcg_stream.argtypes = [_VP]
         lib.pcg_stream.restype = _VP
         for name in ("pcg_create", "pcg_destroy", "pcg_set_inputs", "pcg_count",
@@ -97,7 +100,7 @@ EXPORTED = (
     "pcg_copy_degrees", "pcg_fill", "pcg_fill_rows", "pcg_count_device", "pcg_fill_device",
     "pcg_build_device", "pcg_set_profiling", "pcg_kernel_times", "pcg_set_option", "pcg_stream",
     "pcg_degrees_device", "pcg_fill_rows_device", "pcg_prep_device", "pcg_color_dynamic",
-    "pcg_assign_lists",
+    "pcg_assign_lists", "pcg_validate",
 )
 
 
@@ -212,6 +215,20 @@ class Context:
                                               ctypes.c_uint64(base_key), int(P), int(L), int(base),
                                               _ptr(out)), "pcg_assign_lists")
         return out
+
+    def validate(self, words: np.ndarray, num_qubits: int, active: np.ndarray,
+                 color: np.ndarray, cap: int) -> tuple:
+        """Exhaustive properness check on the device: (violations, edges, first pairs)."""
+        words = np.ascontiguousarray(words, dtype=np.uint64)
+        active = np.ascontiguousarray(active, dtype=np.int64)
+        color = np.ascontiguousarray(color, dtype=np.int64)
+        pairs = np.empty((max(int(cap), 1), 2), dtype=np.int64)
+        nv, ne = _I64(0), _I64(0)
+        self._check(self.lib.pcg_validate(self.h, _ptr(words), int(words.shape[0]),
+                                          int(words.shape[1]), int(num_qubits), _ptr(active),
+                                          int(active.size), _ptr(color), int(cap), _ptr(pairs),
+                                          ctypes.byref(nv), ctypes.byref(ne)), "pcg_validate")
+        return int(nv.value), int(ne.value), pairs[:min(int(cap), int(nv.value))]
 
     def count_device(self) -> tuple:
         c = Counts()

@@ -1217,3 +1217,120 @@ extern "C" int pcg_assign_lists(pcg_ctx *ctx, const int64_t *active, int64_t n, 
     ctx->staged = false;  // the staging buffers now hold lists, not a build's inputs
     return rc;
 }
+
+// --------------------------------------------------------------------------------------
+// exhaustive validator (validation.py:41-131, exhaustive mode)
+// --------------------------------------------------------------------------------------
+namespace {
+struct CountAt {
+    const int64_t *c;
+    int64_t n;
+    __host__ __device__ int64_t operator()(int64_t i) const { return i < n ? c[i] : 0; }
+};
+}  // namespace
+
+extern "C" int pcg_validate(pcg_ctx *ctx, const uint64_t *words, int64_t n_total, int32_t nwords,
+                            int32_t num_qubits, const int64_t *active, int64_t n_active,
+                            const int64_t *color, int32_t cap, int64_t *pairs_out,
+                            int64_t *violations, int64_t *edges) {
+    if (!ctx || !violations || !edges) return PCG_E_ARG;
+    ctx->err.clear();
+    ctx->staged = false;  // the validator reuses the build's staging buffers
+    ctx->counted = false;
+    if (n_active < 0 || n_total < 0 || n_active > n_total || num_qubits < 1 || nwords < 1 ||
+        (int64_t)nwords * 64 < 3LL * num_qubits || n_active > (1LL << 30) || cap < 0)
+        return fail(ctx, PCG_E_ARG, "bad validation dimensions");
+    if (n_active > 0 && (!words || !active || !color)) return fail(ctx, PCG_E_ARG, "null input pointer");
+    if (cap > 0 && !pairs_out) return fail(ctx, PCG_E_ARG, "null pairs_out");
+    *violations = 0;
+    *edges = 0;
+    if (n_active < 2) return PCG_OK;
+    PCG_TRY_CUDA(ctx, cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    ctx->n_total = n_total;
+    ctx->n = n_active;
+    ctx->nwords = nwords;
+    ctx->q = num_qubits;
+    ctx->npad = round_up(n_active, K1_FR_JB);
+    PCG_ALLOC(ctx, ctx->bad, 16);
+    PCG_ALLOC(ctx, ctx->scal, 64);
+    PCG_ALLOC(ctx, ctx->words, (size_t)n_total * nwords * 8);
+    PCG_ALLOC(ctx, ctx->active, (size_t)n_active * 8);
+    PCG_ALLOC(ctx, ctx->vcolor, (size_t)n_active * 8);
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->words.p, words, (size_t)n_total * nwords * 8,
+                                      cudaMemcpyHostToDevice, s));
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->active.p, active, (size_t)n_active * 8,
+                                      cudaMemcpyHostToDevice, s));
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->vcolor.p, color, (size_t)n_active * 8,
+                                      cudaMemcpyHostToDevice, s));
+    // bit planes (raw 3-bit words when a code is invalid: the exact predicate either way)
+    int rc = encode_vectors(ctx, false);
+    if (rc) return rc;
+    int32_t bad = 0;
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&bad, ctx->bad.p, 4, cudaMemcpyDeviceToHost, s));
+    PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+    if (bad) {
+        rc = encode_vectors(ctx, true);
+        if (rc) return rc;
+    }
+    // |E|: the commuting-pair sweep (K1)
+    if (fr_supported(ctx->kw)) {
+        PCG_ALLOC(ctx, ctx->H, (size_t)ctx->npad * ctx->kw * 4 * 4);
+        launch_fr_prep(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
+        PCG_CHECK_LAUNCH(ctx);
+    }
+    PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->scal.p, 0, 64, s));
+    int64_t pairs = 0;
+    int launches = 0;
+    rc = run_k1(ctx, 0, 1, &pairs, &launches);
+    if (rc) return rc;
+    // color classes: stable sort of (color, local index)
+    const int64_t n = n_active;
+    PCG_ALLOC(ctx, ctx->vkeys, (size_t)n * 8);
+    PCG_ALLOC(ctx, ctx->vkeys2, (size_t)n * 8);
+    PCG_ALLOC(ctx, ctx->vvals, (size_t)n * 4);
+    PCG_ALLOC(ctx, ctx->vvals2, (size_t)n * 4);
+    PCG_ALLOC(ctx, ctx->vcnt, (size_t)(n + 1) * 8);
+    PCG_ALLOC(ctx, ctx->voff, (size_t)(n + 1) * 8);
+    launch_class_keys(ctx->vcolor.as<int64_t>(), n, ctx->vkeys.as<int64_t>(),
+                      ctx->vvals.as<int32_t>(), s);
+    PCG_CHECK_LAUNCH(ctx);
+    size_t tmp = 0;
+    PCG_TRY_CUDA(ctx, cub::DeviceRadixSort::SortPairs(nullptr, tmp, ctx->vkeys.as<int64_t>(),
+                                                      ctx->vkeys2.as<int64_t>(), ctx->vvals.as<int32_t>(),
+                                                      ctx->vvals2.as<int32_t>(), (int)n, 0, 64, s));
+    PCG_ALLOC(ctx, ctx->cubtmp, tmp);
+    PCG_TRY_CUDA(ctx, cub::DeviceRadixSort::SortPairs(ctx->cubtmp.p, tmp, ctx->vkeys.as<int64_t>(),
+                                                      ctx->vkeys2.as<int64_t>(), ctx->vvals.as<int32_t>(),
+                                                      ctx->vvals2.as<int32_t>(), (int)n, 0, 64, s));
+    launch_class_pairs(false, ctx->vkeys2.as<int64_t>(), ctx->vvals2.as<int32_t>(), n,
+                       ctx->A.as<uint32_t>(), ctx->B.as<uint32_t>(), ctx->kw,
+                       ctx->vcnt.as<int64_t>(), nullptr, 0, nullptr, s);
+    PCG_CHECK_LAUNCH(ctx);
+    cub::CountingInputIterator<int64_t> idx(0);
+    cub::TransformInputIterator<int64_t, CountAt, cub::CountingInputIterator<int64_t>> cv(
+        idx, CountAt{ctx->vcnt.as<int64_t>(), n});
+    size_t t2 = 0;
+    PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, t2, cv, ctx->voff.as<int64_t>(), n + 1, s));
+    PCG_ALLOC(ctx, ctx->cubtmp, t2);
+    PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->cubtmp.p, t2, cv, ctx->voff.as<int64_t>(), n + 1, s));
+    int64_t total = 0;
+    unsigned long long anti = 0;
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&total, ctx->voff.as<int64_t>() + n, 8, cudaMemcpyDeviceToHost, s));
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&anti, ctx->scal.p, 8, cudaMemcpyDeviceToHost, s));
+    PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+    *violations = total;
+    *edges = pairs - (int64_t)anti;
+    const int64_t take = std::min<int64_t>(total, cap);
+    if (take > 0) {
+        PCG_ALLOC(ctx, ctx->vpairs, (size_t)take * 16);
+        launch_class_pairs(true, ctx->vkeys2.as<int64_t>(), ctx->vvals2.as<int32_t>(), n,
+                           ctx->A.as<uint32_t>(), ctx->B.as<uint32_t>(), ctx->kw, nullptr,
+                           ctx->voff.as<int64_t>(), take, ctx->vpairs.as<int64_t>(), s);
+        PCG_CHECK_LAUNCH(ctx);
+        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(pairs_out, ctx->vpairs.p, (size_t)take * 16,
+                                          cudaMemcpyDeviceToHost, s));
+        PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+    }
+    return PCG_OK;
+}

@@ -148,6 +148,10 @@ void seg_geometry(int64_t n, int64_t max_bits, int32_t *wb, int32_t *nwin, int32
 int launch_window_bounds(const int32_t *bstart, const int32_t *bpos, const int32_t *bmemp,
                          int64_t P, int nwin, int32_t wb, int32_t *bnd, cudaStream_t s);
 int launch_fill_seg(const RowArgs &a, const SegArgs &g, bool out64, int sms, cudaStream_t s);
+int launch_class_keys(const int64_t *color, int64_t n, int64_t *keys, int32_t *vals, cudaStream_t s);
+int launch_class_pairs(bool emit, const int64_t *keys, const int32_t *vals, int64_t n,
+                       const uint32_t *A, const uint32_t *B, int32_t kw, int64_t *cnt,
+                       const int64_t *off, int64_t cap, int64_t *pairs, cudaStream_t s);
 int launch_compact(const int32_t *deg, int64_t n, const int32_t *compact, const int64_t *rowoff,
                    const int64_t *active, int64_t *members_out, int64_t *offsets_out,
                    cudaStream_t s);
@@ -208,4 +212,5 @@ struct pcg_ctx {
     bool prep_timed = false;  // prep events recorded, elapsed time pending
     int64_t mask_words = 0;   // owned/bucket mask words of the staged build
     pcg::DevBuf bnd;          // segmented fill window bounds
+    pcg::DevBuf vcolor, vkeys, vkeys2, vvals, vvals2, vcnt, voff, vpairs;  // validator
 };
