@@ -957,12 +957,12 @@ static int fill_rows_device(pcg_ctx *ctx, int64_t r0, int64_t r1, const int32_t 
         SegArgs g{};
         // measured: small windows (more warps per SM) win at config 2; at 1M ids fewer,
         // larger windows win (each window re-decodes the words that straddle its edges)
-        const int64_t max_bits = ctx->seg_bits > 0 ? ctx->seg_bits : (ctx->n <= 131072 ? 33792 : 61440);
+        const int64_t max_bits = ctx->seg_bits > 0 ? ctx->seg_bits : (ctx->n <= 131072 ? 33792 : 64512);
         seg_geometry(ctx->n, max_bits, &g.wb, &g.nwin, &g.seg);
         const int wpm = (ctx->m_max + 31) / 32;
         g.desc_cap = (ctx->lmax * (wpm + (g.nwin > 1 ? 1 : 0)) + 7) & ~7;  // x8 padding
         g.warp_words = ((g.wb >> 5) + 32 + 2 * g.desc_cap + 3) & ~3;
-        g.warps = ctx->seg_warps > 0 ? ctx->seg_warps : 2;
+        g.warps = ctx->seg_warps > 0 ? ctx->seg_warps : (ctx->n <= 131072 ? 2 : 4);
         if ((size_t)g.warp_words * 4 * g.warps <= 227u * 1024u) {
             if (g.nwin > 1) {
                 PCG_ALLOC(ctx, ctx->bnd, (size_t)ctx->P * (g.nwin + 1) * 4);

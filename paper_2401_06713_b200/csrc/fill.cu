@@ -13,9 +13,10 @@
 //  2. count: lane l owns bitmap words [l*S, l*S+S) — a contiguous id segment — and popcounts
 //     them; a warp exclusive scan gives every lane the output position of its segment.
 //     S is odd, so the loads of the 32 lanes hit 32 distinct banks.
-//  3. extract: uniform steps over the segment's words; in each step every lane emits the ids
-//     of its word (three unrolled, a rarely taken loop for more) into its own contiguous run of
-//     the row's output slice, and clears the word.
+//     The count pass also records the lane's nonzero words (a 64-bit summary; S <= 63).
+//  3. extract: each lane visits only its nonzero words (ascending), clears them and emits
+//     their ids (three unrolled, a rarely taken loop for more) into its own contiguous run of
+//     the row's output slice.  Sparse rows (1M ids, ~3k entries) skip the empty words.
 //
 // Windows: n <= wb is one window (config 2: 100k ids = 12.8 KB of bitmap).  Larger n uses
 // per-color window bounds (k_window_bounds: members below each window start), and a word that
@@ -206,22 +207,38 @@ __global__ void __launch_bounds__(SEG_MAX_WARPS * 32) k_fill_seg(RowArgs a, SegA
                 __syncwarp();
             }
             // ---- count: lane l owns words [l*S, l*S+S) — a contiguous id segment (S odd: the
-            // 32 lanes' loads hit 32 distinct banks)
+            // 32 lanes' loads hit 32 distinct banks).  The same pass records which of the
+            // lane's words are nonzero (S <= 63 bits), so extraction touches only those.
             int cnt = 0;
+            uint32_t nz0 = 0u, nz1 = 0u;
 #pragma unroll 4
-            for (int q = 0; q < S; ++q) cnt += __popc(s_lds(seg_s + (uint32_t)q * 4u));
+            for (int q = 0; q < S; ++q) {
+                const uint32_t v = s_lds(seg_s + (uint32_t)q * 4u);
+                cnt += __popc(v);
+                const uint32_t f = v != 0u ? 1u : 0u;
+                if (q < 32) nz0 |= f << q; else nz1 |= f << (q - 32);
+            }
             int tot;
             const int pos = seg_excl_scan(cnt, lane, tot);
-            // ---- extract: uniform steps over the segment's words; each lane emits the (at most
-            // two, in the common case) ids of its word into its own run of the row's slice
+            // ---- extract: each step takes the lane's next nonzero word, clears it and emits
+            // its ids (three unrolled; a rarely taken loop for more) into the lane's own run of
+            // the row's output slice
             OutT *op = orow + pos;
             const int32_t cb0 = (MULTI ? w0 : 0) + lane * S * 32;
-#pragma unroll 2
-            for (int q = 0; q < S; ++q) {
+            while (__any_sync(0xffffffffu, (nz0 | nz1) != 0u)) {
+                if ((nz0 | nz1) == 0u) continue;
+                int q;
+                if (nz0) {
+                    q = __ffs(nz0) - 1;
+                    nz0 &= nz0 - 1u;
+                } else {
+                    q = 31 + __ffs(nz1);
+                    nz1 &= nz1 - 1u;
+                }
                 uint32_t v = s_lds(seg_s + (uint32_t)q * 4u);
-                if (v) s_sts(seg_s + (uint32_t)q * 4u, 0u);
+                s_sts(seg_s + (uint32_t)q * 4u, 0u);
                 const int32_t cb = cb0 + q * 32;
-                if (v) {
+                {
                     const int32_t j = cb + __ffs(v) - 1;
                     v &= v - 1u;
                     *op++ = (OutT)(COMPACT ? __ldg(compact + j) : j);
@@ -236,12 +253,10 @@ __global__ void __launch_bounds__(SEG_MAX_WARPS * 32) k_fill_seg(RowArgs a, SegA
                     v &= v - 1u;
                     *op++ = (OutT)(COMPACT ? __ldg(compact + j) : j);
                 }
-                while (__any_sync(0xffffffffu, v != 0u)) {  // words with 4+ ids
-                    if (v) {
-                        const int32_t j = cb + __ffs(v) - 1;
-                        v &= v - 1u;
-                        *op++ = (OutT)(COMPACT ? __ldg(compact + j) : j);
-                    }
+                while (v) {  // words with 4+ ids
+                    const int32_t j = cb + __ffs(v) - 1;
+                    v &= v - 1u;
+                    *op++ = (OutT)(COMPACT ? __ldg(compact + j) : j);
                 }
             }
             orow += tot;
@@ -292,7 +307,7 @@ int run_seg(const RowArgs &a, const SegArgs &g, int sms, cudaStream_t s) {
 // loads), window wb = 1024*S bits.  `max_bits` caps the per-warp bitmap.
 void seg_geometry(int64_t n, int64_t max_bits, int32_t *wb, int32_t *nwin, int32_t *seg) {
     // S words per lane, S odd (conflict-free lane-segment loads); the window is 1024*S ids
-    int64_t smax = std::max<int64_t>(1, max_bits / 1024);
+    int64_t smax = std::min<int64_t>(63, std::max<int64_t>(1, max_bits / 1024));
     if ((smax & 1) == 0) smax -= 1;
     int64_t S = (std::max<int64_t>(n, 1) + 1023) / 1024;
     if ((S & 1) == 0) S += 1;
