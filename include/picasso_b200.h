@@ -166,6 +166,13 @@ int pcg_validate(pcg_ctx *ctx, const uint64_t *words, int64_t n_total, int32_t n
                  const int64_t *color, int32_t cap, int64_t *pairs_out, int64_t *violations,
                  int64_t *edges);
 
+/*
+ * Pin (on=1) or unpin (on=0) a host range with cudaHostRegister.  pcg_fill copies the
+ * neighbor ids straight into a pinned destination (no staging buffer); the Python layer
+ * registers its reused host output buffer once (hostpool.py).
+ */
+int pcg_host_register(void *ptr, uint64_t bytes, int32_t on);
+
 #ifdef __cplusplus
 }
 #endif

@@ -83,6 +83,8 @@ def library():
         lib.pcg_validate.argtypes = [_VP, _VP, _I64, _I32, _I32, _VP, _I64, _VP, _I32, _VP,
                                      ctypes.POINTER(_I64), ctypes.POINTER(_I64)]
         lib.pcg_validate.restype = ctypes.c_int
+        lib.pcg_host_register.argtypes = [_VP, ctypes.c_uint64, _I32]
+        lib.pcg_host_register.restype = ctypes.c_int
         lib.pcg_stream.argtypes = [_VP]
         lib.pcg_stream.restype = _VP
         for name in ("pcg_create", "pcg_destroy", "pcg_set_inputs", "pcg_count",
@@ -100,7 +102,7 @@ EXPORTED = (
     "pcg_copy_degrees", "pcg_fill", "pcg_fill_rows", "pcg_count_device", "pcg_fill_device",
     "pcg_build_device", "pcg_set_profiling", "pcg_kernel_times", "pcg_set_option", "pcg_stream",
     "pcg_degrees_device", "pcg_fill_rows_device", "pcg_prep_device", "pcg_color_dynamic",
-    "pcg_assign_lists", "pcg_validate",
+    "pcg_assign_lists", "pcg_validate", "pcg_host_register",
 )
 
 
@@ -248,6 +250,11 @@ class Context:
         n = _I32(0)
         self._check(self.lib.pcg_fill_device(self.h, ctypes.byref(n)), "pcg_fill_device")
         return int(n.value)
+
+
+def host_register(a: np.ndarray, on: bool = True) -> bool:
+    """Pin/unpin a numpy buffer for direct DMA (cudaHostRegister); False if it failed."""
+    return library().pcg_host_register(_ptr(a), ctypes.c_uint64(a.nbytes), 1 if on else 0) == PCG_OK
 
 
 _tls = threading.local()

@@ -154,8 +154,23 @@ int pcg_destroy(pcg_ctx *ctx) {
                       &ctx->scal, &ctx->bad, &ctx->members_o, &ctx->offsets_o, &ctx->nbr_o,
                       &ctx->gdeg, &ctx->items, &ctx->eidx, &ctx->bpos, &ctx->bmemp,
                       &ctx->posof, &ctx->maskoff, &ctx->masks, &ctx->heavy, &ctx->runlen,
-                      &ctx->runoff, &ctx->runs};
+                      &ctx->runoff, &ctx->runs, &ctx->bnd, &ctx->vcolor, &ctx->vkeys,
+                      &ctx->vkeys2, &ctx->vvals, &ctx->vvals2, &ctx->vcnt, &ctx->voff,
+                      &ctx->vpairs};
     for (DevBuf *b : bufs) release(*b);
+    for (void *p : ctx->ring)
+        if (p) cudaFreeHost(p);
+    for (auto &e : ctx->ring_ev) cudaEventDestroy(e);
+    for (auto &st : ctx->ring_st) cudaStreamDestroy(st);
+    for (auto &e : ctx->chunk_ev) cudaEventDestroy(e);
+    for (uint8_t *p : ctx->hbytes)
+        if (p) cudaFreeHost(p);
+    if (ctx->hxval) cudaFreeHost(ctx->hxval);
+    if (ctx->hxoff) cudaFreeHost(ctx->hxoff);
+    release(ctx->dbytes);
+    release(ctx->dxcnt);
+    release(ctx->dxoff);
+    release(ctx->dxval);
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
     for (auto &h : ctx->stage)
@@ -177,6 +192,9 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "fill_algo")) ctx->fill_algo = (int)value;
     else if (!strcmp(key, "seg_bits")) ctx->seg_bits = (int)value;
     else if (!strcmp(key, "own_algo")) ctx->own_algo = (int)value;
+    else if (!strcmp(key, "d2h_chunk")) ctx->d2h_chunk = (int)value;
+    else if (!strcmp(key, "d2h_threads")) ctx->d2h_threads = (int)value;
+    else if (!strcmp(key, "d2h_mode")) ctx->d2h_mode = (int)value;
     else if (!strcmp(key, "seg_warps")) ctx->seg_warps = (int)value;
     else return fail(ctx, PCG_E_ARG, std::string("unknown option ") + key);
     return PCG_OK;
@@ -867,42 +885,311 @@ static void widen_range(int64_t *to, const int32_t *from, size_t len) {
     for (size_t x = 0; x < len; ++x) to[x] = from[x];
 }
 
-// Same pipeline, int32 device ids widened to the API's int64 during the host-side copy, so
-// only half the bytes cross PCIe.
-static int d2h_widen(pcg_ctx *ctx, int64_t *dst, const int32_t *src, size_t count) {
+// In-place widening of one chunk: its int32 ids were copied into the upper half of the
+// chunk's own int64 range.  Ascending order never overwrites an unread id (element x's
+// int64 store ends at byte 8x+8 <= 4*len + 4x + 4, where the unread ids start), and each
+// 16-id step loads before it stores.
+__attribute__((target("avx512f"))) static void widen_inplace_avx512(int64_t *to, size_t len) {
+    const int32_t *from = reinterpret_cast<const int32_t *>(to + len) - len;
+    size_t x = 0;
+    for (; x < len && (reinterpret_cast<uintptr_t>(to + x) & 63); ++x) to[x] = from[x];
+    for (; x + 16 <= len; x += 16) {
+        const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(from + x));
+        const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(from + x + 8));
+        _mm512_stream_si512(reinterpret_cast<__m512i *>(to + x), _mm512_cvtepi32_epi64(a));
+        _mm512_stream_si512(reinterpret_cast<__m512i *>(to + x + 8), _mm512_cvtepi32_epi64(b));
+    }
+    for (; x < len; ++x) to[x] = from[x];
+    _mm_sfence();
+}
+
+static void widen_inplace(int64_t *to, size_t len) {
+    static const bool avx512 = __builtin_cpu_supports("avx512f");
+    if (avx512) {
+        widen_inplace_avx512(to, len);
+        return;
+    }
+    const int32_t *from = reinterpret_cast<const int32_t *>(to + len) - len;
+    for (size_t x = 0; x < len; ++x) {
+        const int64_t v = from[x];
+        to[x] = v;
+    }
+}
+
+// ---- byte-delta copy-out (delta.cu): decoder -------------------------------------------
+// Decodes entries [x0, x1) (a whole number of rows) from their gap bytes `g` (g[0] is entry
+// x0) into dst (int64, the API's output).  `rs` = the host offsets array (row starts),
+// `r0` = the row of x0, `xv` = exceptions (row-major), `xc` = the exception cursor at x0.
+// SIMD path: aligned 16-entry groups with no escape byte and no row start are an in-register
+// prefix sum added to the running value, widened and stored with streaming stores.
+__attribute__((target("avx512f"))) static void delta_decode_avx512(
+    int64_t *dst, const uint8_t *g, int64_t x0, int64_t x1, const int64_t *rs, int64_t r0,
+    const int32_t *xv, int64_t xc) {
+    int64_t r = r0;
+    int64_t next = rs[r0 + 1];  // first entry of the next row
+    int32_t acc = -1;
+    int64_t x = x0;
+    const __m512i zero = _mm512_setzero_si512();
+    const __m128i esc = _mm_set1_epi8((char)255);
+    while (x < x1) {
+        const bool aligned = (reinterpret_cast<uintptr_t>(dst + x) & 63) == 0 && x + 16 <= x1 &&
+                             next >= x + 16;
+        if (aligned) {
+            const __m128i v = _mm_loadu_si128(reinterpret_cast<const __m128i *>(g + (x - x0)));
+            if (_mm_movemask_epi8(_mm_cmpeq_epi8(v, esc)) == 0) {
+                __m512i t = _mm512_cvtepu8_epi32(v);
+                t = _mm512_add_epi32(t, _mm512_alignr_epi32(t, zero, 15));
+                t = _mm512_add_epi32(t, _mm512_alignr_epi32(t, zero, 14));
+                t = _mm512_add_epi32(t, _mm512_alignr_epi32(t, zero, 12));
+                t = _mm512_add_epi32(t, _mm512_alignr_epi32(t, zero, 8));
+                t = _mm512_add_epi32(t, _mm512_set1_epi32(acc));
+                _mm512_stream_si512(reinterpret_cast<__m512i *>(dst + x),
+                                    _mm512_cvtepi32_epi64(_mm512_castsi512_si256(t)));
+                _mm512_stream_si512(reinterpret_cast<__m512i *>(dst + x + 8),
+                                    _mm512_cvtepi32_epi64(_mm512_extracti64x4_epi64(t, 1)));
+                acc = _mm_extract_epi32(_mm512_extracti32x4_epi32(t, 3), 3);
+                x += 16;
+                continue;
+            }
+        }
+        // scalar step (row starts, escapes, unaligned heads and tails)
+        if (x == next) {
+            ++r;
+            next = rs[r + 1];
+            acc = -1;
+        }
+        const uint8_t b = g[x - x0];
+        acc = b == 255 ? xv[xc++] : acc + (int32_t)b;
+        dst[x] = acc;
+        ++x;
+    }
+    _mm_sfence();
+}
+
+static void delta_decode_scalar(int64_t *dst, const uint8_t *g, int64_t x0, int64_t x1,
+                                const int64_t *rs, int64_t r0, const int32_t *xv, int64_t xc) {
+    int64_t r = r0, next = rs[r0 + 1];
+    int32_t acc = -1;
+    for (int64_t x = x0; x < x1; ++x) {
+        if (x == next) {
+            ++r;
+            next = rs[r + 1];
+            acc = -1;
+        }
+        const uint8_t b = g[x - x0];
+        acc = b == 255 ? xv[xc++] : acc + (int32_t)b;
+        dst[x] = acc;
+    }
+}
+
+// Public-build copy-out of the neighbor ids: byte-delta encode on the device, copy gap bytes
+// (pipelined per worker, row-aligned chunks) + exceptions, decode on the host into `dst`.
+// `offsets` is the host copy of the CSR offsets (nm+1 entries, already transferred).
+static int d2h_delta(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, int64_t nm, int64_t nnz) {
     cudaStream_t s = ctx->stream;
-    const size_t CH = 8ull << 20;  // ids per chunk (32 MiB of int32)
-    for (int k = 0; k < 2; ++k)
-        if (!ctx->stage[k]) PCG_TRY_CUDA(ctx, cudaHostAlloc(&ctx->stage[k], 32ull << 20, cudaHostAllocDefault));
+    PCG_ALLOC(ctx, ctx->dbytes, (size_t)nnz);
+    PCG_ALLOC(ctx, ctx->dxcnt, (size_t)(nm + 1) * 4);
+    PCG_ALLOC(ctx, ctx->dxoff, (size_t)(nm + 1) * 8);
+    launch_delta(false, ctx->nbr_o.as<int32_t>(), ctx->offsets_o.as<int64_t>(), nm,
+                 ctx->dbytes.as<uint8_t>(), ctx->dxcnt.as<int32_t>(), nullptr, nullptr, ctx->sms, s);
+    PCG_CHECK_LAUNCH(ctx);
+    cub::CountingInputIterator<int64_t> idx(0);
+    cub::TransformInputIterator<int64_t, DegAt, cub::CountingInputIterator<int64_t>> xc(
+        idx, DegAt{ctx->dxcnt.as<int32_t>(), nm});
+    size_t tmp = 0;
+    PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, tmp, xc, ctx->dxoff.as<int64_t>(), nm + 1, s));
+    PCG_ALLOC(ctx, ctx->cubtmp, tmp);
+    PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->cubtmp.p, tmp, xc, ctx->dxoff.as<int64_t>(), nm + 1, s));
+    if (ctx->hxoff_cap < (size_t)(nm + 1)) {
+        if (ctx->hxoff) cudaFreeHost(ctx->hxoff);
+        ctx->hxoff = nullptr;
+        PCG_TRY_CUDA(ctx, cudaHostAlloc(reinterpret_cast<void **>(&ctx->hxoff), (size_t)(nm + 1) * 8, cudaHostAllocDefault));
+        ctx->hxoff_cap = (size_t)(nm + 1);
+    }
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->hxoff, ctx->dxoff.p, (size_t)(nm + 1) * 8, cudaMemcpyDeviceToHost, s));
+    PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+    const int64_t X = ctx->hxoff[nm];
+    PCG_ALLOC(ctx, ctx->dxval, (size_t)std::max<int64_t>(X, 1) * 4);
+    launch_delta(true, ctx->nbr_o.as<int32_t>(), ctx->offsets_o.as<int64_t>(), nm, nullptr, nullptr,
+                 ctx->dxoff.as<int64_t>(), ctx->dxval.as<int32_t>(), ctx->sms, s);
+    PCG_CHECK_LAUNCH(ctx);
+    if (ctx->hx_cap < (size_t)std::max<int64_t>(X, 1)) {
+        if (ctx->hxval) cudaFreeHost(ctx->hxval);
+        ctx->hxval = nullptr;
+        ctx->hx_cap = (size_t)std::max<int64_t>(X, 1) + ((size_t)std::max<int64_t>(X, 1) >> 2);
+        PCG_TRY_CUDA(ctx, cudaHostAlloc(reinterpret_cast<void **>(&ctx->hxval), ctx->hx_cap * 4, cudaHostAllocDefault));
+    }
+    if (X > 0)
+        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->hxval, ctx->dxval.p, (size_t)X * 4, cudaMemcpyDeviceToHost, s));
+    // row-aligned chunks of ~CH entries
+    const int64_t CH = ctx->d2h_chunk > 0 ? ctx->d2h_chunk : (int64_t)1 << 19;
+    std::vector<int64_t> cr;  // chunk row bounds
+    cr.push_back(0);
+    while (cr.back() < nm) {
+        const int64_t want = offsets[cr.back()] + CH;
+        int64_t r = std::upper_bound(offsets + cr.back() + 1, offsets + nm + 1, want) - offsets - 1;
+        if (r <= cr.back()) r = cr.back() + 1;  // a row longer than CH: its own chunk
+        cr.push_back(std::min<int64_t>(r, nm));
+    }
+    const size_t nch = cr.size() - 1;
+    size_t maxb = 0;
+    for (size_t k = 0; k < nch; ++k) maxb = std::max<size_t>(maxb, (size_t)(offsets[cr[k + 1]] - offsets[cr[k]]));
+    const int W = ctx->d2h_threads > 0 ? ctx->d2h_threads : std::min(16, omp_get_num_procs());
+    if (ctx->hbytes_cap < maxb || (int)ctx->hbytes.size() != 2 * W) {
+        for (uint8_t *p : ctx->hbytes)
+            if (p) cudaFreeHost(p);
+        ctx->hbytes.assign(2 * W, nullptr);
+        ctx->hbytes_cap = std::max<size_t>(maxb, (size_t)CH);
+        for (int k = 0; k < 2 * W; ++k)
+            PCG_TRY_CUDA(ctx, cudaHostAlloc(reinterpret_cast<void **>(&ctx->hbytes[k]), ctx->hbytes_cap, cudaHostAllocDefault));
+    }
+    while ((int)ctx->ring_ev.size() < 2 * W + 1) {
+        cudaEvent_t e;
+        PCG_TRY_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ctx->ring_ev.push_back(e);
+    }
+    while ((int)ctx->ring_st.size() < W) {
+        cudaStream_t st;
+        PCG_TRY_CUDA(ctx, cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        ctx->ring_st.push_back(st);
+    }
+    cudaEvent_t ready = ctx->ring_ev[2 * W];
+    PCG_TRY_CUDA(ctx, cudaEventRecord(ready, s));  // bytes + exceptions queued before it
+    static const bool simd = __builtin_cpu_supports("avx512f");
+    const uint8_t *src = ctx->dbytes.as<uint8_t>();
+    int failed = 0;
+#pragma omp parallel num_threads(W)
+    {
+        const int w = omp_get_thread_num();
+        cudaSetDevice(ctx->device);
+        cudaStream_t st = ctx->ring_st[w];
+        cudaStreamWaitEvent(st, ready, 0);
+        auto issue = [&](size_t k, int slot) -> cudaError_t {
+            const int64_t b0 = offsets[cr[k]], b1 = offsets[cr[k + 1]];
+            cudaError_t e = cudaMemcpyAsync(ctx->hbytes[2 * w + slot], src + b0, (size_t)(b1 - b0),
+                                            cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaEventRecord(ctx->ring_ev[2 * w + slot], st);
+            return e;
+        };
+        int slot = 0;
+        if ((size_t)w < nch && issue(w, 0) != cudaSuccess) failed = 1;
+        if (cudaEventSynchronize(ready) != cudaSuccess) failed = 1;  // exceptions on the host
+        for (size_t k = w; k < nch && !failed; k += W, slot ^= 1) {
+            if (k + W < nch && issue(k + W, slot ^ 1) != cudaSuccess) failed = 1;
+            if (cudaEventSynchronize(ctx->ring_ev[2 * w + slot]) != cudaSuccess) {
+                failed = 1;
+                break;
+            }
+            const int64_t r0 = cr[k], x0 = offsets[r0], x1 = offsets[cr[k + 1]];
+            if (simd)
+                delta_decode_avx512(dst, ctx->hbytes[2 * w + slot], x0, x1, offsets, r0, ctx->hxval,
+                                    ctx->hxoff[r0]);
+            else
+                delta_decode_scalar(dst, ctx->hbytes[2 * w + slot], x0, x1, offsets, r0, ctx->hxval,
+                                    ctx->hxoff[r0]);
+        }
+        cudaStreamSynchronize(st);
+    }
+    if (failed) return fail(ctx, PCG_E_CUDA, "delta copy-out failed");
+    return PCG_OK;
+}
+
+// D2H straight into a pinned (registered) int64 destination: every chunk's int32 ids land in
+// the upper half of its own int64 range and are widened there by the worker that owns the
+// chunk — no staging buffer, so host DRAM sees the DMA writes and the int64 stores only.
+static int d2h_widen_direct(pcg_ctx *ctx, int64_t *dst, const int32_t *src, size_t count) {
+    const size_t CH = ctx->d2h_chunk > 0 ? (size_t)ctx->d2h_chunk : (size_t)1 << 20;  // ids
+    const int W = ctx->d2h_threads > 0 ? ctx->d2h_threads : std::min(16, omp_get_num_procs());
     const size_t nch = (count + CH - 1) / CH;
     if (nch == 0) return PCG_OK;
-    auto issue = [&](size_t k) -> cudaError_t {
-        const size_t off = k * CH, len = std::min(CH, count - off);
-        cudaError_t e = cudaMemcpyAsync(ctx->stage[k & 1], src + off, len * 4,
-                                        cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess) e = cudaEventRecord(ctx->ev[6 + (k & 1)], s);
-        return e;
-    };
-    auto drain = [&](size_t k) -> cudaError_t {
-        cudaError_t e = cudaEventSynchronize(ctx->ev[6 + (k & 1)]);
-        if (e != cudaSuccess) return e;
-        const size_t off = k * CH, len = std::min(CH, count - off);
-        const int32_t *from = static_cast<const int32_t *>(ctx->stage[k & 1]);
-        int64_t *to = dst + off;
-        const int parts = 16;
-#pragma omp parallel for num_threads(std::min(16, omp_get_num_procs())) schedule(static)
-        for (int t = 0; t < parts; ++t) {
-            const size_t a = len * t / parts, b = len * (t + 1) / parts;
-            widen_range(to + a, from + a, b - a);
-        }
-        return cudaSuccess;
-    };
-    PCG_TRY_CUDA(ctx, issue(0));
-    for (size_t k = 1; k < nch; ++k) {
-        PCG_TRY_CUDA(ctx, issue(k));
-        PCG_TRY_CUDA(ctx, drain(k - 1));
+    while (ctx->chunk_ev.size() < nch) {
+        cudaEvent_t e;
+        PCG_TRY_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ctx->chunk_ev.push_back(e);
     }
-    PCG_TRY_CUDA(ctx, drain(nch - 1));
+    // all copies queued up front on the build stream (after the fill), in chunk order
+    for (size_t k = 0; k < nch; ++k) {
+        const size_t off = k * CH, len = std::min(CH, count - off);
+        int32_t *half = reinterpret_cast<int32_t *>(dst + off + len) - len;
+        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(half, src + off, len * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        PCG_TRY_CUDA(ctx, cudaEventRecord(ctx->chunk_ev[k], ctx->stream));
+    }
+    int failed = 0;
+#pragma omp parallel for num_threads(W) schedule(static, 1)
+    for (long k = 0; k < (long)nch; ++k) {
+        if (cudaEventSynchronize(ctx->chunk_ev[k]) != cudaSuccess) {
+            failed = 1;
+            continue;
+        }
+        const size_t off = (size_t)k * CH, len = std::min(CH, count - off);
+        widen_inplace(dst + off, len);
+    }
+    if (failed) return fail(ctx, PCG_E_CUDA, "direct D2H copy failed");
+    return PCG_OK;
+}
+
+// Same pipeline, int32 device ids widened to the API's int64 during the host-side copy, so
+// only half the bytes cross PCIe.  W host workers (one OpenMP region for the whole copy), each
+// with its own stream and two pinned staging chunks: worker w takes chunks w, w+W, ...; it
+// keeps the DMA of its next chunk in flight while it widens the current one, so the copy
+// engines and all host cores stay busy without a per-chunk fork/join.  (The e2e at config 2
+// is bound by host memory traffic: 0.83 GB of DMA writes and 1.66 GB of int64 stores.)
+static int d2h_widen(pcg_ctx *ctx, int64_t *dst, const int32_t *src, size_t count) {
+    const size_t CH = ctx->d2h_chunk > 0 ? (size_t)ctx->d2h_chunk : (size_t)1 << 20;  // ids
+    const int W = ctx->d2h_threads > 0 ? ctx->d2h_threads : std::min(16, omp_get_num_procs());
+    const size_t nch = (count + CH - 1) / CH;
+    if (nch == 0) return PCG_OK;
+    if (ctx->ring_bytes != CH * 4 || (int)ctx->ring.size() != 2 * W) {
+        for (void *p : ctx->ring)
+            if (p) cudaFreeHost(p);
+        ctx->ring.assign(2 * W, nullptr);
+        ctx->ring_bytes = CH * 4;
+        for (int k = 0; k < 2 * W; ++k)
+            PCG_TRY_CUDA(ctx, cudaHostAlloc(&ctx->ring[k], CH * 4, cudaHostAllocDefault));
+    }
+    while ((int)ctx->ring_ev.size() < 2 * W + 1) {
+        cudaEvent_t e;
+        PCG_TRY_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ctx->ring_ev.push_back(e);
+    }
+    while ((int)ctx->ring_st.size() < W) {
+        cudaStream_t st;
+        PCG_TRY_CUDA(ctx, cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        ctx->ring_st.push_back(st);
+    }
+    // the workers' streams start after everything queued on the build stream (the fill)
+    cudaEvent_t ready = ctx->ring_ev[2 * W];
+    PCG_TRY_CUDA(ctx, cudaEventRecord(ready, ctx->stream));
+    int failed = 0;
+#pragma omp parallel num_threads(W)
+    {
+        const int w = omp_get_thread_num();
+        cudaSetDevice(ctx->device);
+        cudaStream_t st = ctx->ring_st[w];
+        cudaStreamWaitEvent(st, ready, 0);
+        auto issue = [&](size_t k, int slot) -> cudaError_t {
+            const size_t off = k * CH, len = std::min(CH, count - off);
+            if (ctx->d2h_mode == 2) return cudaEventRecord(ctx->ring_ev[2 * w + slot], st);  // widen only
+            cudaError_t e = cudaMemcpyAsync(ctx->ring[2 * w + slot], src + off, len * 4,
+                                            cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaEventRecord(ctx->ring_ev[2 * w + slot], st);
+            return e;
+        };
+        int slot = 0;
+        if ((size_t)w < nch && issue(w, 0) != cudaSuccess) failed = 1;
+        for (size_t k = w; k < nch && !failed; k += W, slot ^= 1) {
+            if (k + W < nch && issue(k + W, slot ^ 1) != cudaSuccess) failed = 1;
+            if (cudaEventSynchronize(ctx->ring_ev[2 * w + slot]) != cudaSuccess) {
+                failed = 1;
+                break;
+            }
+            const size_t off = k * CH, len = std::min(CH, count - off);
+            if (ctx->d2h_mode != 1)  // (diagnostic mode 1: copies only)
+                widen_range(dst + off, static_cast<const int32_t *>(ctx->ring[2 * w + slot]), len);
+        }
+        cudaStreamSynchronize(st);
+    }
+    if (failed) return fail(ctx, PCG_E_CUDA, "pipelined D2H copy failed");
     return PCG_OK;
 }
 
@@ -1054,7 +1341,16 @@ static int fill_impl(pcg_ctx *ctx, bool to_host, int64_t *members, int64_t *offs
     }
     PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
     if (to_host && nnz > 0 && neighbors) {
-        rc = d2h_widen(ctx, neighbors, ctx->nbr_o.as<int32_t>(), (size_t)nnz);
+        cudaPointerAttributes at{};
+        const bool pinned = cudaPointerGetAttributes(&at, neighbors) == cudaSuccess &&
+                            at.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+        if (ctx->d2h_mode == 0 && offsets)  // byte-delta copy-out (default)
+            rc = d2h_delta(ctx, neighbors, offsets, nm, nnz);
+        else if (pinned && ctx->d2h_mode == 3)
+            rc = d2h_widen_direct(ctx, neighbors, ctx->nbr_o.as<int32_t>(), (size_t)nnz);
+        else
+            rc = d2h_widen(ctx, neighbors, ctx->nbr_o.as<int32_t>(), (size_t)nnz);
         if (rc) return rc;
     }
     if (ctx->prof) {
@@ -1331,6 +1627,19 @@ extern "C" int pcg_validate(pcg_ctx *ctx, const uint64_t *words, int64_t n_total
         PCG_TRY_CUDA(ctx, cudaMemcpyAsync(pairs_out, ctx->vpairs.p, (size_t)take * 16,
                                           cudaMemcpyDeviceToHost, s));
         PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+    }
+    return PCG_OK;
+}
+
+// Pin (register) / unpin a host range for direct DMA: the reused host output buffer of the
+// public build (hostpool.py) is registered once, so later builds copy straight into it.
+extern "C" int pcg_host_register(void *ptr, uint64_t bytes, int32_t on) {
+    if (!ptr || bytes == 0) return PCG_E_ARG;
+    cudaError_t e = on ? cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterDefault)
+                       : cudaHostUnregister(ptr);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return PCG_E_CUDA;
     }
     return PCG_OK;
 }

@@ -1,0 +1,68 @@
+// Byte-delta encoding of the conflict CSR for the device->host copy of the public build.
+//
+// The host API returns int64 neighbor ids (conflict.py:148-161), so the host must write 8
+// bytes per CSR entry; at config 2 (207M entries) the copy-out is bound by host memory
+// traffic, not by PCIe.  Rows are strictly ascending, so an entry is sent as its gap to the
+// previous entry of the row (the first entry: its value + 1): one byte when the gap is below
+// 255, else the escape byte 255 and the full id in an exception list (row-major order).  PCIe
+// carries ~1 byte per entry instead of 4, and the host reads 1 byte per 8 it writes.
+//
+//   k_delta_count : warp per row — gap bytes, exceptions per row
+//   (exclusive scan of the per-row exception counts, CUB)
+//   k_delta_exc   : warp per row — the exceptions of the row, in entry order (ballot ranks)
+#include <cub/cub.cuh>
+
+#include "pcg_internal.cuh"
+
+namespace pcg {
+
+namespace {
+
+template <bool WRITE>
+__global__ void k_delta(const int32_t *__restrict__ nbr, const int64_t *__restrict__ rowoff,
+                        int64_t rows, uint8_t *__restrict__ bytes, int32_t *__restrict__ xcount,
+                        const int64_t *__restrict__ xoff, int32_t *__restrict__ xval) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = w; r < rows; r += nw) {
+        const int64_t b = rowoff[r], e = rowoff[r + 1];
+        int cnt = 0;
+        int64_t xo = WRITE ? xoff[r] : 0;
+        for (int64_t x0 = b; x0 < e; x0 += 32) {
+            const int64_t x = x0 + lane;
+            uint32_t gap = 0u;
+            int32_t v = 0;
+            if (x < e) {
+                v = nbr[x];
+                gap = x == b ? (uint32_t)v + 1u : (uint32_t)(v - nbr[x - 1]);
+            }
+            const bool esc = x < e && gap >= 255u;
+            const uint32_t bal = __ballot_sync(0xffffffffu, esc);
+            if (!WRITE) {
+                if (x < e) bytes[x] = esc ? (uint8_t)255 : (uint8_t)gap;
+                cnt += __popc(bal);
+            } else {
+                if (esc) xval[xo + __popc(bal & ((1u << lane) - 1u))] = v;
+                xo += __popc(bal);
+            }
+        }
+        if (!WRITE && lane == 0) xcount[r] = cnt;
+    }
+}
+
+}  // namespace
+
+int launch_delta(bool write, const int32_t *nbr, const int64_t *rowoff, int64_t rows,
+                 uint8_t *bytes, int32_t *xcount, const int64_t *xoff, int32_t *xval, int sms,
+                 cudaStream_t s) {
+    if (rows <= 0) return 0;
+    const int64_t grid = std::min<int64_t>((rows + 7) / 8, (int64_t)sms * 16);
+    if (write)
+        k_delta<true><<<(unsigned)grid, 256, 0, s>>>(nbr, rowoff, rows, bytes, xcount, xoff, xval);
+    else
+        k_delta<false><<<(unsigned)grid, 256, 0, s>>>(nbr, rowoff, rows, bytes, xcount, xoff, xval);
+    return 1;
+}
+
+}  // namespace pcg

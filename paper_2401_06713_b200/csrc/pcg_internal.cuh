@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "../../include/picasso_b200.h"
 
@@ -148,6 +149,9 @@ void seg_geometry(int64_t n, int64_t max_bits, int32_t *wb, int32_t *nwin, int32
 int launch_window_bounds(const int32_t *bstart, const int32_t *bpos, const int32_t *bmemp,
                          int64_t P, int nwin, int32_t wb, int32_t *bnd, cudaStream_t s);
 int launch_fill_seg(const RowArgs &a, const SegArgs &g, bool out64, int sms, cudaStream_t s);
+int launch_delta(bool write, const int32_t *nbr, const int64_t *rowoff, int64_t rows,
+                 uint8_t *bytes, int32_t *xcount, const int64_t *xoff, int32_t *xval, int sms,
+                 cudaStream_t s);
 int launch_class_keys(const int64_t *color, int64_t n, int64_t *keys, int32_t *vals, cudaStream_t s);
 int launch_class_pairs(bool emit, const int64_t *keys, const int32_t *vals, int64_t n,
                        const uint32_t *A, const uint32_t *B, int32_t kw, int64_t *cnt,
@@ -213,4 +217,21 @@ struct pcg_ctx {
     int64_t mask_words = 0;   // owned/bucket mask words of the staged build
     pcg::DevBuf bnd;          // segmented fill window bounds
     pcg::DevBuf vcolor, vkeys, vkeys2, vvals, vvals2, vcnt, voff, vpairs;  // validator
+    // pipelined D2H of the neighbor ids: ring of pinned staging chunks
+    int d2h_chunk = 0;        // ids per chunk (0 auto)
+    int d2h_threads = 0;      // host widening threads (0 auto)
+    int d2h_mode = 0;         // 0 byte-delta copy-out; 3 direct int32 copy into pinned
+                              // memory; 4 staged int32 copy; 1/2 diagnostics (copies /
+                              // widening only, staged path)
+    std::vector<void *> ring;
+    size_t ring_bytes = 0;
+    std::vector<cudaEvent_t> ring_ev;
+    std::vector<cudaStream_t> ring_st;
+    std::vector<cudaEvent_t> chunk_ev;  // direct D2H: one event per chunk
+    pcg::DevBuf dbytes, dxcnt, dxoff, dxval;  // byte-delta encoded CSR (public-build copy-out)
+    std::vector<uint8_t *> hbytes;             // pinned per-worker byte staging
+    size_t hbytes_cap = 0;
+    int32_t *hxval = nullptr;                  // pinned exceptions + per-row offsets
+    int64_t *hxoff = nullptr;
+    size_t hx_cap = 0, hxoff_cap = 0;
 };

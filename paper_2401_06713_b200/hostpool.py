@@ -12,6 +12,11 @@ Ownership is exact.  A buffer is reused only when the pool holds the sole refere
 (``sys.getrefcount``).  Every array carved from it keeps it alive through numpy's ``.base``
 chain, so a result the caller still holds is never overwritten.
 
+Once a buffer is reused it is also pinned (``cudaHostRegister``, once), and ``pcg_fill``
+copies the neighbor ids straight into it and widens them in place: no staging buffer, so
+host DRAM sees only the DMA writes and the int64 stores (the e2e at config 2 is bound by host
+memory traffic).  ``PICASSO_HOST_PIN=0`` keeps the staged copy.
+
 ``PICASSO_HOST_POOL=0`` disables the pool.  ``release()`` frees the cached buffer.
 """
 
@@ -20,6 +25,7 @@ from __future__ import annotations
 import os
 import sys
 import threading
+import weakref
 
 import numpy as np
 
@@ -42,11 +48,37 @@ def empty_int64(count: int) -> np.ndarray:
         b = _buf
         # references: the module global + the local ``b`` + getrefcount's argument
         if b is not None and b.size >= count and sys.getrefcount(b) <= 3:
+            _pin(b)
             return b[:count]
         # busy or too small: the new buffer becomes the pooled one (a busy old buffer now
         # lives only as long as the caller's result)
         _buf = np.empty(count, dtype=np.int64)
         return _buf
+
+
+_pinned: set = set()
+
+
+def _pin(b: np.ndarray) -> None:
+    """Register a reused buffer for direct DMA (once; unregistered when it is freed).  The
+    build then copies the neighbor ids straight into it, without a staging buffer."""
+    if id(b) in _pinned or os.environ.get("PICASSO_HOST_PIN", "1") == "0":
+        return
+    from . import _native
+
+    if _native.host_register(b, True):
+        key = id(b)
+        _pinned.add(key)
+        ptr, nbytes = b.ctypes.data, b.nbytes
+
+        def unpin(ptr=ptr, nbytes=nbytes, key=key):
+            _pinned.discard(key)
+            try:
+                _native.library().pcg_host_register(ptr, nbytes, 0)
+            except Exception:  # noqa: BLE001 - interpreter shutdown
+                pass
+
+        weakref.finalize(b, unpin)
 
 
 def release() -> None:

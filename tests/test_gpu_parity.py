@@ -340,3 +340,46 @@ def test_whole_run_50k_recorded_golden(golden_ref):
     assert res.oracle_edges == r["oracle_edges"]
     assert res.peak_conflict_edges == r["peak_conflict_edges"]
     assert sha(res.color) == r["color_sha"]
+
+
+def test_pinned_direct_copy_matches(golden_ref):
+    """The second build reuses (and pins) the pooled host buffer: neighbor ids are copied
+    straight into it and widened in place.  Both copies give the reference CSR."""
+    from paper_2401_06713_b200 import hostpool
+
+    g = golden_ref["builds_hashed"]["q32_n20000"]
+    v = pauli_view(20000, 32, 0)
+    lists = random_lists(v, seed=0)
+    for _ in range(3):
+        gc = b200.build(v, lists)
+        assert gc.graph.neighbors.nbytes >= hostpool.MIN_POOLED_BYTES
+        assert sha(gc.graph.neighbors) == g["neighbors_sha"]
+        assert sha(gc.graph.offsets) == g["offsets_sha"]
+        gc = None
+
+
+@pytest.mark.parametrize("n,pct,alpha", [(3000, 12.5, 2.0), (40000, 40.0, 0.6), (70000, 25.0, 1.0)])
+def test_delta_copy_out_matches_widened_copy(n, pct, alpha):
+    """The public build ships CSR gaps as bytes (escapes to an exception list for gaps >= 255
+    and first entries) and decodes them on the host; the plain int32 copy-out (option
+    d2h_mode 4) must give the same arrays, for dense and very sparse rows (long gaps) and
+    for fresh (unaligned) and pooled destinations."""
+    ps = b200.PauliSet.from_strings(b200.random_pauli_strings(n, 32, seed=11))
+    v = b200.pauli_view(ps)
+    plan = b200.plan_iteration(1, n, b200.PaletteParams(pct, alpha, seed=3))
+    lists = b200.assign_random_lists(plan, v.active, 3)
+    ctx = _native.context()
+    try:
+        ctx.option("d2h_mode", 4)
+        want = b200.build(v, lists)
+        ref = (want.graph.offsets.copy(), want.graph.neighbors.copy(), want.members.copy())
+        want = None
+        ctx.option("d2h_mode", 0)
+        for _ in range(2):
+            got = b200.build(v, lists)
+            assert np.array_equal(got.graph.offsets, ref[0])
+            assert np.array_equal(got.members, ref[2])
+            assert np.array_equal(got.graph.neighbors, ref[1])
+            got = None
+    finally:
+        ctx.option("d2h_mode", 0)
