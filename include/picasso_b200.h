@@ -173,6 +173,10 @@ int pcg_validate(pcg_ctx *ctx, const uint64_t *words, int64_t n_total, int32_t n
  */
 int pcg_host_register(void *ptr, uint64_t bytes, int32_t on);
 
+/* Bytes the last pcg_fill copied device -> host: members, offsets and the neighbor ids
+ * (sent as byte gaps + an exception list and decoded into the int64 output on the host). */
+int64_t pcg_last_copy_bytes(const pcg_ctx *ctx);
+
 #ifdef __cplusplus
 }
 #endif

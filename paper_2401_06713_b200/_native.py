@@ -85,6 +85,8 @@ def library():
         lib.pcg_validate.restype = ctypes.c_int
         lib.pcg_host_register.argtypes = [_VP, ctypes.c_uint64, _I32]
         lib.pcg_host_register.restype = ctypes.c_int
+        lib.pcg_last_copy_bytes.argtypes = [_VP]
+        lib.pcg_last_copy_bytes.restype = ctypes.c_int64
         lib.pcg_stream.argtypes = [_VP]
         lib.pcg_stream.restype = _VP
         for name in ("pcg_create", "pcg_destroy", "pcg_set_inputs", "pcg_count",
@@ -102,7 +104,7 @@ EXPORTED = (
     "pcg_copy_degrees", "pcg_fill", "pcg_fill_rows", "pcg_count_device", "pcg_fill_device",
     "pcg_build_device", "pcg_set_profiling", "pcg_kernel_times", "pcg_set_option", "pcg_stream",
     "pcg_degrees_device", "pcg_fill_rows_device", "pcg_prep_device", "pcg_color_dynamic",
-    "pcg_assign_lists", "pcg_validate", "pcg_host_register",
+    "pcg_assign_lists", "pcg_validate", "pcg_host_register", "pcg_last_copy_bytes",
 )
 
 
@@ -145,6 +147,9 @@ class Context:
         if rc == PCG_E_OOM:
             raise MemoryError(f"{what}: {msg}")
         raise DeviceError(f"{what} failed (code {rc}): {msg}")
+
+    def last_copy_bytes(self) -> int:
+        return int(self.lib.pcg_last_copy_bytes(self.h))
 
     def stream_handle(self) -> int:
         return int(self.lib.pcg_stream(self.h) or 0)

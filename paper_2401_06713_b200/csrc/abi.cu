@@ -1021,6 +1021,7 @@ static int d2h_delta(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, int64_t
     }
     if (X > 0)
         PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->hxval, ctx->dxval.p, (size_t)X * 4, cudaMemcpyDeviceToHost, s));
+    ctx->copy_bytes += (int64_t)nnz + X * 4 + (nm + 1) * 8;  // gap bytes, exceptions, offsets
     // row-aligned chunks of ~CH entries
     const int64_t CH = ctx->d2h_chunk > 0 ? ctx->d2h_chunk : (int64_t)1 << 19;
     std::vector<int64_t> cr;  // chunk row bounds
@@ -1332,6 +1333,7 @@ static int fill_impl(pcg_ctx *ctx, bool to_host, int64_t *members, int64_t *offs
     }
     if (ctx->prof) cudaEventRecord(ctx->ev[5], s);
     if (to_host) {
+        ctx->copy_bytes = (nm > 0 && members ? nm * 8 : 0) + (offsets ? (nm + 1) * 8 : 0);
         if (nm > 0 && members)
             PCG_TRY_CUDA(ctx, cudaMemcpyAsync(members, ctx->members_o.p, nm * 8,
                                               cudaMemcpyDeviceToHost, s));
@@ -1351,6 +1353,7 @@ static int fill_impl(pcg_ctx *ctx, bool to_host, int64_t *members, int64_t *offs
             rc = d2h_widen_direct(ctx, neighbors, ctx->nbr_o.as<int32_t>(), (size_t)nnz);
         else
             rc = d2h_widen(ctx, neighbors, ctx->nbr_o.as<int32_t>(), (size_t)nnz);
+        if (ctx->d2h_mode != 0 || !offsets) ctx->copy_bytes += nnz * 4;
         if (rc) return rc;
     }
     if (ctx->prof) {
@@ -1643,3 +1646,7 @@ extern "C" int pcg_host_register(void *ptr, uint64_t bytes, int32_t on) {
     }
     return PCG_OK;
 }
+
+// Bytes the last pcg_fill copied device -> host (members, offsets and the encoded neighbor
+// ids), for the benchmark's e2e accounting.
+extern "C" int64_t pcg_last_copy_bytes(const pcg_ctx *ctx) { return ctx ? ctx->copy_bytes : 0; }

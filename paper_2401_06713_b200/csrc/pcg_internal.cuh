@@ -228,6 +228,7 @@ struct pcg_ctx {
     std::vector<cudaEvent_t> ring_ev;
     std::vector<cudaStream_t> ring_st;
     std::vector<cudaEvent_t> chunk_ev;  // direct D2H: one event per chunk
+    int64_t copy_bytes = 0;                    // D2H bytes of the last pcg_fill
     pcg::DevBuf dbytes, dxcnt, dxoff, dxval;  // byte-delta encoded CSR (public-build copy-out)
     std::vector<uint8_t *> hbytes;             // pinned per-worker byte staging
     size_t hbytes_cap = 0;
