@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(SEG_MAX_WARPS * 32) k_fill_seg(RowArgs a, SegA
         for (int k = 0; k < g.nwin; ++k) {
             const int32_t w0 = k * g.wb;
             const uint32_t wlen = (uint32_t)(min((int64_t)a.n, (int64_t)w0 + g.wb) - w0);
+            const uint32_t wbase_s = bm_s - (uint32_t)(w0 >> 5) * 4u;  // bitmap word of id 0
             // ---- descriptors of the words of this window, flattened over the row's colors:
             // (first bucket position of the word, the owned mask word itself)
             int lo0 = 0, n0 = s0.W, lo1 = 0, n1 = s1.W;
@@ -181,11 +182,11 @@ __global__ void __launch_bounds__(SEG_MAX_WARPS * 32) k_fill_seg(RowArgs a, SegA
                 for (int u = 0; u < SEG_CH; ++u) {
                     const int2 d = desc[f0 + u];
                     const int32_t x = __ldg(bmem_l + (uint32_t)d.x);
-                    const uint32_t off = MULTI ? (uint32_t)(x - w0) : (uint32_t)x;
                     bool adm = ((uint32_t)d.y & lanebit) != 0u;
-                    if (MULTI) adm = adm && off < wlen;
-                    addr[u] = adm ? bm_s + ((off >> 5) << 2) : dummy_s;
-                    bit[u] = adm ? (1u << (off & 31)) : 0u;
+                    if (MULTI) adm = adm && (uint32_t)(x - w0) < wlen;
+                    // w0 is a multiple of 32: the window base folds into the bitmap address
+                    addr[u] = adm ? wbase_s + ((uint32_t)x >> 5) * 4u : dummy_s;
+                    bit[u] = adm ? (1u << (x & 31)) : 0u;
                 }
                 uint32_t old[SEG_CH];
 #pragma unroll
@@ -210,14 +211,22 @@ __global__ void __launch_bounds__(SEG_MAX_WARPS * 32) k_fill_seg(RowArgs a, SegA
             // 32 lanes' loads hit 32 distinct banks).  The same pass records which of the
             // lane's words are nonzero (S <= 63 bits), so extraction touches only those.
             int cnt = 0;
-            uint32_t nz0 = 0u, nz1 = 0u;
+            uint32_t ra = 0u, rb = 0u;  // nonzero flags, shifted in (word q at bit S1-1-q)
+            const int S1 = min(S, 32);
 #pragma unroll 4
-            for (int q = 0; q < S; ++q) {
+            for (int q = 0; q < S1; ++q) {
                 const uint32_t v = s_lds(seg_s + (uint32_t)q * 4u);
                 cnt += __popc(v);
-                const uint32_t f = v != 0u ? 1u : 0u;
-                if (q < 32) nz0 |= f << q; else nz1 |= f << (q - 32);
+                ra = (ra << 1) | min(v, 1u);
             }
+#pragma unroll 4
+            for (int q = 32; q < S; ++q) {
+                const uint32_t v = s_lds(seg_s + (uint32_t)q * 4u);
+                cnt += __popc(v);
+                rb = (rb << 1) | min(v, 1u);
+            }
+            uint32_t nz0 = __brev(ra) >> (32 - S1);                  // bit q <-> word q
+            uint32_t nz1 = S > 32 ? __brev(rb) >> (64 - S) : 0u;     // bit q-32 <-> word q
             int tot;
             const int pos = seg_excl_scan(cnt, lane, tot);
             // ---- extract: each step takes the lane's next nonzero word, clears it and emits
@@ -225,38 +234,34 @@ __global__ void __launch_bounds__(SEG_MAX_WARPS * 32) k_fill_seg(RowArgs a, SegA
             // the row's output slice
             OutT *op = orow + pos;
             const int32_t cb0 = (MULTI ? w0 : 0) + lane * S * 32;
-            while (__any_sync(0xffffffffu, (nz0 | nz1) != 0u)) {
-                if ((nz0 | nz1) == 0u) continue;
-                int q;
-                if (nz0) {
-                    q = __ffs(nz0) - 1;
-                    nz0 &= nz0 - 1u;
-                } else {
-                    q = 31 + __ffs(nz1);
-                    nz1 &= nz1 - 1u;
-                }
+            uint64_t nz = ((uint64_t)nz1 << 32) | nz0;
+            int e = 0;
+            while (__any_sync(0xffffffffu, nz != 0ull)) {
+                if (nz == 0ull) continue;
+                const int q = __ffsll((long long)nz) - 1;
+                nz &= nz - 1ull;
                 uint32_t v = s_lds(seg_s + (uint32_t)q * 4u);
                 s_sts(seg_s + (uint32_t)q * 4u, 0u);
                 const int32_t cb = cb0 + q * 32;
                 {
                     const int32_t j = cb + __ffs(v) - 1;
                     v &= v - 1u;
-                    *op++ = (OutT)(COMPACT ? __ldg(compact + j) : j);
+                    op[e++] = (OutT)(COMPACT ? __ldg(compact + j) : j);
                 }
                 if (v) {
                     const int32_t j = cb + __ffs(v) - 1;
                     v &= v - 1u;
-                    *op++ = (OutT)(COMPACT ? __ldg(compact + j) : j);
+                    op[e++] = (OutT)(COMPACT ? __ldg(compact + j) : j);
                 }
                 if (v) {
                     const int32_t j = cb + __ffs(v) - 1;
                     v &= v - 1u;
-                    *op++ = (OutT)(COMPACT ? __ldg(compact + j) : j);
+                    op[e++] = (OutT)(COMPACT ? __ldg(compact + j) : j);
                 }
                 while (v) {  // words with 4+ ids
                     const int32_t j = cb + __ffs(v) - 1;
                     v &= v - 1u;
-                    *op++ = (OutT)(COMPACT ? __ldg(compact + j) : j);
+                    op[e++] = (OutT)(COMPACT ? __ldg(compact + j) : j);
                 }
             }
             orow += tot;
