@@ -243,6 +243,7 @@ def bench_gpu(args) -> None:
     ctx = _native.context(local)
     ctx.profiling(True)
     stage(view, lists, ctx)  # H2D of the inputs: not part of `value`
+    ctx.option("k1_async", 1)  # K1 (view_edges_scanned only) next to the conflict-row passes
     stream = torch.cuda.ExternalStream(ctx.stream_handle())
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 

@@ -173,6 +173,14 @@ int pcg_validate(pcg_ctx *ctx, const uint64_t *words, int64_t n_total, int32_t n
  */
 int pcg_host_register(void *ptr, uint64_t bytes, int32_t on);
 
+/*
+ * With the option "k1_async" set, pcg_count launches the commuting-pair sweep (K1) on a side
+ * stream next to the conflict-row passes and returns anticommuting = -1; this call waits for
+ * it and returns the anticommuting count (view_edges_scanned = pairs_in_shard - it).
+ * Without the option it returns the count pcg_count already reported.
+ */
+int pcg_k1_result(pcg_ctx *ctx, int64_t *anticommuting);
+
 /* Bytes the last pcg_fill copied device -> host: members, offsets and the neighbor ids
  * (sent as byte gaps + an exception list and decoded into the int64 output on the host). */
 int64_t pcg_last_copy_bytes(const pcg_ctx *ctx);

@@ -85,6 +85,8 @@ def library():
         lib.pcg_validate.restype = ctypes.c_int
         lib.pcg_host_register.argtypes = [_VP, ctypes.c_uint64, _I32]
         lib.pcg_host_register.restype = ctypes.c_int
+        lib.pcg_k1_result.argtypes = [_VP, ctypes.POINTER(_I64)]
+        lib.pcg_k1_result.restype = ctypes.c_int
         lib.pcg_last_copy_bytes.argtypes = [_VP]
         lib.pcg_last_copy_bytes.restype = ctypes.c_int64
         lib.pcg_stream.argtypes = [_VP]
@@ -105,6 +107,7 @@ EXPORTED = (
     "pcg_build_device", "pcg_set_profiling", "pcg_kernel_times", "pcg_set_option", "pcg_stream",
     "pcg_degrees_device", "pcg_fill_rows_device", "pcg_prep_device", "pcg_color_dynamic",
     "pcg_assign_lists", "pcg_validate", "pcg_host_register", "pcg_last_copy_bytes",
+    "pcg_k1_result",
 )
 
 
@@ -147,6 +150,12 @@ class Context:
         if rc == PCG_E_OOM:
             raise MemoryError(f"{what}: {msg}")
         raise DeviceError(f"{what} failed (code {rc}): {msg}")
+
+    def k1_result(self) -> int:
+        """Anticommuting pairs of the last count (waits for an asynchronous K1)."""
+        a = _I64(0)
+        self._check(self.lib.pcg_k1_result(self.h, ctypes.byref(a)), "pcg_k1_result")
+        return int(a.value)
 
     def last_copy_bytes(self) -> int:
         return int(self.lib.pcg_last_copy_bytes(self.h))

@@ -150,9 +150,14 @@ def build(view, lists, *, edge_budget: Optional[int] = None, threads: int = 1,
     CG, EG = _result_types(view)
     ctx = stage(view, lists)
     n = view.n_active
-    c = ctx.count(0, 1, 0, n)
+    # the commuting-pair sweep (view_edges_scanned only) runs on a side stream next to the
+    # conflict-row passes and the copy-out; its count is collected after the fill
+    ctx.option("k1_async", 1)
+    try:
+        c = ctx.count(0, 1, 0, n)
+    finally:
+        ctx.option("k1_async", 0)
     total = int(c.deg_sum) // 2
-    scanned = int(c.pairs_in_shard - c.anticommuting)
     last_stats.n_active = n
     last_stats.raw_words_mode = bool(c.raw_words_mode)
     last_stats.deg_upper_sum = int(c.deg_upper_sum)
@@ -167,6 +172,7 @@ def build(view, lists, *, edge_budget: Optional[int] = None, threads: int = 1,
     offsets = np.empty(nm + 1, dtype=np.int64)
     neighbors = hostpool.empty_int64(2 * total)
     ctx.fill(members, offsets, neighbors)
+    scanned = int(c.pairs_in_shard - ctx.k1_result())
     if nm == 0:
         offsets[0] = 0
     return CG(members=members, graph=EG(n=nm, offsets=offsets, neighbors=neighbors),

@@ -163,6 +163,9 @@ int pcg_destroy(pcg_ctx *ctx) {
     for (auto &e : ctx->ring_ev) cudaEventDestroy(e);
     for (auto &st : ctx->ring_st) cudaStreamDestroy(st);
     for (auto &e : ctx->chunk_ev) cudaEventDestroy(e);
+    if (ctx->k1_stream) cudaStreamDestroy(ctx->k1_stream);
+    if (ctx->k1_fork) cudaEventDestroy(ctx->k1_fork);
+    if (ctx->k1_done) cudaEventDestroy(ctx->k1_done);
     for (uint8_t *p : ctx->hbytes)
         if (p) cudaFreeHost(p);
     if (ctx->hxval) cudaFreeHost(ctx->hxval);
@@ -195,6 +198,7 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "d2h_chunk")) ctx->d2h_chunk = (int)value;
     else if (!strcmp(key, "d2h_threads")) ctx->d2h_threads = (int)value;
     else if (!strcmp(key, "d2h_mode")) ctx->d2h_mode = (int)value;
+    else if (!strcmp(key, "k1_async")) ctx->k1_async = (int)value;
     else if (!strcmp(key, "seg_warps")) ctx->seg_warps = (int)value;
     else return fail(ctx, PCG_E_ARG, std::string("unknown option ") + key);
     return PCG_OK;
@@ -275,6 +279,12 @@ __global__ void k_iota(int32_t *x, int64_t n) {
 }  // namespace pcg_prep
 using namespace pcg_prep;
 
+// A K1 still running on the side stream reads the bit planes and adds into scal[0]: the main
+// stream waits for it before either is rewritten.
+static void k1_join(pcg_ctx *ctx) {
+    if (ctx->k1_pending && ctx->k1_done) cudaStreamWaitEvent(ctx->stream, ctx->k1_done, 0);
+}
+
 static BucketArgs bucket_args(const pcg_ctx *ctx) {
     BucketArgs b{};
     b.P = ctx->P;
@@ -298,6 +308,7 @@ static BucketArgs bucket_args(const pcg_ctx *ctx) {
 // and fill passes; the benchmark times it as part of every step.
 static int prep_device(pcg_ctx *ctx) {
     cudaStream_t s = ctx->stream;
+    k1_join(ctx);
     const int64_t n_active = ctx->n, entries = ctx->entries, P = ctx->P;
     if (n_active == 0) return PCG_OK;
     if (ctx->prof) cudaEventRecord(ctx->ev[10], s);
@@ -488,6 +499,8 @@ extern "C" int pcg_set_inputs(pcg_ctx *ctx, const uint64_t *words, int64_t n_tot
                               int64_t palette_size) {
     if (!ctx) return PCG_E_ARG;
     ctx->err.clear();
+    if (ctx->k1_pending && ctx->k1_done) cudaEventSynchronize(ctx->k1_done);  // planes reused
+    ctx->k1_pending = false;
     ctx->staged = false;
     ctx->counted = false;
     if (n_active < 0 || n_total < 0 || n_active > n_total || num_qubits < 1 || nwords < 1 ||
@@ -595,8 +608,8 @@ static int64_t direct_pairs(int64_t n, int64_t T, int64_t t0, int64_t t1) {
     return p;
 }
 
-static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, int *launches) {
-    cudaStream_t s = ctx->stream;
+static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, int *launches,
+                  cudaStream_t s) {
     unsigned long long *anti = ctx->scal.as<unsigned long long>();
     const int64_t n = ctx->n;
     if (k1_algo(ctx) == 2) {
@@ -684,6 +697,7 @@ static int count_impl(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t r0, 
         return fail(ctx, PCG_E_ARG, "bad shard or row range");
     PCG_TRY_CUDA(ctx, cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
+    k1_join(ctx);
     pcg_counts c{};
     c.n_active = ctx->n;
     c.raw_words_mode = ctx->raw ? 1 : 0;
@@ -702,11 +716,29 @@ static int count_impl(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t r0, 
         return PCG_OK;
     }
     PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->scal.p, 0, 40, s));
-    if (ctx->prof) cudaEventRecord(ctx->ev[0], s);
     int64_t pairs = 0;
-    int rc = run_k1(ctx, shard, nshards, &pairs, launches);
+    int rc;
+    // K1 only produces view_edges_scanned: with k1_async it runs on a side stream next to the
+    // conflict-row passes and its count is collected later (pcg_k1_result)
+    const bool async = ctx->k1_async && nshards == 1;
+    cudaStream_t ks = s;
+    if (async) {
+        if (!ctx->k1_stream) PCG_TRY_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->k1_stream, cudaStreamNonBlocking));
+        if (!ctx->k1_fork) PCG_TRY_CUDA(ctx, cudaEventCreateWithFlags(&ctx->k1_fork, cudaEventDisableTiming));
+        if (!ctx->k1_done) PCG_TRY_CUDA(ctx, cudaEventCreateWithFlags(&ctx->k1_done, cudaEventDisableTiming));
+        ks = ctx->k1_stream;
+        PCG_TRY_CUDA(ctx, cudaEventRecord(ctx->k1_fork, s));
+        PCG_TRY_CUDA(ctx, cudaStreamWaitEvent(ks, ctx->k1_fork, 0));
+    }
+    if (ctx->prof) cudaEventRecord(ctx->ev[0], ks);
+    rc = run_k1(ctx, shard, nshards, &pairs, launches, ks);
     if (rc) return rc;
-    if (ctx->prof) cudaEventRecord(ctx->ev[1], s);
+    if (ctx->prof) cudaEventRecord(ctx->ev[1], ks);
+    if (async) {
+        PCG_TRY_CUDA(ctx, cudaEventRecord(ctx->k1_done, ks));
+        ctx->k1_pending = true;
+    }
+    if (ctx->prof) cudaEventRecord(ctx->ev[8], s);
     const RowArgs a = row_args(ctx, r0, r1);
     *launches += ctx->owned ? launch_count_owned(a, ctx->sms, s)
                             : launch_rows(a, false, false, ctx->sms, s);
@@ -729,8 +761,8 @@ static int count_impl(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t r0, 
     if (ctx->prof) {
         if (ctx->prep_timed) cudaEventElapsedTime(&ctx->ktimes[4], ctx->ev[10], ctx->ev[11]);
         ctx->prep_timed = false;
-        cudaEventElapsedTime(&ctx->ktimes[0], ctx->ev[0], ctx->ev[1]);
-        cudaEventElapsedTime(&ctx->ktimes[1], ctx->ev[1], ctx->ev[2]);
+        if (!async) cudaEventElapsedTime(&ctx->ktimes[0], ctx->ev[0], ctx->ev[1]);
+        cudaEventElapsedTime(&ctx->ktimes[1], ctx->ev[8], ctx->ev[2]);
     }
     if (ctx->own_check) {
         ctx->own_check = false;
@@ -742,7 +774,7 @@ static int count_impl(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t r0, 
             return count_impl(ctx, shard, nshards, r0, r1, out, launches);
         }
     }
-    c.anticommuting = (int64_t)h[0];
+    c.anticommuting = async ? -1 : (int64_t)h[0];  // -1: pending, see pcg_k1_result
     c.pairs_in_shard = pairs;
     c.deg_sum = (int64_t)h[1];
     c.deg_upper_sum = (int64_t)h[2];
@@ -1377,6 +1409,22 @@ extern "C" int pcg_count_device(pcg_ctx *ctx, pcg_counts *out, int32_t *launches
     return rc;
 }
 
+extern "C" int pcg_k1_result(pcg_ctx *ctx, int64_t *anticommuting) {
+    if (!ctx || !anticommuting) return PCG_E_ARG;
+    if (!ctx->counted) return fail(ctx, PCG_E_STATE, "pcg_k1_result before pcg_count");
+    if (ctx->k1_pending) {
+        PCG_TRY_CUDA(ctx, cudaSetDevice(ctx->device));
+        unsigned long long a = 0;
+        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&a, ctx->scal.p, 8, cudaMemcpyDeviceToHost, ctx->k1_stream));
+        PCG_TRY_CUDA(ctx, cudaStreamSynchronize(ctx->k1_stream));
+        if (ctx->prof) cudaEventElapsedTime(&ctx->ktimes[0], ctx->ev[0], ctx->ev[1]);
+        ctx->last.anticommuting = (int64_t)a;
+        ctx->k1_pending = false;
+    }
+    *anticommuting = ctx->last.anticommuting;
+    return PCG_OK;
+}
+
 extern "C" int pcg_build_device(pcg_ctx *ctx, pcg_counts *out, int32_t *launches) {
     if (!ctx) return PCG_E_ARG;
     if (!ctx->staged) return fail(ctx, PCG_E_STATE, "pcg_build_device before pcg_set_inputs");
@@ -1388,7 +1436,14 @@ extern "C" int pcg_build_device(pcg_ctx *ctx, pcg_counts *out, int32_t *launches
     if (rc) return rc;
     rc = fill_impl(ctx, false, nullptr, nullptr, nullptr, &l);
     if (launches) *launches = l;
-    return rc;
+    if (rc) return rc;
+    if (ctx->k1_pending) {
+        int64_t anti = 0;
+        rc = pcg_k1_result(ctx, &anti);
+        if (rc) return rc;
+        if (out) out->anticommuting = anti;
+    }
+    return PCG_OK;
 }
 
 extern "C" int pcg_fill_device(pcg_ctx *ctx, int32_t *launches) {
@@ -1534,6 +1589,8 @@ extern "C" int pcg_validate(pcg_ctx *ctx, const uint64_t *words, int64_t n_total
                             int64_t *violations, int64_t *edges) {
     if (!ctx || !violations || !edges) return PCG_E_ARG;
     ctx->err.clear();
+    if (ctx->k1_pending && ctx->k1_done) cudaEventSynchronize(ctx->k1_done);
+    ctx->k1_pending = false;
     ctx->staged = false;  // the validator reuses the build's staging buffers
     ctx->counted = false;
     if (n_active < 0 || n_total < 0 || n_active > n_total || num_qubits < 1 || nwords < 1 ||
@@ -1581,7 +1638,7 @@ extern "C" int pcg_validate(pcg_ctx *ctx, const uint64_t *words, int64_t n_total
     PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->scal.p, 0, 64, s));
     int64_t pairs = 0;
     int launches = 0;
-    rc = run_k1(ctx, 0, 1, &pairs, &launches);
+    rc = run_k1(ctx, 0, 1, &pairs, &launches, s);
     if (rc) return rc;
     // color classes: stable sort of (color, local index)
     const int64_t n = n_active;

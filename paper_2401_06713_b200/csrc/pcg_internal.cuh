@@ -229,6 +229,10 @@ struct pcg_ctx {
     std::vector<cudaStream_t> ring_st;
     std::vector<cudaEvent_t> chunk_ev;  // direct D2H: one event per chunk
     int64_t copy_bytes = 0;                    // D2H bytes of the last pcg_fill
+    int k1_async = 0;                          // K1 on a side stream, result collected later
+    bool k1_pending = false;
+    cudaStream_t k1_stream = nullptr;
+    cudaEvent_t k1_fork = nullptr, k1_done = nullptr;
     pcg::DevBuf dbytes, dxcnt, dxoff, dxval;  // byte-delta encoded CSR (public-build copy-out)
     std::vector<uint8_t *> hbytes;             // pinned per-worker byte staging
     size_t hbytes_cap = 0;

@@ -11,7 +11,7 @@ from conftest import ROOT
 def _declared():
     with open(os.path.join(ROOT, "include", "picasso_b200.h")) as f:
         text = f.read()
-    return sorted(set(re.findall(r"\b(pcg_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(pcg_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_library_exports_all_declared_symbols():
