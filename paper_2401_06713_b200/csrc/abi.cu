@@ -195,6 +195,7 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "fill_algo")) ctx->fill_algo = (int)value;
     else if (!strcmp(key, "seg_bits")) ctx->seg_bits = (int)value;
     else if (!strcmp(key, "own_algo")) ctx->own_algo = (int)value;
+    else if (!strcmp(key, "own_direct")) ctx->own_direct = (int)value;
     else if (!strcmp(key, "d2h_chunk")) ctx->d2h_chunk = (int)value;
     else if (!strcmp(key, "d2h_threads")) ctx->d2h_threads = (int)value;
     else if (!strcmp(key, "d2h_mode")) ctx->d2h_mode = (int)value;
@@ -425,6 +426,12 @@ static int prep_device(pcg_ctx *ctx) {
             o.l_magic = (uint32_t)(((1ull << 32) + (uint64_t)std::max(1, ctx->L) - 1) /
                                    (uint64_t)std::max(1, ctx->L));
             if ((int64_t)m_max * std::max(1, ctx->L) >= (1 << 20)) o.fr = 0;  // umulhi range
+            // direct-mapped ownership when the color table fits shared memory next to the
+            // rest (tags: level 6 bits | color 14 bits | member 12 bits), rectangular lists,
+            // and groups of members sharing a smaller color stay small (one level per member)
+            o.dtab_words = (int32_t)((P + 3) & ~3LL);
+            o.direct = (o.fr && ctx->own_direct != 0 && !ctx->ragged && P <= 14336 &&
+                        (int64_t)m_max * std::max(1, ctx->lmax - 1) <= 4 * P) ? 1 : 0;
             PCG_TRY_CUDA(ctx, cudaMemsetAsync(o.overflow, 0, 4, s));
             const bool want_runs = ctx->fill_algo == 4;  // run lengths only feed the runs fill
             b.runlen = nullptr;
@@ -766,6 +773,8 @@ static int count_impl(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t r0, 
     }
     if (ctx->own_check) {
         ctx->own_check = false;
+        if (ovf && ctx->owned && getenv("PICASSO_DEBUG"))
+            fprintf(stderr, "[picasso] ownership overflow (flag %d): bucket-mask fallback\n", ovf);
         if (ovf && ctx->owned) {  // a color's ownership table overflowed: plain bucket masks
             ctx->owned = false;   // (pairs deduplicated by the row bitmap) and count again
             BucketArgs b = bucket_args(ctx);

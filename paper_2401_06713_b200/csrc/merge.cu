@@ -21,6 +21,7 @@ namespace {
 
 constexpr int OWN_THREADS = 256;
 constexpr int OWN_COLL = 2048;        // collision list capacity
+constexpr int OWN_LCAP = 2048;        // direct ownership: losers per level
 constexpr int MERGE_WARPS = 4;
 
 template <int KW>
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_masks(BucketArgs b, OwnAr
         }
         __syncthreads();
         const int nc = min(ncoll, OWN_COLL);
-        if (overflow && tid == 0) atomicExch(o.overflow, 1);
+        if (overflow && tid == 0) atomicMax(o.overflow, overflow);
         for (int q = tid; q < nc; q += OWN_THREADS) {
             const uint32_t slot = coll[q] >> 12;
             const int k2 = (int)(coll[q] & 0xfffu);
@@ -205,18 +206,27 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
     constexpr int NIB = 8 * KW;
     extern __shared__ __align__(16) uint32_t osm[];
     const int HS = o.hash_slots;
+    // ownership state: hash (large palettes) or a direct-mapped table over the colors
     uint32_t *table = osm;                                        // HS: (c'+1)<<12 | first k
     unsigned short *head = reinterpret_cast<unsigned short *>(osm + HS);  // HS: last coll + 1
     uint32_t *coll = osm + HS + HS / 2;                           // OWN_COLL: slot<<12 | k
     int32_t *link = reinterpret_cast<int32_t *>(coll + OWN_COLL); // OWN_COLL: previous in slot
-    int32_t *sid = link + OWN_COLL;                               // member ids (m_cap)
+    uint32_t *dtab = osm;                                         // direct: P level|c|k tags
+    uint32_t *lA = osm + o.dtab_words;                            // direct: losers (c'<<12|k)
+    uint32_t *lB = lA + OWN_LCAP;
+    int32_t *sid = reinterpret_cast<int32_t *>(osm + (o.direct ? o.dtab_words + 2 * OWN_LCAP
+                                                               : HS + HS / 2 + 2 * OWN_COLL));
     uint32_t *T = reinterpret_cast<uint32_t *>(sid + ((o.m_cap + 3) & ~3));  // NIB*16 table
     uint32_t *BT = T + NIB * 16;                                  // 32*KW transposed bits
-    __shared__ int ncoll, overflow;
+    __shared__ int ncoll, overflow, nlose;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NWARPS = OWN_THREADS / 32;
     const uint32_t T_s = (uint32_t)__cvta_generic_to_shared(T);
-    for (int x = tid; x < HS + HS / 2; x += OWN_THREADS) osm[x] = 0u;
+    if (o.direct) {
+        for (int x = tid; x < o.dtab_words; x += OWN_THREADS) osm[x] = 0u;
+    } else {
+        for (int x = tid; x < HS + HS / 2; x += OWN_THREADS) osm[x] = 0u;
+    }
     for (int64_t c = blockIdx.x; c < b.P; c += gridDim.x) {
         const int m = b.bstart[c + 1] - b.bstart[c];
         if (m < 2) {
@@ -317,7 +327,66 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
                 slot = (slot + 1) & (HS - 1);
             }
         };
-        if (!o.loff) {
+        if (o.direct) {
+            // Leveled direct-mapped ownership: at level 1 every (c' < c, member k) writes the
+            // tag (level, c, k) into slot c' (last writer wins); after a barrier every writer
+            // whose tag was overwritten is a loser: it shares c' with the slot's winner (pair
+            // not owned by c) and retries at the next level with the other losers.  Level by
+            // level each group of members sharing c' yields every pair exactly once.
+            auto clear_pair = [&](int k1, int k2) {
+                atomicAnd(&out[(int64_t)k1 * W + (k2 >> 5)], ~(1u << (k2 & 31)));
+                atomicAnd(&out[(int64_t)k2 * W + (k1 >> 5)], ~(1u << (k1 & 31)));
+            };
+            const uint32_t ctag = (uint32_t)c << 12;
+            const uint32_t items = (uint32_t)m * (uint32_t)o.L;
+            if (tid == 0) nlose = 0;
+            for (uint32_t e = tid; e < items; e += OWN_THREADS) {
+                const int k = (int)__umulhi(e, o.l_magic);
+                const int32_t cx = o.lrel[(int64_t)sid[k] * o.L + (e - (uint32_t)k * (uint32_t)o.L)];
+                if (cx < c) dtab[cx] = (1u << 26) | ctag | (uint32_t)k;
+            }
+            __syncthreads();
+            for (uint32_t e = tid; e < items; e += OWN_THREADS) {
+                const int k = (int)__umulhi(e, o.l_magic);
+                const int32_t cx = o.lrel[(int64_t)sid[k] * o.L + (e - (uint32_t)k * (uint32_t)o.L)];
+                if (cx < c) {
+                    const uint32_t w = dtab[cx];
+                    if (w != ((1u << 26) | ctag | (uint32_t)k)) {
+                        clear_pair(k, (int)(w & 0xfffu));
+                        const int q = atomicAdd(&nlose, 1);
+                        if (q < OWN_LCAP) lA[q] = ((uint32_t)cx << 12) | (uint32_t)k;
+                        else overflow = 2;
+                    }
+                }
+            }
+            __syncthreads();
+            int nl = min(nlose, OWN_LCAP);
+            uint32_t *src = lA, *dst = lB;
+            for (uint32_t level = 2; nl > 0; ++level) {
+                if (level >= 64) {  // a color shared by 64+ members of one bucket: dedupe path
+                    if (tid == 0) overflow = 3;
+                    break;
+                }
+                __syncthreads();
+                if (tid == 0) nlose = 0;
+                for (int q = tid; q < nl; q += OWN_THREADS)
+                    dtab[src[q] >> 12] = (level << 26) | ctag | (src[q] & 0xfffu);
+                __syncthreads();
+                for (int q = tid; q < nl; q += OWN_THREADS) {
+                    const uint32_t w = dtab[src[q] >> 12];
+                    const int k = (int)(src[q] & 0xfffu);
+                    if (w != ((level << 26) | ctag | (uint32_t)k)) {
+                        clear_pair(k, (int)(w & 0xfffu));
+                        dst[atomicAdd(&nlose, 1)] = src[q];
+                    }
+                }
+                __syncthreads();
+                nl = nlose;
+                uint32_t *t = src;
+                src = dst;
+                dst = t;
+            }
+        } else if (!o.loff) {
             const uint32_t items = (uint32_t)m * (uint32_t)o.L;
             for (uint32_t e = tid; e < items; e += OWN_THREADS) {
                 const int k = (int)__umulhi(e, o.l_magic);  // e / L (exact for e < 2^20)
@@ -335,8 +404,8 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
             }
         }
         __syncthreads();
-        const int nc = min(ncoll, OWN_COLL);
-        if (overflow && tid == 0) atomicExch(o.overflow, 1);
+        const int nc = o.direct ? 0 : min(ncoll, OWN_COLL);
+        if (overflow && tid == 0) atomicMax(o.overflow, overflow);
         for (int q = tid; q < nc; q += OWN_THREADS) {
             const uint32_t slot = coll[q] >> 12;
             const int k2 = (int)(coll[q] & 0xfffu);
@@ -358,10 +427,13 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
                 b.runlen[b.bstart[c] + k] = cnt;
             }
         }
-        // reset the table and the chain heads this color touched
-        for (int x = 4 * tid; x < HS; x += 4 * OWN_THREADS)
-            *reinterpret_cast<uint4 *>(table + x) = make_uint4(0u, 0u, 0u, 0u);
-        for (int q = tid; q < nc; q += OWN_THREADS) head[coll[q] >> 12] = 0;  // (16-bit store)
+        // reset the hash table and the chain heads this color touched (direct tags carry the
+        // color: nothing to reset)
+        if (!o.direct) {
+            for (int x = 4 * tid; x < HS; x += 4 * OWN_THREADS)
+                *reinterpret_cast<uint4 *>(table + x) = make_uint4(0u, 0u, 0u, 0u);
+            for (int q = tid; q < nc; q += OWN_THREADS) head[coll[q] >> 12] = 0;  // (16-bit store)
+        }
         __syncthreads();
     }
 }
@@ -988,8 +1060,9 @@ int run_owned(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s) {
 template <int KW>
 int run_owned_fr(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s) {
     int per_sm = 0;
-    const size_t smem = (size_t)(o.hash_slots + o.hash_slots / 2 + 2 * OWN_COLL +
-                                 ((o.m_cap + 3) & ~3) + 8 * KW * 16 + 32 * KW) * 4;
+    const size_t state = o.direct ? (size_t)o.dtab_words + 2 * OWN_LCAP
+                                  : (size_t)o.hash_slots + o.hash_slots / 2 + 2 * OWN_COLL;
+    const size_t smem = (state + ((o.m_cap + 3) & ~3) + 8 * KW * 16 + 32 * KW) * 4;
     cudaFuncSetAttribute(k_owned_fr<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_owned_fr<KW>, OWN_THREADS, smem);
     if (per_sm < 1) per_sm = 1;

@@ -71,6 +71,8 @@ struct OwnArgs {
     int32_t m_cap;         // >= largest bucket
     int32_t fr;            // 1: four-Russians mask kernel (kw in {2,4,6,8})
     uint32_t l_magic;      // ceil(2^32 / L): item -> member by umulhi
+    int32_t direct;        // 1: direct-mapped ownership table over the colors (small P)
+    int32_t dtab_words;    // its size (>= P, multiple of 4)
 };
 
 struct RunArgs {
@@ -188,6 +190,7 @@ struct pcg_ctx {
     int seg_bits = 0;   // segmented fill: max window bits per warp (0 auto)
     int seg_warps = 0;  // segmented fill: warps per block (0 auto)
     int own_algo = 0;   // owned masks: 0 four-Russians tables (when kw allows), 1 per-pair
+    int own_direct = 1; // ownership: 1 direct-mapped color table when P is small, 0 hash
     int k2_mode = 0;    // 0 auto, 1 partner gathers, 2 bucket masks + bitmap dedupe, 3 owned masks + merge
 
     // state of the last count

@@ -37,12 +37,15 @@ def test_every_golden_build(golden_cases, k1_algo, k2_mode):
         case.check(b200.build(case.view, case.lists))
 
 
-@pytest.mark.parametrize("own_algo", [0, 1], ids=["own-fourrussians", "own-perpair"])
-def test_owned_mask_kernels(golden_cases, golden_ref, own_algo):
-    """Both owned-mask kernels (table-driven and per-pair) give the reference CSR."""
+@pytest.mark.parametrize("own_algo,own_direct", [(0, 1), (0, 0), (1, 0)],
+                         ids=["own-fourrussians-direct", "own-fourrussians-hash", "own-perpair"])
+def test_owned_mask_kernels(golden_cases, golden_ref, own_algo, own_direct):
+    """The owned-mask kernels (table-driven / per-pair masks; direct-mapped / hashed
+    ownership) give the reference CSR."""
     ctx = _native.context()
     ctx.option("k2_mode", 3)
     ctx.option("own_algo", own_algo)
+    ctx.option("own_direct", own_direct)
     try:
         for case in golden_cases:
             case.check(b200.build(case.view, case.lists))
@@ -54,6 +57,7 @@ def test_owned_mask_kernels(golden_cases, golden_ref, own_algo):
                 g["offsets_sha"], g["neighbors_sha"])
     finally:
         ctx.option("own_algo", 0)
+        ctx.option("own_direct", 1)
         ctx.option("k2_mode", 0)
 
 
