@@ -430,8 +430,12 @@ static int prep_device(pcg_ctx *ctx) {
             // rest (tags: level 6 bits | color 14 bits | member 12 bits), rectangular lists,
             // and groups of members sharing a smaller color stay small (one level per member)
             o.dtab_words = (int32_t)((P + 3) & ~3LL);
+            o.l16 = P < 65536 ? 1 : 0;
             o.direct = (o.fr && ctx->own_direct != 0 && !ctx->ragged && P <= 14336 &&
                         (int64_t)m_max * std::max(1, ctx->lmax - 1) <= 4 * P) ? 1 : 0;
+            // measured: staging the lists pays when they are u16 (small palettes); u32 lists
+            // next to the hash table cost occupancy (config 3)
+            o.stage_lists = (!ctx->ragged && o.l16) ? 1 : 0;
             PCG_TRY_CUDA(ctx, cudaMemsetAsync(o.overflow, 0, 4, s));
             const bool want_runs = ctx->fill_algo == 4;  // run lengths only feed the runs fill
             b.runlen = nullptr;

@@ -21,7 +21,7 @@ namespace {
 
 constexpr int OWN_THREADS = 256;
 constexpr int OWN_COLL = 2048;        // collision list capacity
-constexpr int OWN_LCAP = 2048;        // direct ownership: losers per level
+constexpr int OWN_LCAP = 1024;        // direct ownership: losers per level
 constexpr int MERGE_WARPS = 4;
 
 template <int KW>
@@ -218,6 +218,12 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
                                                                : HS + HS / 2 + 2 * OWN_COLL));
     uint32_t *T = reinterpret_cast<uint32_t *>(sid + ((o.m_cap + 3) & ~3));  // NIB*16 table
     uint32_t *BT = T + NIB * 16;                                  // 32*KW transposed bits
+    uint32_t *sB = BT + 32 * KW;                                  // members' partner vectors
+    // members' color lists (rectangular lists): u16 when the palette allows, else u32
+    void *sLv = sB + o.m_cap * KW;
+    unsigned short *sL16 = reinterpret_cast<unsigned short *>(sLv);
+    int32_t *sL32 = reinterpret_cast<int32_t *>(sLv);
+    const bool stage_lists = o.stage_lists != 0;
     __shared__ int ncoll, overflow, nlose;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NWARPS = OWN_THREADS / 32;
@@ -242,6 +248,19 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
         }
         for (int t = tid; t < m; t += OWN_THREADS) sid[t] = mem[t];
         __syncthreads();
+        // stage the members' partner vectors and color lists once (all loads in flight
+        // together; every later pass reads shared memory)
+        for (int x = tid; x < m * KW; x += OWN_THREADS)
+            sB[x] = __ldg(b.B + (int64_t)sid[x / KW] * KW + x % KW);
+        if (stage_lists) {
+            const uint32_t items = (uint32_t)m * (uint32_t)o.L;
+            for (uint32_t e = tid; e < items; e += OWN_THREADS) {
+                const int k = (int)__umulhi(e, o.l_magic);
+                const int32_t cx = __ldg(o.lrel + (int64_t)sid[k] * o.L + (e - (uint32_t)k * (uint32_t)o.L));
+                if (o.l16) sL16[e] = (unsigned short)cx; else sL32[e] = cx;
+            }
+        }
+        __syncthreads();
         // ---- commute masks
         for (int k0 = 0; k0 < m; k0 += OWN_THREADS) {
             const int k = k0 + tid;
@@ -262,7 +281,7 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
 #pragma unroll
                     for (int pp = 0; pp < PER; ++pp) {
                         const int p = warp * PER + pp;
-                        const uint32_t word = t < m ? __ldg(b.B + (int64_t)sid[t] * KW + (p >> 5)) : 0u;
+                        const uint32_t word = t < m ? sB[t * KW + (p >> 5)] : 0u;
                         const uint32_t bal = __ballot_sync(0xffffffffu, (word >> (p & 31)) & 1u);
                         if (lane == 0) BT[p] = bal;
                     }
@@ -342,13 +361,13 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
             if (tid == 0) nlose = 0;
             for (uint32_t e = tid; e < items; e += OWN_THREADS) {
                 const int k = (int)__umulhi(e, o.l_magic);
-                const int32_t cx = o.lrel[(int64_t)sid[k] * o.L + (e - (uint32_t)k * (uint32_t)o.L)];
+                const int32_t cx = o.l16 ? (int32_t)sL16[e] : sL32[e];
                 if (cx < c) dtab[cx] = (1u << 26) | ctag | (uint32_t)k;
             }
             __syncthreads();
             for (uint32_t e = tid; e < items; e += OWN_THREADS) {
                 const int k = (int)__umulhi(e, o.l_magic);
-                const int32_t cx = o.lrel[(int64_t)sid[k] * o.L + (e - (uint32_t)k * (uint32_t)o.L)];
+                const int32_t cx = o.l16 ? (int32_t)sL16[e] : sL32[e];
                 if (cx < c) {
                     const uint32_t w = dtab[cx];
                     if (w != ((1u << 26) | ctag | (uint32_t)k)) {
@@ -390,8 +409,8 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
             const uint32_t items = (uint32_t)m * (uint32_t)o.L;
             for (uint32_t e = tid; e < items; e += OWN_THREADS) {
                 const int k = (int)__umulhi(e, o.l_magic);  // e / L (exact for e < 2^20)
-                const int x = (int)(e - (uint32_t)k * (uint32_t)o.L);
-                const int32_t cx = o.lrel[(int64_t)sid[k] * o.L + x];
+                const int32_t cx = !stage_lists ? o.lrel[(int64_t)sid[k] * o.L + (e - (uint32_t)k * (uint32_t)o.L)]
+                                 : o.l16 ? (int32_t)sL16[e] : sL32[e];
                 if (cx < c) insert((uint32_t)cx + 1u, k);
             }
         } else {
@@ -1062,7 +1081,9 @@ int run_owned_fr(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s)
     int per_sm = 0;
     const size_t state = o.direct ? (size_t)o.dtab_words + 2 * OWN_LCAP
                                   : (size_t)o.hash_slots + o.hash_slots / 2 + 2 * OWN_COLL;
-    const size_t smem = (state + ((o.m_cap + 3) & ~3) + 8 * KW * 16 + 32 * KW) * 4;
+    const size_t lists = o.stage_lists ? (size_t)o.m_cap * o.L * (o.l16 ? 2 : 4) : 0;
+    const size_t smem = (state + ((o.m_cap + 3) & ~3) + 8 * KW * 16 + 32 * KW +
+                         (size_t)o.m_cap * KW) * 4 + ((lists + 15) & ~(size_t)15);
     cudaFuncSetAttribute(k_owned_fr<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_owned_fr<KW>, OWN_THREADS, smem);
     if (per_sm < 1) per_sm = 1;

@@ -73,6 +73,8 @@ struct OwnArgs {
     uint32_t l_magic;      // ceil(2^32 / L): item -> member by umulhi
     int32_t direct;        // 1: direct-mapped ownership table over the colors (small P)
     int32_t dtab_words;    // its size (>= P, multiple of 4)
+    int32_t l16;           // members' lists staged as u16 (palette < 65536)
+    int32_t stage_lists;   // stage the members' lists in shared memory (direct mode, or u16)
 };
 
 struct RunArgs {
