@@ -200,6 +200,7 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "d2h_threads")) ctx->d2h_threads = (int)value;
     else if (!strcmp(key, "d2h_mode")) ctx->d2h_mode = (int)value;
     else if (!strcmp(key, "k1_async")) ctx->k1_async = (int)value;
+    else if (!strcmp(key, "k1_wide")) ctx->k1_wide = (int)value;
     else if (!strcmp(key, "seg_warps")) ctx->seg_warps = (int)value;
     else return fail(ctx, PCG_E_ARG, std::string("unknown option ") + key);
     return PCG_OK;
@@ -490,7 +491,9 @@ static int prep_device(pcg_ctx *ctx) {
     // four-Russians row offsets
     if (fr_supported(ctx->kw)) {
         PCG_ALLOC(ctx, ctx->H, (size_t)ctx->npad * ctx->kw * 4 * 4);
-        launch_fr_prep(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
+        ctx->h_wide = fr_jb(ctx->kw, ctx->k1_wide) == K1_FR_JB2;
+        if (ctx->h_wide) launch_fr_prep2(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
+        else launch_fr_prep(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
         PCG_CHECK_LAUNCH(ctx);
     }
     PCG_ALLOC(ctx, ctx->deg, (size_t)n_active * 4);
@@ -534,7 +537,7 @@ extern "C" int pcg_set_inputs(pcg_ctx *ctx, const uint64_t *words, int64_t n_tot
     ctx->P = std::max<int64_t>(1, (palette_size + 63) / 64) * 64;
     palette_size = ctx->P;
     ctx->ragged = list_off != nullptr;
-    ctx->npad = round_up(n_active, K1_FR_JB);
+    ctx->npad = round_up(n_active, K1_FR_JB2);
     int64_t entries = 0;
     int32_t lmax = list_len;
     if (ctx->ragged) {
@@ -590,8 +593,8 @@ static int k1_algo(const pcg_ctx *ctx) {
 static int64_t fr_ichunk(const pcg_ctx *ctx) { return ctx->fr_ichunk > 0 ? ctx->fr_ichunk : 2048; }
 
 // pairs (i<j, both < n) inside four-Russians item (jb, rows [i0,i1))
-static int64_t fr_item_pairs(int64_t n, int64_t jb, int64_t i0, int64_t i1) {
-    const int64_t jlo = jb * K1_FR_JB, jhi = std::min(n, jlo + (int64_t)K1_FR_JB);
+static int64_t fr_item_pairs(int64_t n, int64_t jb, int64_t i0, int64_t i1, int64_t JB) {
+    const int64_t jlo = jb * JB, jhi = std::min(n, jlo + JB);
     int64_t p = 0;
     const int64_t full_hi = std::min(i1, jlo);
     if (full_hi > i0) p += (full_hi - i0) * (jhi - jlo);
@@ -624,10 +627,11 @@ static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, 
     unsigned long long *anti = ctx->scal.as<unsigned long long>();
     const int64_t n = ctx->n;
     if (k1_algo(ctx) == 2) {
-        const int64_t njb = ctx->npad / K1_FR_JB, ic = fr_ichunk(ctx);
+        const int64_t JB = ctx->h_wide ? K1_FR_JB2 : K1_FR_JB;
+        const int64_t njb = ctx->npad / JB, ic = fr_ichunk(ctx);
         std::vector<int64_t> start(njb + 1, 0);
         for (int64_t jb = 0; jb < njb; ++jb) {
-            const int64_t jlast = std::min(n, (jb + 1) * (int64_t)K1_FR_JB);
+            const int64_t jlast = std::min(n, (jb + 1) * JB);
             start[jb + 1] = start[jb] + (jlast + ic - 1) / ic;
         }
         const int64_t items = start[njb];
@@ -638,9 +642,9 @@ static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, 
             int64_t p = 0, jb = 0;
             for (int64_t it = i0; it < i1; ++it) {
                 while (start[jb + 1] <= it) ++jb;
-                const int64_t jlast = std::min(n, (jb + 1) * (int64_t)K1_FR_JB);
+                const int64_t jlast = std::min(n, (jb + 1) * JB);
                 const int64_t r0 = (it - start[jb]) * ic, r1 = std::min(r0 + ic, jlast);
-                p += fr_item_pairs(n, jb, r0, r1);
+                p += fr_item_pairs(n, jb, r0, r1, JB);
             }
             *pairs = p;
         }
@@ -648,9 +652,14 @@ static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, 
         PCG_ALLOC(ctx, ctx->items, (size_t)(njb + 1) * 8);
         PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->items.p, start.data(), (size_t)(njb + 1) * 8,
                                           cudaMemcpyHostToDevice, s));
-        *launches += launch_commute_fr_items(ctx->B.as<uint32_t>(), ctx->H.as<uint32_t>(),
-                                             ctx->kw, n, ctx->items.as<int64_t>(), njb,
-                                             (int32_t)ic, i0, i1, anti, ctx->sms, s);
+        if (ctx->h_wide)
+            *launches += launch_commute_fr2_items(ctx->B.as<uint32_t>(), ctx->H.as<uint32_t>(),
+                                                  ctx->kw, n, ctx->items.as<int64_t>(), njb,
+                                                  (int32_t)ic, i0, i1, anti, ctx->sms, s);
+        else
+            *launches += launch_commute_fr_items(ctx->B.as<uint32_t>(), ctx->H.as<uint32_t>(),
+                                                 ctx->kw, n, ctx->items.as<int64_t>(), njb,
+                                                 (int32_t)ic, i0, i1, anti, ctx->sms, s);
     } else {
         const int64_t T = ctx->npad / K1_TILE, NT = tri_tiles(T);
         const int64_t t0 = NT * shard / nshards, t1 = NT * (shard + 1) / nshards;
@@ -1620,7 +1629,7 @@ extern "C" int pcg_validate(pcg_ctx *ctx, const uint64_t *words, int64_t n_total
     ctx->n = n_active;
     ctx->nwords = nwords;
     ctx->q = num_qubits;
-    ctx->npad = round_up(n_active, K1_FR_JB);
+    ctx->npad = round_up(n_active, K1_FR_JB2);
     PCG_ALLOC(ctx, ctx->bad, 16);
     PCG_ALLOC(ctx, ctx->scal, 64);
     PCG_ALLOC(ctx, ctx->words, (size_t)n_total * nwords * 8);
@@ -1645,7 +1654,9 @@ extern "C" int pcg_validate(pcg_ctx *ctx, const uint64_t *words, int64_t n_total
     // |E|: the commuting-pair sweep (K1)
     if (fr_supported(ctx->kw)) {
         PCG_ALLOC(ctx, ctx->H, (size_t)ctx->npad * ctx->kw * 4 * 4);
-        launch_fr_prep(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
+        ctx->h_wide = fr_jb(ctx->kw, ctx->k1_wide) == K1_FR_JB2;
+        if (ctx->h_wide) launch_fr_prep2(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
+        else launch_fr_prep(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
         PCG_CHECK_LAUNCH(ctx);
     }
     PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->scal.p, 0, 64, s));

@@ -264,6 +264,146 @@ __global__ void __launch_bounds__(FR_WARPS * 32) k_commute_fr(
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Four-Russians kernel, wide entries: a 2048-partner j-block, lane t owns partners
+// 64t..64t+63 and every table entry is 64-bit (two 32-partner words).  One LDS.64 + one
+// PRMT per 4-bit slice per 2048 pairs per warp: half the shared-memory instructions and
+// address computations of the 32-bit layout for the same wavefronts (the 32-bit kernel is
+// bound by LSU instruction issue — mio_throttle — at ~54% of the shared wavefront peak).
+// Entry (g, v, t) lives at byte (g>>1)*8192 + ((v<<1)|(g&1))*256 + t*8: the slice-pair
+// offset is an LDS immediate (unrolled g), the rest is one PRMT of the row's precomputed
+// byte ((v<<1)|(g&1)) (k_fr_prep2) with the lane's t*8.
+// ---------------------------------------------------------------------------------------
+template <int KW>
+__global__ void k_fr_prep2(const uint32_t *__restrict__ A, int64_t npad, uint32_t *__restrict__ H) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= npad) return;
+    const uint32_t *a = A + i * KW;
+    uint32_t *h = H + i * (KW * 4);
+#pragma unroll
+    for (int k = 0; k < KW; ++k) {
+        const uint32_t w = a[k];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {  // slices g = 8k+2m (low half) and 8k+2m+1 (high half)
+            const uint32_t v0 = (w >> (8 * m)) & 15u, v1 = (w >> (8 * m + 4)) & 15u;
+            h[k * 4 + m] = ((v0 << 1) << 8) | ((((v1 << 1) | 1u) << 8) << 16);
+        }
+    }
+}
+
+template <int KW>
+__global__ void __launch_bounds__(FR_WARPS * 32) k_commute_fr2(
+    const uint32_t *__restrict__ B, const uint32_t *__restrict__ H, int64_t n,
+    const int64_t *__restrict__ item_start, int64_t njb, int32_t ichunk, int64_t item0,
+    int64_t item1, unsigned long long *__restrict__ anti) {
+    constexpr int K = 32 * KW;           // bits per vector
+    constexpr int NG = K / 4;            // 4-bit slices
+    constexpr int JB = 2048;
+    constexpr int TBL_BYTES = (NG / 2) * 8192;
+    constexpr int BT_STRIDE = K + 1;     // padded row of the transposed block
+    extern __shared__ __align__(16) uint32_t smem[];
+    char *tbl = reinterpret_cast<char *>(smem);
+    uint32_t *bt = smem + TBL_BYTES / 4;       // 64 * BT_STRIDE
+    __shared__ unsigned long long red[FR_WARPS];
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lb = (uint32_t)lane * 8u;
+    const uint32_t tbl_s = (uint32_t)__cvta_generic_to_shared(tbl);
+
+    const int64_t nitems = item1 - item0;
+    const int64_t my0 = item0 + nitems * blockIdx.x / gridDim.x;
+    const int64_t my1 = item0 + nitems * (blockIdx.x + 1) / gridDim.x;
+    int64_t cur_jb = -1;
+    unsigned long long local = 0;
+
+    for (int64_t it = my0; it < my1; ++it) {
+        int64_t lo = 0, hi = njb;
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (item_start[mid] <= it) lo = mid; else hi = mid;
+        }
+        const int64_t jb = lo, ic = it - item_start[jb];
+        if (jb != cur_jb) {
+            __syncthreads();  // previous tables no longer in use
+            // phase A: transpose the 2048 partner vectors into bit rows bt[t][k], t = 32-group
+            for (int t = warp; t < 64; t += FR_WARPS) {
+                const uint32_t *bj = B + (jb * JB + 32 * t + lane) * KW;
+                uint32_t v[KW];
+#pragma unroll
+                for (int k = 0; k < KW; ++k) v[k] = __ldg(bj + k);
+#pragma unroll
+                for (int k = 0; k < KW; ++k) {
+                    uint32_t mine = 0;
+#pragma unroll
+                    for (int s = 0; s < 32; ++s) {
+                        const uint32_t word = __ballot_sync(0xffffffffu, (v[k] >> s) & 1u);
+                        if (lane == s) mine = word;
+                    }
+                    bt[t * BT_STRIDE + 32 * k + lane] = mine;
+                }
+            }
+            __syncthreads();
+            // phase B: 16 XOR combinations per slice; lane t builds the entry of groups 2t, 2t+1
+            for (int g = warp; g < NG; g += FR_WARPS) {
+                const uint32_t *r0 = bt + (2 * lane) * BT_STRIDE + 4 * g;
+                const uint32_t *r1 = r0 + BT_STRIDE;
+                const uint32_t a0 = r0[0], a1 = r0[1], a2 = r0[2], a3 = r0[3];
+                const uint32_t c0 = r1[0], c1 = r1[1], c2 = r1[2], c3 = r1[3];
+                char *dst = tbl + (g >> 1) * 8192 + (g & 1) * 256 + lane * 8;
+#pragma unroll
+                for (int v = 0; v < 16; ++v) {
+                    uint32_t e0 = 0, e1 = 0;
+                    if (v & 1) { e0 ^= a0; e1 ^= c0; }
+                    if (v & 2) { e0 ^= a1; e1 ^= c1; }
+                    if (v & 4) { e0 ^= a2; e1 ^= c2; }
+                    if (v & 8) { e0 ^= a3; e1 ^= c3; }
+                    *reinterpret_cast<uint2 *>(dst + v * 512) = make_uint2(e0, e1);
+                }
+            }
+            __syncthreads();
+            cur_jb = jb;
+        }
+        const int64_t jlast = min(n, (jb + 1) * (int64_t)JB);  // exclusive
+        const int64_t i0 = ic * ichunk;
+        const int64_t i1 = min(i0 + ichunk, jlast);
+        const int64_t jbase = jb * JB + 64 * lane;
+        for (int64_t i = i0 + warp; i < i1; i += FR_WARPS) {
+            const uint4 *hp = reinterpret_cast<const uint4 *>(H + i * (KW * 4));
+            uint32_t acc0 = 0, acc1 = 0;
+#pragma unroll
+            for (int k = 0; k < KW; ++k) {
+                const uint4 hv = __ldg(hp + k);
+                const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    // slices g = 8k+2m and g+1 share the slice pair (g>>1) = 4k+m
+                    const uint32_t base = tbl_s + (uint32_t)(4 * k + m) * 8192u;
+                    const uint32_t ad0 = base + __byte_perm(hw[m], lb, 0x7614);
+                    const uint32_t ad1 = base + __byte_perm(hw[m], lb, 0x7634);
+                    uint2 e0, e1;
+                    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(e0.x), "=r"(e0.y) : "r"(ad0));
+                    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(e1.x), "=r"(e1.y) : "r"(ad1));
+                    acc0 ^= e0.x ^ e1.x;
+                    acc1 ^= e0.y ^ e1.y;
+                }
+            }
+            // partners j = jbase + s (word 0) and jbase + 32 + s (word 1) with j > i
+            const int64_t d0 = i - jbase, d1 = d0 - 32;
+            const uint32_t m0 = d0 < 0 ? 0xffffffffu : (d0 >= 31 ? 0u : ~((2u << d0) - 1u));
+            const uint32_t m1 = d1 < 0 ? 0xffffffffu : (d1 >= 31 ? 0u : ~((2u << d1) - 1u));
+            local += __popc(acc0 & m0) + __popc(acc1 & m1);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
+    if (lane == 0) red[warp] = local;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long s = 0;
+        for (int w = 0; w < FR_WARPS; ++w) s += red[w];
+        if (s) atomicAdd(anti, s);
+    }
+}
+
 template <typename K>
 int occupancy_grid(K kernel, int threads, size_t smem, int sms, int64_t work) {
     int per_sm = 0;
@@ -285,6 +425,24 @@ int run_direct(const uint32_t *A, const uint32_t *B, int64_t T, int64_t t0, int6
 template <int KW>
 size_t fr_smem() {
     return (size_t)(KW * 32 / 4) * 16 * 32 * 4 + (size_t)32 * (KW * 32 + 1) * 4;
+}
+
+template <int KW>
+size_t fr2_smem() {
+    return (size_t)(KW * 32 / 4 / 2) * 8192 + (size_t)64 * (KW * 32 + 1) * 4;
+}
+
+template <int KW>
+int run_fr2(const uint32_t *B, const uint32_t *H, int64_t n, const int64_t *item_start,
+            int64_t njb, int32_t ichunk, int64_t item0, int64_t item1,
+            unsigned long long *anti, int sms, cudaStream_t s) {
+    const size_t smem = fr2_smem<KW>();
+    cudaFuncSetAttribute(k_commute_fr2<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    const int grid = occupancy_grid(k_commute_fr2<KW>, FR_WARPS * 32, smem, sms, item1 - item0);
+    k_commute_fr2<KW><<<grid, FR_WARPS * 32, smem, s>>>(B, H, n, item_start, njb, ichunk, item0,
+                                                       item1, anti);
+    return 1;
 }
 
 template <int KW>
@@ -323,6 +481,30 @@ int launch_commute_direct(const uint32_t *A, const uint32_t *B, int32_t kw, int6
 }
 
 bool fr_supported(int32_t kw) { return kw == 2 || kw == 4 || kw == 6 || kw == 8; }
+
+int fr_jb(int32_t kw, int wide) { return (wide && (kw == 2 || kw == 4)) ? K1_FR_JB2 : K1_FR_JB; }
+
+int launch_fr_prep2(const uint32_t *A, int32_t kw, int64_t npad, uint32_t *H, cudaStream_t s) {
+    const int tb = 256;
+    const unsigned grid = (unsigned)((npad + tb - 1) / tb);
+    switch (kw) {
+        case 2: k_fr_prep2<2><<<grid, tb, 0, s>>>(A, npad, H); return 1;
+        case 4: k_fr_prep2<4><<<grid, tb, 0, s>>>(A, npad, H); return 1;
+        default: return 0;
+    }
+}
+
+int launch_commute_fr2_items(const uint32_t *B, const uint32_t *H, int32_t kw, int64_t n,
+                             const int64_t *item_start, int64_t njb, int32_t ichunk,
+                             int64_t item0, int64_t item1, unsigned long long *anti, int sms,
+                             cudaStream_t s) {
+    if (item1 <= item0) return 0;
+    switch (kw) {
+        case 2: return run_fr2<2>(B, H, n, item_start, njb, ichunk, item0, item1, anti, sms, s);
+        case 4: return run_fr2<4>(B, H, n, item_start, njb, ichunk, item0, item1, anti, sms, s);
+        default: return 0;
+    }
+}
 
 int launch_fr_prep(const uint32_t *A, int32_t kw, int64_t npad, uint32_t *H, cudaStream_t s) {
     const int tb = 256;

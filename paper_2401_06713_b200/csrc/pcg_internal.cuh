@@ -30,6 +30,7 @@ void release(DevBuf &b);
 // ---------------------------------------------------------------------------
 constexpr int K1_TILE = 128;  // rows == cols of one upper-triangle tile (direct kernel)
 constexpr int K1_FR_JB = 1024;  // j-block of the four-Russians kernel (32 lanes x 32 bits)
+constexpr int K1_FR_JB2 = 2048; // j-block of the wide four-Russians kernel (32 lanes x 64 bits)
 
 // ---------------------------------------------------------------------------
 // Arguments of the conflict-row kernels (K2).
@@ -137,6 +138,12 @@ int launch_commute_fr_items(const uint32_t *B, const uint32_t *H, int32_t kw, in
                             int64_t item0, int64_t item1, unsigned long long *anti, int sms,
                             cudaStream_t s);
 int launch_fr_prep(const uint32_t *A, int32_t kw, int64_t npad, uint32_t *H, cudaStream_t s);
+int fr_jb(int32_t kw, int wide);
+int launch_fr_prep2(const uint32_t *A, int32_t kw, int64_t npad, uint32_t *H, cudaStream_t s);
+int launch_commute_fr2_items(const uint32_t *B, const uint32_t *H, int32_t kw, int64_t n,
+                             const int64_t *item_start, int64_t njb, int32_t ichunk,
+                             int64_t item0, int64_t item1, unsigned long long *anti, int sms,
+                             cudaStream_t s);
 int launch_rows(const RowArgs &a, bool fill, bool out64, int sms, cudaStream_t s);
 int launch_bucket_layout(const BucketArgs &b, int64_t entries, cudaStream_t s);
 int launch_bucket_masks(const BucketArgs &b, int sms, cudaStream_t s);
@@ -183,6 +190,8 @@ struct pcg_ctx {
 
     // options
     int k1_algo = 0;    // 0 auto, 1 direct, 2 four-Russians
+    int k1_wide = 1;    // four-Russians with 64-bit entries (2048-partner blocks) when kw <= 4
+    bool h_wide = false;  // the staged H offsets are in the wide kernel's format
     int window = 0;     // K2 window bits (0 auto)
     int fr_ichunk = 0;  // four-Russians i-chunk (0 auto)
     int merge_cap = 0;  // fill-merge buffer cap (0 auto; testing knob)

@@ -16,12 +16,14 @@ from conftest import oracle_builder, pauli_view, random_lists, sha
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=[1, 2], ids=["k1-direct", "k1-fourrussians"])
+@pytest.fixture(params=[(1, 0), (2, 0), (2, 1)], ids=["k1-direct", "k1-fourrussians", "k1-fourrussians-wide"])
 def k1_algo(request):
     ctx = _native.context()
-    ctx.option("k1_algo", request.param)
+    ctx.option("k1_algo", request.param[0])
+    ctx.option("k1_wide", request.param[1])
     yield request.param
     ctx.option("k1_algo", 0)
+    ctx.option("k1_wide", 1)
 
 
 @pytest.fixture(params=[1, 2, 3], ids=["k2-gather", "k2-bucketmasks", "k2-owned"])

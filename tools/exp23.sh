@@ -1,0 +1,6 @@
+#!/bin/bash
+O=gpurun_out/$1; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_validation.py -q -x > $O/pytest.log 2>&1; echo "rc=$?" >> $O/pytest.log
+for cfg in "--wide 1" "--wide 0"; do echo "== c2 $cfg"; timeout 300 python tools/quick_perf.py --n 100000 --q 32 $cfg --reps 3; done > $O/c2.txt 2>&1
+for cfg in "--wide 1" "--wide 0"; do echo "== c3 $cfg"; timeout 600 python tools/quick_perf.py --n 1000000 --q 64 $cfg --reps 2; done > $O/c3.txt 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:'k_commute_fr2' -s 1 -c 1 -o $O/k1_c2 python tools/quick_perf.py --n 100000 --q 32 --reps 2 > $O/ncu.log 2>&1

@@ -23,6 +23,7 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--seg-bits", type=int, default=0)
 ap.add_argument("--seg-warps", type=int, default=0)
 ap.add_argument("--own", type=int, default=0)
+ap.add_argument("--wide", type=int, default=1)
 ap.add_argument("--own-direct", type=int, default=1)
 ap.add_argument("--check", action="store_true", help="compare the CSR with fill_algo 3")
 a = ap.parse_args()
@@ -40,6 +41,7 @@ ctx.option("fill_algo", a.fill)
 ctx.option("seg_bits", a.seg_bits)
 ctx.option("seg_warps", a.seg_warps)
 ctx.option("own_algo", a.own)
+ctx.option("k1_wide", a.wide)
 ctx.option("own_direct", a.own_direct)
 ctx.profiling(True)
 stage(v, lists, ctx)
