@@ -335,7 +335,7 @@ def bench_gpu(args) -> None:
                      "traffic_source": (measured_traffic("k_fill_seg") or (None, None))[1],
                      "bytes_per_launch": int(fill_bytes),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
-        "int_roofline": {"kernel": "commuting-pair sweep (k_commute_fr)", "achieved": k1_rate,
+        "int_roofline": {"kernel": "commuting-pair sweep (k_commute_fr2, 64-bit four-Russians tables)", "achieved": k1_rate,
                          "unit": "pairs/s", "peak": popc_bound,
                          "peak_model": "148 SMs x 16 POPC/clk x measured SM clock (1 POPC per pair)",
                          "frac": k1_rate / popc_bound},
