@@ -182,7 +182,9 @@ int pcg_host_register(void *ptr, uint64_t bytes, int32_t on);
 int pcg_k1_result(pcg_ctx *ctx, int64_t *anticommuting);
 
 /* Bytes the last pcg_fill copied device -> host: members, offsets and the neighbor ids
- * (sent as byte gaps + an exception list and decoded into the int64 output on the host). */
+ * (sent as gaps + an exception list and decoded into the int64 output on the host; 8-bit
+ * gaps while the mean gap is <= 64 ids, else 16-bit — option "d2h_gap16": 1 forces 16-bit,
+ * 2 forces 8-bit). */
 int64_t pcg_last_copy_bytes(const pcg_ctx *ctx);
 
 #ifdef __cplusplus

@@ -201,6 +201,7 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "d2h_mode")) ctx->d2h_mode = (int)value;
     else if (!strcmp(key, "k1_async")) ctx->k1_async = (int)value;
     else if (!strcmp(key, "k1_wide")) ctx->k1_wide = (int)value;
+    else if (!strcmp(key, "d2h_gap16")) ctx->d2h_gap16 = (int)value;
     else if (!strcmp(key, "seg_warps")) ctx->seg_warps = (int)value;
     else return fail(ctx, PCG_E_ARG, std::string("unknown option ") + key);
     return PCG_OK;
@@ -976,22 +977,32 @@ static void widen_inplace(int64_t *to, size_t len) {
 // `r0` = the row of x0, `xv` = exceptions (row-major), `xc` = the exception cursor at x0.
 // SIMD path: aligned 16-entry groups with no escape byte and no row start are an in-register
 // prefix sum added to the running value, widened and stored with streaming stores.
+template <typename G>
 __attribute__((target("avx512f"))) static void delta_decode_avx512(
-    int64_t *dst, const uint8_t *g, int64_t x0, int64_t x1, const int64_t *rs, int64_t r0,
+    int64_t *dst, const G *g, int64_t x0, int64_t x1, const int64_t *rs, int64_t r0,
     const int32_t *xv, int64_t xc) {
+    constexpr uint32_t ESC = sizeof(G) == 1 ? 255u : 65535u;
     int64_t r = r0;
     int64_t next = rs[r0 + 1];  // first entry of the next row
     int32_t acc = -1;
     int64_t x = x0;
     const __m512i zero = _mm512_setzero_si512();
-    const __m128i esc = _mm_set1_epi8((char)255);
     while (x < x1) {
         const bool aligned = (reinterpret_cast<uintptr_t>(dst + x) & 63) == 0 && x + 16 <= x1 &&
                              next >= x + 16;
         if (aligned) {
-            const __m128i v = _mm_loadu_si128(reinterpret_cast<const __m128i *>(g + (x - x0)));
-            if (_mm_movemask_epi8(_mm_cmpeq_epi8(v, esc)) == 0) {
-                __m512i t = _mm512_cvtepu8_epi32(v);
+            __m512i t;
+            bool clean;
+            if constexpr (sizeof(G) == 1) {
+                const __m128i v = _mm_loadu_si128(reinterpret_cast<const __m128i *>(g + (x - x0)));
+                clean = _mm_movemask_epi8(_mm_cmpeq_epi8(v, _mm_set1_epi8((char)255))) == 0;
+                t = _mm512_cvtepu8_epi32(v);
+            } else {
+                const __m256i v = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(g + (x - x0)));
+                clean = _mm256_movemask_epi8(_mm256_cmpeq_epi16(v, _mm256_set1_epi16((short)-1))) == 0;
+                t = _mm512_cvtepu16_epi32(v);
+            }
+            if (clean) {
                 t = _mm512_add_epi32(t, _mm512_alignr_epi32(t, zero, 15));
                 t = _mm512_add_epi32(t, _mm512_alignr_epi32(t, zero, 14));
                 t = _mm512_add_epi32(t, _mm512_alignr_epi32(t, zero, 12));
@@ -1012,16 +1023,18 @@ __attribute__((target("avx512f"))) static void delta_decode_avx512(
             next = rs[r + 1];
             acc = -1;
         }
-        const uint8_t b = g[x - x0];
-        acc = b == 255 ? xv[xc++] : acc + (int32_t)b;
+        const uint32_t b = g[x - x0];
+        acc = b == ESC ? xv[xc++] : acc + (int32_t)b;
         dst[x] = acc;
         ++x;
     }
     _mm_sfence();
 }
 
-static void delta_decode_scalar(int64_t *dst, const uint8_t *g, int64_t x0, int64_t x1,
+template <typename G>
+static void delta_decode_scalar(int64_t *dst, const G *g, int64_t x0, int64_t x1,
                                 const int64_t *rs, int64_t r0, const int32_t *xv, int64_t xc) {
+    constexpr uint32_t ESC = sizeof(G) == 1 ? 255u : 65535u;
     int64_t r = r0, next = rs[r0 + 1];
     int32_t acc = -1;
     for (int64_t x = x0; x < x1; ++x) {
@@ -1030,10 +1043,18 @@ static void delta_decode_scalar(int64_t *dst, const uint8_t *g, int64_t x0, int6
             next = rs[r + 1];
             acc = -1;
         }
-        const uint8_t b = g[x - x0];
-        acc = b == 255 ? xv[xc++] : acc + (int32_t)b;
+        const uint32_t b = g[x - x0];
+        acc = b == ESC ? xv[xc++] : acc + (int32_t)b;
         dst[x] = acc;
     }
+}
+
+template <typename G>
+static void delta_decode(bool simd, int64_t *dst, const void *g, int64_t x0, int64_t x1,
+                         const int64_t *rs, int64_t r0, const int32_t *xv, int64_t xc) {
+    const G *gg = static_cast<const G *>(g);
+    if (simd) delta_decode_avx512<G>(dst, gg, x0, x1, rs, r0, xv, xc);
+    else delta_decode_scalar<G>(dst, gg, x0, x1, rs, r0, xv, xc);
 }
 
 // Public-build copy-out of the neighbor ids: byte-delta encode on the device, copy gap bytes
@@ -1041,11 +1062,15 @@ static void delta_decode_scalar(int64_t *dst, const uint8_t *g, int64_t x0, int6
 // `offsets` is the host copy of the CSR offsets (nm+1 entries, already transferred).
 static int d2h_delta(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, int64_t nm, int64_t nnz) {
     cudaStream_t s = ctx->stream;
-    PCG_ALLOC(ctx, ctx->dbytes, (size_t)nnz);
+    // gap width: bytes while the mean gap (ids per row / entries per row) is small
+    const double mean_gap = nnz > 0 ? (double)ctx->n * (double)nm / (double)nnz : 0.0;
+    const bool wide = ctx->d2h_gap16 == 1 || (ctx->d2h_gap16 == 0 && mean_gap > 64.0);
+    const size_t gb = wide ? 2 : 1;  // bytes per gap
+    PCG_ALLOC(ctx, ctx->dbytes, (size_t)nnz * gb);
     PCG_ALLOC(ctx, ctx->dxcnt, (size_t)(nm + 1) * 4);
     PCG_ALLOC(ctx, ctx->dxoff, (size_t)(nm + 1) * 8);
-    launch_delta(false, ctx->nbr_o.as<int32_t>(), ctx->offsets_o.as<int64_t>(), nm,
-                 ctx->dbytes.as<uint8_t>(), ctx->dxcnt.as<int32_t>(), nullptr, nullptr, ctx->sms, s);
+    launch_delta(false, wide, ctx->nbr_o.as<int32_t>(), ctx->offsets_o.as<int64_t>(), nm,
+                 ctx->dbytes.p, ctx->dxcnt.as<int32_t>(), nullptr, nullptr, ctx->sms, s);
     PCG_CHECK_LAUNCH(ctx);
     cub::CountingInputIterator<int64_t> idx(0);
     cub::TransformInputIterator<int64_t, DegAt, cub::CountingInputIterator<int64_t>> xc(
@@ -1064,8 +1089,8 @@ static int d2h_delta(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, int64_t
     PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
     const int64_t X = ctx->hxoff[nm];
     PCG_ALLOC(ctx, ctx->dxval, (size_t)std::max<int64_t>(X, 1) * 4);
-    launch_delta(true, ctx->nbr_o.as<int32_t>(), ctx->offsets_o.as<int64_t>(), nm, nullptr, nullptr,
-                 ctx->dxoff.as<int64_t>(), ctx->dxval.as<int32_t>(), ctx->sms, s);
+    launch_delta(true, wide, ctx->nbr_o.as<int32_t>(), ctx->offsets_o.as<int64_t>(), nm, nullptr,
+                 nullptr, ctx->dxoff.as<int64_t>(), ctx->dxval.as<int32_t>(), ctx->sms, s);
     PCG_CHECK_LAUNCH(ctx);
     if (ctx->hx_cap < (size_t)std::max<int64_t>(X, 1)) {
         if (ctx->hxval) cudaFreeHost(ctx->hxval);
@@ -1075,7 +1100,7 @@ static int d2h_delta(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, int64_t
     }
     if (X > 0)
         PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->hxval, ctx->dxval.p, (size_t)X * 4, cudaMemcpyDeviceToHost, s));
-    ctx->copy_bytes += (int64_t)nnz + X * 4 + (nm + 1) * 8;  // gap bytes, exceptions, offsets
+    ctx->copy_bytes += (int64_t)nnz * (int64_t)gb + X * 4 + (nm + 1) * 8;  // gaps, exceptions, offsets
     // row-aligned chunks of ~CH entries
     const int64_t CH = ctx->d2h_chunk > 0 ? ctx->d2h_chunk : (int64_t)1 << 19;
     std::vector<int64_t> cr;  // chunk row bounds
@@ -1088,13 +1113,14 @@ static int d2h_delta(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, int64_t
     }
     const size_t nch = cr.size() - 1;
     size_t maxb = 0;
-    for (size_t k = 0; k < nch; ++k) maxb = std::max<size_t>(maxb, (size_t)(offsets[cr[k + 1]] - offsets[cr[k]]));
+    for (size_t k = 0; k < nch; ++k)
+        maxb = std::max<size_t>(maxb, (size_t)(offsets[cr[k + 1]] - offsets[cr[k]]) * gb);
     const int W = ctx->d2h_threads > 0 ? ctx->d2h_threads : std::min(16, omp_get_num_procs());
     if (ctx->hbytes_cap < maxb || (int)ctx->hbytes.size() != 2 * W) {
         for (uint8_t *p : ctx->hbytes)
             if (p) cudaFreeHost(p);
         ctx->hbytes.assign(2 * W, nullptr);
-        ctx->hbytes_cap = std::max<size_t>(maxb, (size_t)CH);
+        ctx->hbytes_cap = std::max<size_t>(maxb, (size_t)CH * gb);
         for (int k = 0; k < 2 * W; ++k)
             PCG_TRY_CUDA(ctx, cudaHostAlloc(reinterpret_cast<void **>(&ctx->hbytes[k]), ctx->hbytes_cap, cudaHostAllocDefault));
     }
@@ -1111,7 +1137,7 @@ static int d2h_delta(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, int64_t
     cudaEvent_t ready = ctx->ring_ev[2 * W];
     PCG_TRY_CUDA(ctx, cudaEventRecord(ready, s));  // bytes + exceptions queued before it
     static const bool simd = __builtin_cpu_supports("avx512f");
-    const uint8_t *src = ctx->dbytes.as<uint8_t>();
+    const uint8_t *src = ctx->dbytes.as<uint8_t>();  // gap array, gb bytes per entry
     int failed = 0;
 #pragma omp parallel num_threads(W)
     {
@@ -1121,8 +1147,8 @@ static int d2h_delta(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, int64_t
         cudaStreamWaitEvent(st, ready, 0);
         auto issue = [&](size_t k, int slot) -> cudaError_t {
             const int64_t b0 = offsets[cr[k]], b1 = offsets[cr[k + 1]];
-            cudaError_t e = cudaMemcpyAsync(ctx->hbytes[2 * w + slot], src + b0, (size_t)(b1 - b0),
-                                            cudaMemcpyDeviceToHost, st);
+            cudaError_t e = cudaMemcpyAsync(ctx->hbytes[2 * w + slot], src + b0 * gb,
+                                            (size_t)(b1 - b0) * gb, cudaMemcpyDeviceToHost, st);
             if (e == cudaSuccess) e = cudaEventRecord(ctx->ring_ev[2 * w + slot], st);
             return e;
         };
@@ -1136,12 +1162,12 @@ static int d2h_delta(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, int64_t
                 break;
             }
             const int64_t r0 = cr[k], x0 = offsets[r0], x1 = offsets[cr[k + 1]];
-            if (simd)
-                delta_decode_avx512(dst, ctx->hbytes[2 * w + slot], x0, x1, offsets, r0, ctx->hxval,
-                                    ctx->hxoff[r0]);
+            if (wide)
+                delta_decode<uint16_t>(simd, dst, ctx->hbytes[2 * w + slot], x0, x1, offsets, r0,
+                                       ctx->hxval, ctx->hxoff[r0]);
             else
-                delta_decode_scalar(dst, ctx->hbytes[2 * w + slot], x0, x1, offsets, r0, ctx->hxval,
-                                    ctx->hxoff[r0]);
+                delta_decode<uint8_t>(simd, dst, ctx->hbytes[2 * w + slot], x0, x1, offsets, r0,
+                                      ctx->hxval, ctx->hxoff[r0]);
         }
         cudaStreamSynchronize(st);
     }

@@ -160,8 +160,8 @@ void seg_geometry(int64_t n, int64_t max_bits, int32_t *wb, int32_t *nwin, int32
 int launch_window_bounds(const int32_t *bstart, const int32_t *bpos, const int32_t *bmemp,
                          int64_t P, int nwin, int32_t wb, int32_t *bnd, cudaStream_t s);
 int launch_fill_seg(const RowArgs &a, const SegArgs &g, bool out64, int sms, cudaStream_t s);
-int launch_delta(bool write, const int32_t *nbr, const int64_t *rowoff, int64_t rows,
-                 uint8_t *bytes, int32_t *xcount, const int64_t *xoff, int32_t *xval, int sms,
+int launch_delta(bool write, bool wide, const int32_t *nbr, const int64_t *rowoff, int64_t rows,
+                 void *bytes, int32_t *xcount, const int64_t *xoff, int32_t *xval, int sms,
                  cudaStream_t s);
 int launch_class_keys(const int64_t *color, int64_t n, int64_t *keys, int32_t *vals, cudaStream_t s);
 int launch_class_pairs(bool emit, const int64_t *keys, const int32_t *vals, int64_t n,
@@ -243,6 +243,7 @@ struct pcg_ctx {
     std::vector<cudaStream_t> ring_st;
     std::vector<cudaEvent_t> chunk_ev;  // direct D2H: one event per chunk
     int64_t copy_bytes = 0;                    // D2H bytes of the last pcg_fill
+    int d2h_gap16 = 0;  // delta copy-out gap width: 0 auto (mean gap), 1 16-bit, 2 bytes
     int k1_async = 0;                          // K1 on a side stream, result collected later
     bool k1_pending = false;
     cudaStream_t k1_stream = nullptr;

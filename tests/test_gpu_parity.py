@@ -381,11 +381,14 @@ def test_delta_copy_out_matches_widened_copy(n, pct, alpha):
         ref = (want.graph.offsets.copy(), want.graph.neighbors.copy(), want.members.copy())
         want = None
         ctx.option("d2h_mode", 0)
-        for _ in range(2):
-            got = b200.build(v, lists)
-            assert np.array_equal(got.graph.offsets, ref[0])
-            assert np.array_equal(got.members, ref[2])
-            assert np.array_equal(got.graph.neighbors, ref[1])
-            got = None
+        for gap16 in (0, 1, 2):  # auto, 16-bit gaps, byte gaps
+            ctx.option("d2h_gap16", gap16)
+            for _ in range(2):
+                got = b200.build(v, lists)
+                assert np.array_equal(got.graph.offsets, ref[0])
+                assert np.array_equal(got.members, ref[2])
+                assert np.array_equal(got.graph.neighbors, ref[1])
+                got = None
     finally:
         ctx.option("d2h_mode", 0)
+        ctx.option("d2h_gap16", 0)
