@@ -300,6 +300,8 @@ def bench_gpu(args) -> None:
     # device CSR ids are int32 (widened to the API's int64 on the host during the D2H copy)
     fill_bytes = (2 * edges) * 4 + (members + 1) * 8 + members * 8 + n * plan.list_size * 4 + words_b
     achieved = fill_bytes / (fill_ms * 1e-3) / 1e9
+    # the fill kernel the native layer picks for this size (abi.cu fill_rows_device)
+    fill_kernel = "k_fill_blk" if n <= 131072 else "k_fill_seg"
     # the commuting-pair sweep against the survey's POPC-issue bound (1 POPC / pair / clk)
     sm_mhz = (clocks.summary().get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0))
     popc_bound = 148 * 16 * sm_mhz * 1e6
@@ -323,16 +325,16 @@ def bench_gpu(args) -> None:
                 "host_output_bytes_per_step": int(out_bytes),
                 "host_output": "int64 numpy (members, offsets, neighbors); the neighbors buffer "
                                "is reused across steps once the previous step's graph is "
-                               "dropped (hostpool.py); neighbor ids cross PCIe as byte gaps "
-                               "and are decoded on the host"},
+                               "dropped (hostpool.py); neighbor ids cross PCIe as 8- or 16-bit "
+                               "gaps and are decoded on the host"},
         "gpu_launches": int(launches),
         "kernel_ms": {"commute_sweep_k1": float(kt[0]), "conflict_rows_count_k2b": float(kt[1]),
                       "conflict_rows_fill_k2b": float(kt[2]), "compaction": float(kt[3]),
                       "prep_incl_bucket_masks_k2a": float(kt[4])},
-        "roofline": {"bound": "hbm", "kernel": "conflict-row fill (k_fill_seg)",
+        "roofline": {"bound": "hbm", "kernel": f"conflict-row fill ({fill_kernel})",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": (measured_traffic("k_fill_seg") or (None, None))[0],
-                     "traffic_source": (measured_traffic("k_fill_seg") or (None, None))[1],
+                     "traffic": (measured_traffic(fill_kernel) or (None, None))[0],
+                     "traffic_source": (measured_traffic(fill_kernel) or (None, None))[1],
                      "bytes_per_launch": int(fill_bytes),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
         "int_roofline": {"kernel": "commuting-pair sweep (k_commute_fr2, 64-bit four-Russians tables)", "achieved": k1_rate,

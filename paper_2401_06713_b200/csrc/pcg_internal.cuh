@@ -97,6 +97,18 @@ struct SegArgs {
     const int32_t *bnd;    // (P, nwin+1) members of each bucket below each window start
 };
 
+struct BlkArgs {
+    int32_t threads;       // threads per CTA (one row per CTA)
+    int32_t groups;        // 128-id groups per thread (power of two <= 16)
+    int32_t wb;            // window ids = threads * groups * 128
+    int32_t nwin;          // windows per row
+    int32_t dcap;          // descriptor slots in shared memory (multiple of 8)
+    int32_t lcap;          // color slots (>= longest list)
+    int32_t nga;           // bitmap groups held in shared memory (multiple of groups)
+    int32_t ecap;          // admitted-id list capacity per window (0: always re-decode)
+    const int32_t *bnd;    // (P, nwin+1) members of each bucket below each window start
+};
+
 struct MergeArgs {
     int32_t cap;           // ids per warp buffer; longer rows go to the bitmap fill
     int32_t *heavy;        // out: rows longer than cap
@@ -159,6 +171,9 @@ int launch_fill_coop(const RowArgs &a, bool out64, int sms, cudaStream_t s);
 void seg_geometry(int64_t n, int64_t max_bits, int32_t *wb, int32_t *nwin, int32_t *seg);
 int launch_window_bounds(const int32_t *bstart, const int32_t *bpos, const int32_t *bmemp,
                          int64_t P, int nwin, int32_t wb, int32_t *bnd, cudaStream_t s);
+size_t blk_smem_bytes(const BlkArgs &g, int groups);
+void blk_geometry(int64_t n, int threads, int groups, BlkArgs *g);
+int launch_fill_blk(const RowArgs &a, const BlkArgs &g, bool out64, int sms, cudaStream_t s);
 int launch_fill_seg(const RowArgs &a, const SegArgs &g, bool out64, int sms, cudaStream_t s);
 int launch_delta(bool write, bool wide, const int32_t *nbr, const int64_t *rowoff, int64_t rows,
                  void *bytes, int32_t *xcount, const int64_t *xoff, int32_t *xval, int sms,
@@ -195,9 +210,10 @@ struct pcg_ctx {
     int window = 0;     // K2 window bits (0 auto)
     int fr_ichunk = 0;  // four-Russians i-chunk (0 auto)
     int merge_cap = 0;  // fill-merge buffer cap (0 auto; testing knob)
-    int fill_algo = 0;  // owned masks: 0 segmented fill (warp-decoded words, lane-segment
-                        // harvest), 3 lane-per-bucket bitmap fill, 1 cooperative bitmap,
-                        // 2 merge, 4 TMA-staged owned runs
+    int fill_algo = 0;  // owned masks: 0 auto (block fill up to 128K ids, else segmented),
+                        // 5 block fill (CTA per row), 6 segmented fill (warp-decoded words,
+                        // lane-segment harvest), 3 lane-per-bucket bitmap fill,
+                        // 1 cooperative bitmap, 2 merge, 4 TMA-staged owned runs
     int seg_bits = 0;   // segmented fill: max window bits per warp (0 auto)
     int seg_warps = 0;  // segmented fill: warps per block (0 auto)
     int own_algo = 0;   // owned masks: 0 four-Russians tables (when kw allows), 1 per-pair
@@ -244,6 +260,7 @@ struct pcg_ctx {
     std::vector<cudaEvent_t> chunk_ev;  // direct D2H: one event per chunk
     int64_t copy_bytes = 0;                    // D2H bytes of the last pcg_fill
     int d2h_gap16 = 0;  // delta copy-out gap width: 0 auto (mean gap), 1 16-bit, 2 bytes
+    int blk_threads = 0, blk_groups = 0, blk_dcap = 0, blk_ecap = 0;  // block fill geometry (0 = auto)
     int k1_async = 0;                          // K1 on a side stream, result collected later
     bool k1_pending = false;
     cudaStream_t k1_stream = nullptr;

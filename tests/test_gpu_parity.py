@@ -79,8 +79,8 @@ def test_merge_heavy_rows_fallback(golden_cases, cap):
         ctx.option("k2_mode", 0)
 
 
-@pytest.mark.parametrize("fill_algo", [0, 1, 2, 3, 4],
-                         ids=["segmented", "coop", "merge", "lane-bitmap", "runs-tma"])
+@pytest.mark.parametrize("fill_algo", [0, 1, 2, 3, 4, 5, 6],
+                         ids=["auto", "coop", "merge", "lane-bitmap", "runs-tma", "block", "segmented"])
 def test_owned_fill_variants(golden_cases, fill_algo):
     ctx = _native.context()
     ctx.option("k2_mode", 3)
@@ -116,6 +116,7 @@ def test_segmented_fill_geometry(golden_cases, golden_ref, bits, warps):
     """Window size (1..many windows per row) and warps per block must not change a single
     entry."""
     ctx = _native.context()
+    ctx.option("fill_algo", 6)
     ctx.option("seg_bits", bits)
     ctx.option("seg_warps", warps)
     try:
@@ -128,8 +129,36 @@ def test_segmented_fill_geometry(golden_cases, golden_ref, bits, warps):
             assert (sha(gc.graph.offsets), sha(gc.graph.neighbors)) == (
                 g["offsets_sha"], g["neighbors_sha"])
     finally:
+        ctx.option("fill_algo", 0)
         ctx.option("seg_bits", 0)
         ctx.option("seg_warps", 0)
+
+
+@pytest.mark.parametrize("threads,groups,dcap,ecap", [
+    (32, 1, 0, 0), (64, 2, 8, 32), (128, 4, 0, -1), (256, 1, 16, 0), (256, 4, 0, 64),
+    (512, 16, 0, 0), (1024, 8, 24, -1), (128, 8, 0, 0), (96, 2, 0, 100)])
+def test_block_fill_geometry(golden_cases, golden_ref, threads, groups, dcap, ecap):
+    """Block fill: CTA size, groups per thread (1..many windows per row), descriptor chunking
+    and the admitted-id list (fits / overflows into the re-decode / disabled) must not change
+    a single entry."""
+    ctx = _native.context()
+    ctx.option("fill_algo", 5)
+    ctx.option("blk_threads", threads)
+    ctx.option("blk_groups", groups)
+    ctx.option("blk_dcap", dcap)
+    ctx.option("blk_ecap", ecap)
+    try:
+        for case in golden_cases:
+            case.check(b200.build(case.view, case.lists))
+        for n in (10000, 20000):
+            g = golden_ref["builds_hashed"][f"q32_n{n}"]
+            v = pauli_view(n, 32, 0)
+            gc = b200.build(v, random_lists(v, seed=0))
+            assert (sha(gc.graph.offsets), sha(gc.graph.neighbors)) == (
+                g["offsets_sha"], g["neighbors_sha"])
+    finally:
+        for k in ("fill_algo", "blk_threads", "blk_groups", "blk_dcap", "blk_ecap"):
+            ctx.option(k, 0)
 
 
 @pytest.mark.parametrize("window", [4096, 8192])

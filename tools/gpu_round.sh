@@ -12,7 +12,7 @@ timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv \
    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-clocks --no-run > $OUT/ncu_bench.log 2>&1
-for k in k_fill_seg k_owned_fr k_commute_fr2 k_delta; do
+for k in k_fill_blk k_owned_fr k_commute_fr2 k_delta; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 \
      -o $OUT/full_$k python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-clocks --no-run > $OUT/ncu_full_$k.log 2>&1
 done

@@ -25,6 +25,8 @@ ap.add_argument("--seg-warps", type=int, default=0)
 ap.add_argument("--own", type=int, default=0)
 ap.add_argument("--wide", type=int, default=1)
 ap.add_argument("--own-direct", type=int, default=1)
+ap.add_argument("--blk-threads", type=int, default=0)
+ap.add_argument("--blk-groups", type=int, default=0)
 ap.add_argument("--check", action="store_true", help="compare the CSR with fill_algo 3")
 a = ap.parse_args()
 
@@ -43,6 +45,8 @@ ctx.option("seg_warps", a.seg_warps)
 ctx.option("own_algo", a.own)
 ctx.option("k1_wide", a.wide)
 ctx.option("own_direct", a.own_direct)
+ctx.option("blk_threads", a.blk_threads)
+ctx.option("blk_groups", a.blk_groups)
 ctx.profiling(True)
 stage(v, lists, ctx)
 print("prep ms", ctx.kernel_times()[4])
@@ -64,3 +68,12 @@ for r in range(a.reps):
 t = time.time()
 gc = b200.build(v, lists)
 print(f"e2e build {time.time()-t:.3f} s")
+if a.check:  # the same CSR with the default fill
+    import hashlib
+    h = lambda x: hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest()[:16]
+    got = (h(gc.graph.offsets), h(gc.graph.neighbors), h(gc.members))
+    gc = None
+    ctx.option("fill_algo", 0)
+    ref = b200.build(v, lists)
+    want = (h(ref.graph.offsets), h(ref.graph.neighbors), h(ref.members))
+    print("check vs default fill:", "MATCH" if got == want else f"MISMATCH {got} {want}")
