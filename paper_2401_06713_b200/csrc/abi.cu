@@ -10,6 +10,9 @@
 #include <immintrin.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -174,6 +177,11 @@ int pcg_destroy(pcg_ctx *ctx) {
     release(ctx->dxcnt);
     release(ctx->dxoff);
     release(ctx->dxval);
+    release(ctx->mrow);
+    for (auto &e : ctx->piece_ev) cudaEventDestroy(e);
+    if (ctx->scan_ev) cudaEventDestroy(ctx->scan_ev);
+    for (auto &hp : ctx->hxpiece)
+        if (hp.first) cudaFreeHost(hp.first);
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
     for (auto &h : ctx->stage)
@@ -202,6 +210,8 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "k1_async")) ctx->k1_async = (int)value;
     else if (!strcmp(key, "k1_wide")) ctx->k1_wide = (int)value;
     else if (!strcmp(key, "d2h_gap16")) ctx->d2h_gap16 = (int)value;
+    else if (!strcmp(key, "d2h_pipe")) ctx->d2h_pipe = (int)value;
+    else if (!strcmp(key, "d2h_pieces")) ctx->d2h_pieces = (int)value;
     else if (!strcmp(key, "blk_threads")) ctx->blk_threads = (int)value;
     else if (!strcmp(key, "blk_groups")) ctx->blk_groups = (int)value;
     else if (!strcmp(key, "blk_dcap")) ctx->blk_dcap = (int)value;
@@ -1120,7 +1130,7 @@ static int d2h_delta(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, int64_t
     for (size_t k = 0; k < nch; ++k)
         maxb = std::max<size_t>(maxb, (size_t)(offsets[cr[k + 1]] - offsets[cr[k]]) * gb);
     const int W = ctx->d2h_threads > 0 ? ctx->d2h_threads : std::min(16, omp_get_num_procs());
-    if (ctx->hbytes_cap < maxb || (int)ctx->hbytes.size() != 2 * W) {
+    if (ctx->hbytes_cap < maxb || (int)ctx->hbytes.size() < 2 * W) {
         for (uint8_t *p : ctx->hbytes)
             if (p) cudaFreeHost(p);
         ctx->hbytes.assign(2 * W, nullptr);
@@ -1176,6 +1186,201 @@ static int d2h_delta(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, int64_t
         cudaStreamSynchronize(st);
     }
     if (failed) return fail(ctx, PCG_E_CUDA, "delta copy-out failed");
+    return PCG_OK;
+}
+
+static int fill_rows_device(pcg_ctx *ctx, int64_t r0, int64_t r1, const int32_t *deg,
+                            int32_t maxdeg, bool identity, void *out, int64_t out_base,
+                            int *launches, bool out64 = true, const int32_t *rows_list = nullptr);
+
+// Public build, pipelined: the member rows are cut into pieces (whole copy-out chunks).  For
+// each piece the build stream runs the fill (rows via the member -> row list), the gap count,
+// a piece-local scan of the exception counts, a small readback of the piece's exception
+// offsets (their total sizes the exception copy), the gap/exception write and the exception
+// D2H; host workers decode the chunks of every finished piece while later pieces are filled.
+static int fill_delta_pipe(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, int64_t nm,
+                           int64_t nnz, int *launches) {
+    cudaStream_t s = ctx->stream;
+    const double mean_gap = nnz > 0 ? (double)ctx->n * (double)nm / (double)nnz : 0.0;
+    const bool wide = ctx->d2h_gap16 == 1 || (ctx->d2h_gap16 == 0 && mean_gap > 64.0);
+    const size_t gb = wide ? 2 : 1;
+    PCG_ALLOC(ctx, ctx->dbytes, (size_t)nnz * gb);
+    PCG_ALLOC(ctx, ctx->dxcnt, (size_t)(nm + 1) * 4);
+    PCG_ALLOC(ctx, ctx->dxoff, (size_t)(nm + 1) * 8);
+    if (ctx->hxoff_cap < (size_t)(nm + 1)) {
+        if (ctx->hxoff) cudaFreeHost(ctx->hxoff);
+        ctx->hxoff = nullptr;
+        PCG_TRY_CUDA(ctx, cudaHostAlloc(reinterpret_cast<void **>(&ctx->hxoff), (size_t)(nm + 1) * 8, cudaHostAllocDefault));
+        ctx->hxoff_cap = (size_t)(nm + 1);
+    }
+    // copy-out chunks (row-aligned, ~CH entries) and pieces (runs of whole chunks)
+    const int64_t CH = ctx->d2h_chunk > 0 ? ctx->d2h_chunk : (int64_t)1 << 19;
+    std::vector<int64_t> cr;
+    cr.push_back(0);
+    while (cr.back() < nm) {
+        const int64_t want = offsets[cr.back()] + CH;
+        int64_t r = std::upper_bound(offsets + cr.back() + 1, offsets + nm + 1, want) - offsets - 1;
+        if (r <= cr.back()) r = cr.back() + 1;
+        cr.push_back(std::min<int64_t>(r, nm));
+    }
+    const int64_t nch = (int64_t)cr.size() - 1;
+    // measured at c2 (16 host cores): 8-12 pieces with 15 decoders best (e2e median 14.3-14.5
+    // ms vs 16.3-18.9 for fill-then-copy-out); 24 pieces lose to the per-piece readbacks
+    const int64_t want_pieces = ctx->d2h_pieces > 0 ? ctx->d2h_pieces : 8;
+    const int64_t cpp = std::max<int64_t>(1, (nch + want_pieces - 1) / want_pieces);  // chunks per piece
+    const int64_t K = (nch + cpp - 1) / cpp;
+    size_t maxb = 0;
+    for (int64_t k = 0; k < nch; ++k)
+        maxb = std::max<size_t>(maxb, (size_t)(offsets[cr[k + 1]] - offsets[cr[k]]) * gb);
+    // decoders: one core is left to the orchestrating thread
+    const int W = ctx->d2h_threads > 0 ? ctx->d2h_threads
+                                       : std::max(1, std::min(16, omp_get_num_procs() - 1));
+    if (ctx->hbytes_cap < maxb || (int)ctx->hbytes.size() < 2 * W) {
+        for (uint8_t *p : ctx->hbytes)
+            if (p) cudaFreeHost(p);
+        ctx->hbytes.assign(2 * W, nullptr);
+        ctx->hbytes_cap = std::max<size_t>(maxb, (size_t)CH * gb);
+        for (int k = 0; k < 2 * W; ++k)
+            PCG_TRY_CUDA(ctx, cudaHostAlloc(reinterpret_cast<void **>(&ctx->hbytes[k]), ctx->hbytes_cap, cudaHostAllocDefault));
+    }
+    while ((int)ctx->ring_ev.size() < 2 * W + 1) {
+        cudaEvent_t e;
+        PCG_TRY_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ctx->ring_ev.push_back(e);
+    }
+    while ((int)ctx->ring_st.size() < W) {
+        cudaStream_t st;
+        PCG_TRY_CUDA(ctx, cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        ctx->ring_st.push_back(st);
+    }
+    while ((int64_t)ctx->piece_ev.size() < K) {  // blocking-sync: waiters sleep, not spin
+        cudaEvent_t e;
+        PCG_TRY_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync));
+        ctx->piece_ev.push_back(e);
+    }
+    if (!ctx->scan_ev) PCG_TRY_CUDA(ctx, cudaEventCreateWithFlags(&ctx->scan_ev, cudaEventDisableTiming | cudaEventBlockingSync));
+    while ((int64_t)ctx->hxpiece.size() < K) ctx->hxpiece.push_back({nullptr, 0});
+    // the scan's temporary storage, sized for the largest piece
+    cub::CountingInputIterator<int64_t> idx(0);
+    size_t tmp = 0;
+    {
+        cub::TransformInputIterator<int64_t, DegAt, cub::CountingInputIterator<int64_t>> xc(
+            idx, DegAt{ctx->dxcnt.as<int32_t>(), nm});
+        PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, tmp, xc, ctx->dxoff.as<int64_t>(), nm + 1, s));
+    }
+    PCG_ALLOC(ctx, ctx->cubtmp, tmp);
+    // device exceptions of one piece (row starts + long gaps); grown inside a piece if needed
+    PCG_ALLOC(ctx, ctx->dxval, (size_t)(2 * (nm + nnz / 16) / K + 1024) * 4);
+    static const bool simd = __builtin_cpu_supports("avx512f");
+    const uint8_t *src = ctx->dbytes.as<uint8_t>();
+    std::atomic<int64_t> ready(0);  // pieces whose exceptions are queued for the host
+    std::atomic<int> failed(0);
+    int orc = PCG_OK;
+    int64_t xbytes = 0;
+
+    // one piece on the build stream; returns a status (runs on the orchestrating thread)
+    auto run_piece = [&](int64_t p) -> int {
+        const int64_t m0 = cr[p * cpp], m1 = cr[std::min(nch, (p + 1) * cpp)];
+        int rc = fill_rows_device(ctx, m0, m1, ctx->deg.as<int32_t>(), ctx->maxdeg, nm == ctx->n,
+                                  ctx->nbr_o.p, 0, launches, /*out64=*/false, ctx->mrow.as<int32_t>());
+        if (rc) return rc;
+        const int64_t rows = m1 - m0;
+        launch_delta(false, wide, ctx->nbr_o.as<int32_t>(), ctx->offsets_o.as<int64_t>() + m0, rows,
+                     ctx->dbytes.p, ctx->dxcnt.as<int32_t>() + m0, nullptr, nullptr, ctx->sms, s);
+        PCG_CHECK_LAUNCH(ctx);
+        cub::TransformInputIterator<int64_t, DegAt, cub::CountingInputIterator<int64_t>> xc(
+            idx, DegAt{ctx->dxcnt.as<int32_t>() + m0, rows});
+        size_t t = tmp;
+        PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->cubtmp.p, t, xc, ctx->dxoff.as<int64_t>() + m0, rows + 1, s));
+        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->hxoff + m0, ctx->dxoff.as<int64_t>() + m0, (size_t)(rows + 1) * 8,
+                                          cudaMemcpyDeviceToHost, s));
+        PCG_TRY_CUDA(ctx, cudaEventRecord(ctx->scan_ev, s));
+        PCG_TRY_CUDA(ctx, cudaEventSynchronize(ctx->scan_ev));
+        const int64_t X = ctx->hxoff[m1];  // exceptions of this piece (piece-relative offsets)
+        auto &hp = ctx->hxpiece[p];
+        if (hp.second < (size_t)std::max<int64_t>(X, 1)) {
+            if (hp.first) cudaFreeHost(hp.first);
+            hp.first = nullptr;
+            hp.second = (size_t)std::max<int64_t>(X, 1) + ((size_t)std::max<int64_t>(X, 1) >> 2);
+            PCG_TRY_CUDA(ctx, cudaHostAlloc(reinterpret_cast<void **>(&hp.first), hp.second * 4, cudaHostAllocDefault));
+        }
+        PCG_ALLOC(ctx, ctx->dxval, (size_t)std::max<int64_t>(X, 1) * 4);
+        launch_delta(true, wide, ctx->nbr_o.as<int32_t>(), ctx->offsets_o.as<int64_t>() + m0, rows, nullptr,
+                     nullptr, ctx->dxoff.as<int64_t>() + m0, ctx->dxval.as<int32_t>(), ctx->sms, s);
+        PCG_CHECK_LAUNCH(ctx);
+        if (X > 0)
+            PCG_TRY_CUDA(ctx, cudaMemcpyAsync(hp.first, ctx->dxval.p, (size_t)X * 4, cudaMemcpyDeviceToHost, s));
+        PCG_TRY_CUDA(ctx, cudaEventRecord(ctx->piece_ev[p], s));
+        xbytes += X * 4 + (rows + 1) * 8;
+        return PCG_OK;
+    };
+
+#pragma omp parallel num_threads(W + 1)
+    {
+        const int w = omp_get_thread_num();
+        cudaSetDevice(ctx->device);
+        if (w == W) {  // orchestrator: pieces in order on the build stream
+            for (int64_t p = 0; p < K && !failed.load(); ++p) {
+                const int rc = run_piece(p);
+                if (rc) {
+                    orc = rc;
+                    failed.store(1);
+                }
+                ready.store(p + 1, std::memory_order_release);
+            }
+            ready.store(K, std::memory_order_release);
+        } else {  // decoder w: chunks w, w+W, ... double-buffered on its own stream
+            cudaStream_t st = ctx->ring_st[w];
+            auto piece_ready = [&](int64_t k) { return ready.load(std::memory_order_acquire) > k / cpp; };
+            auto issue = [&](int64_t k, int slot) -> cudaError_t {
+                cudaError_t e = cudaStreamWaitEvent(st, ctx->piece_ev[k / cpp], 0);
+                const int64_t b0 = offsets[cr[k]], b1 = offsets[cr[k + 1]];
+                if (e == cudaSuccess)
+                    e = cudaMemcpyAsync(ctx->hbytes[2 * w + slot], src + b0 * gb, (size_t)(b1 - b0) * gb,
+                                        cudaMemcpyDeviceToHost, st);
+                if (e == cudaSuccess) e = cudaEventRecord(ctx->ring_ev[2 * w + slot], st);
+                return e;
+            };
+            int64_t issued = w - W;  // last chunk whose copy is queued
+            int slot = 0;
+            for (int64_t k = w; k < nch && !failed.load(); k += W, slot ^= 1) {
+                if (issued < k) {  // not prefetched: wait for its piece, then copy it
+                    while (!piece_ready(k) && !failed.load())  // sleep: leave the core to the
+                        std::this_thread::sleep_for(std::chrono::microseconds(10));  // orchestrator
+                    if (failed.load() || issue(k, slot) != cudaSuccess) {
+                        failed.store(1);
+                        break;
+                    }
+                    issued = k;
+                }
+                // prefetch the next chunk only if its piece is already out (never wait here)
+                if (k + W < nch && piece_ready(k + W)) {
+                    if (issue(k + W, slot ^ 1) != cudaSuccess) {
+                        failed.store(1);
+                        break;
+                    }
+                    issued = k + W;
+                }
+                const int64_t p = k / cpp;
+                // the piece's exceptions and offsets are on the host once its event completed
+                if (cudaEventSynchronize(ctx->piece_ev[p]) != cudaSuccess ||
+                    cudaEventSynchronize(ctx->ring_ev[2 * w + slot]) != cudaSuccess) {
+                    failed.store(1);
+                    break;
+                }
+                const int64_t r0 = cr[k], x0 = offsets[r0], x1 = offsets[cr[k + 1]];
+                const int32_t *xv = ctx->hxpiece[p].first;
+                if (wide)
+                    delta_decode<uint16_t>(simd, dst, ctx->hbytes[2 * w + slot], x0, x1, offsets, r0, xv, ctx->hxoff[r0]);
+                else
+                    delta_decode<uint8_t>(simd, dst, ctx->hbytes[2 * w + slot], x0, x1, offsets, r0, xv, ctx->hxoff[r0]);
+            }
+            cudaStreamSynchronize(st);
+        }
+    }
+    if (orc) return orc;
+    if (failed.load()) return fail(ctx, PCG_E_CUDA, "pipelined fill / delta copy-out failed");
+    ctx->copy_bytes += (int64_t)nnz * (int64_t)gb + xbytes;  // gaps, exceptions, their offsets
     return PCG_OK;
 }
 
@@ -1283,9 +1488,10 @@ static int d2h_widen(pcg_ctx *ctx, int64_t *dst, const int32_t *src, size_t coun
 // bitmap row kernel; otherwise the bitmap row kernel for every row.
 static int fill_rows_device(pcg_ctx *ctx, int64_t r0, int64_t r1, const int32_t *deg,
                             int32_t maxdeg, bool identity, void *out, int64_t out_base,
-                            int *launches, bool out64 = true) {
+                            int *launches, bool out64, const int32_t *rows_list) {
     cudaStream_t s = ctx->stream;
     RowArgs a = row_args(ctx, r0, r1);
+    if (rows_list) a.rows_list = rows_list;  // [r0, r1) index this list of rows
     a.deg = const_cast<int32_t *>(deg);
     a.rowoff = ctx->rowoff.as<int64_t>();
     a.compact = identity ? nullptr : ctx->compact.as<int32_t>();
@@ -1437,13 +1643,18 @@ static int fill_impl(pcg_ctx *ctx, bool to_host, int64_t *members, int64_t *offs
     PCG_ALLOC(ctx, ctx->members_o, (size_t)std::max<int64_t>(nm, 1) * 8);
     PCG_ALLOC(ctx, ctx->offsets_o, (size_t)(nm + 1) * 8);
     PCG_ALLOC(ctx, ctx->nbr_o, (size_t)std::max<int64_t>(nnz, 1) * 4);
+    // public build with the delta copy-out: the fill runs in pieces inside the copy-out, each
+    // piece overlapping the host decode of the previous ones
+    const bool pipe = to_host && neighbors && offsets && nnz > 0 && ctx->d2h_mode == 0 && ctx->d2h_pipe != 0;
+    if (pipe) PCG_ALLOC(ctx, ctx->mrow, (size_t)std::max<int64_t>(nm, 1) * 4);
     *launches += launch_compact(ctx->deg.as<int32_t>(), n,
                                 nm == n ? nullptr : ctx->compact.as<int32_t>(),
                                 ctx->rowoff.as<int64_t>(), ctx->active.as<int64_t>(),
-                                ctx->members_o.as<int64_t>(), ctx->offsets_o.as<int64_t>(), s);
+                                ctx->members_o.as<int64_t>(), ctx->offsets_o.as<int64_t>(),
+                                pipe ? ctx->mrow.as<int32_t>() : nullptr, s);
     PCG_CHECK_LAUNCH(ctx);
     if (ctx->prof) cudaEventRecord(ctx->ev[4], s);
-    if (nnz > 0) {
+    if (nnz > 0 && !pipe) {
         rc = fill_rows_device(ctx, 0, n, ctx->deg.as<int32_t>(), ctx->maxdeg, nm == n,
                               ctx->nbr_o.p, 0, launches, /*out64=*/false);
         if (rc) return rc;
@@ -1464,7 +1675,9 @@ static int fill_impl(pcg_ctx *ctx, bool to_host, int64_t *members, int64_t *offs
         const bool pinned = cudaPointerGetAttributes(&at, neighbors) == cudaSuccess &&
                             at.type == cudaMemoryTypeHost;
         cudaGetLastError();
-        if (ctx->d2h_mode == 0 && offsets)  // byte-delta copy-out (default)
+        if (pipe)  // pieces of fill + delta copy-out (default)
+            rc = fill_delta_pipe(ctx, neighbors, offsets, nm, nnz, launches);
+        else if (ctx->d2h_mode == 0 && offsets)  // delta copy-out after the whole fill
             rc = d2h_delta(ctx, neighbors, offsets, nm, nnz);
         else if (pinned && ctx->d2h_mode == 3)
             rc = d2h_widen_direct(ctx, neighbors, ctx->nbr_o.as<int32_t>(), (size_t)nnz);

@@ -184,7 +184,7 @@ int launch_class_pairs(bool emit, const int64_t *keys, const int32_t *vals, int6
                        const int64_t *off, int64_t cap, int64_t *pairs, cudaStream_t s);
 int launch_compact(const int32_t *deg, int64_t n, const int32_t *compact, const int64_t *rowoff,
                    const int64_t *active, int64_t *members_out, int64_t *offsets_out,
-                   cudaStream_t s);
+                   int32_t *mrow, cudaStream_t s);
 
 // Tile arithmetic shared by host and kernels.
 __host__ __device__ inline int64_t tri_tiles(int64_t T) { return T * (T + 1) / 2; }
@@ -260,6 +260,12 @@ struct pcg_ctx {
     std::vector<cudaEvent_t> chunk_ev;  // direct D2H: one event per chunk
     int64_t copy_bytes = 0;                    // D2H bytes of the last pcg_fill
     int d2h_gap16 = 0;  // delta copy-out gap width: 0 auto (mean gap), 1 16-bit, 2 bytes
+    int d2h_pipe = 1;   // public build: fill in pieces overlapping the copy-out (0 = off)
+    int d2h_pieces = 0; // pieces of the pipelined fill (0 auto)
+    pcg::DevBuf mrow;   // member -> active row (pipelined fill)
+    std::vector<cudaEvent_t> piece_ev;
+    cudaEvent_t scan_ev = nullptr;
+    std::vector<std::pair<int32_t *, size_t>> hxpiece;  // pinned exceptions per piece
     int blk_threads = 0, blk_groups = 0, blk_dcap = 0, blk_ecap = 0;  // block fill geometry (0 = auto)
     int k1_async = 0;                          // K1 on a side stream, result collected later
     bool k1_pending = false;

@@ -545,7 +545,7 @@ int run_masks(const BucketArgs &b, int sms, cudaStream_t s) {
 __global__ void k_compact(const int32_t *__restrict__ deg, int64_t n,
                           const int32_t *__restrict__ compact, const int64_t *__restrict__ rowoff,
                           const int64_t *__restrict__ active, int64_t *__restrict__ members,
-                          int64_t *__restrict__ offsets) {
+                          int64_t *__restrict__ offsets, int32_t *__restrict__ mrow) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int d = deg[i];
@@ -553,6 +553,7 @@ __global__ void k_compact(const int32_t *__restrict__ deg, int64_t n,
     if (d > 0) {
         members[k] = active[i];
         offsets[k] = rowoff[i];
+        if (mrow) mrow[k] = (int32_t)i;  // member -> active row (pipelined public fill)
     }
     if (i == n - 1) offsets[k + (d > 0 ? 1 : 0)] = rowoff[n];
 }
@@ -586,11 +587,11 @@ int launch_bucket_masks(const BucketArgs &b, int sms, cudaStream_t s) {
 
 int launch_compact(const int32_t *deg, int64_t n, const int32_t *compact, const int64_t *rowoff,
                    const int64_t *active, int64_t *members_out, int64_t *offsets_out,
-                   cudaStream_t s) {
+                   int32_t *mrow, cudaStream_t s) {
     if (n == 0) return 0;
     const int tb = 256;
     k_compact<<<(unsigned)((n + tb - 1) / tb), tb, 0, s>>>(deg, n, compact, rowoff, active,
-                                                           members_out, offsets_out);
+                                                           members_out, offsets_out, mrow);
     return 1;
 }
 
