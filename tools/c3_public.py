@@ -1,12 +1,12 @@
 """Config 3 through the public build (e2e) with sanity checks (diagnostic): sortedness,
-no self loops, offsets/size consistency, symmetry and oracle agreement of sampled rows."""
+no self loops, offsets/size consistency, symmetry of sampled rows.  The oracle comparison of
+sampled rows is tests/test_gpu_scale.py (PICASSO_SCALE=1)."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 import paper_2401_06713_b200 as b200
 import bench
-from oracle.oracle import OracleInstance  # noqa: E402  (test infrastructure: checker only)
 
 view, lists, plan = bench.make_inputs("c3", pinned=True)
 n = view.n_active
@@ -28,11 +28,4 @@ for r in rows:
     for j in row[:5]:
         rj = nb[off[j]:off[j + 1]]
         assert r in rj
-t0 = time.perf_counter()
-orc = OracleInstance(view.backing.words, view.active, lists)
-for r in rows[:8]:
-    loc = int(np.searchsorted(view.active, gc.members[r]))
-    want, _ = orc.row(loc)
-    assert np.array_equal(gc.members[nb[off[r]:off[r + 1]]], view.active[want]), r
-print(f"oracle rows checked in {time.perf_counter()-t0:.1f} s")
-print("c3 sampled rows match the oracle; sorted, symmetric, consistent")
+print("c3 sampled rows: sorted, symmetric, consistent")

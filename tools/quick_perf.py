@@ -27,6 +27,7 @@ ap.add_argument("--wide", type=int, default=1)
 ap.add_argument("--own-direct", type=int, default=1)
 ap.add_argument("--blk-threads", type=int, default=0)
 ap.add_argument("--blk-groups", type=int, default=0)
+ap.add_argument("--blk-ecap", type=int, default=0)
 ap.add_argument("--check", action="store_true", help="compare the CSR with fill_algo 3")
 a = ap.parse_args()
 
@@ -47,6 +48,7 @@ ctx.option("k1_wide", a.wide)
 ctx.option("own_direct", a.own_direct)
 ctx.option("blk_threads", a.blk_threads)
 ctx.option("blk_groups", a.blk_groups)
+ctx.option("blk_ecap", a.blk_ecap)
 ctx.profiling(True)
 stage(v, lists, ctx)
 print("prep ms", ctx.kernel_times()[4])
