@@ -178,6 +178,8 @@ int pcg_destroy(pcg_ctx *ctx) {
     release(ctx->dxoff);
     release(ctx->dxval);
     release(ctx->mrow);
+    release(ctx->dwide);
+    if (ctx->dma_st) cudaStreamDestroy(ctx->dma_st);
     for (auto &e : ctx->piece_ev) cudaEventDestroy(e);
     if (ctx->scan_ev) cudaEventDestroy(ctx->scan_ev);
     for (auto &hp : ctx->hxpiece)
@@ -212,6 +214,7 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "d2h_gap16")) ctx->d2h_gap16 = (int)value;
     else if (!strcmp(key, "d2h_pipe")) ctx->d2h_pipe = (int)value;
     else if (!strcmp(key, "d2h_pieces")) ctx->d2h_pieces = (int)value;
+    else if (!strcmp(key, "d2h_dma")) ctx->d2h_dma = (int)value;
     else if (!strcmp(key, "blk_threads")) ctx->blk_threads = (int)value;
     else if (!strcmp(key, "blk_groups")) ctx->blk_groups = (int)value;
     else if (!strcmp(key, "blk_dcap")) ctx->blk_dcap = (int)value;
@@ -1199,7 +1202,7 @@ static int fill_rows_device(pcg_ctx *ctx, int64_t r0, int64_t r1, const int32_t 
 // offsets (their total sizes the exception copy), the gap/exception write and the exception
 // D2H; host workers decode the chunks of every finished piece while later pieces are filled.
 static int fill_delta_pipe(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, int64_t nm,
-                           int64_t nnz, int *launches) {
+                           int64_t nnz, int *launches, bool pinned_dst) {
     cudaStream_t s = ctx->stream;
     const double mean_gap = nnz > 0 ? (double)ctx->n * (double)nm / (double)nnz : 0.0;
     const bool wide = ctx->d2h_gap16 == 1 || (ctx->d2h_gap16 == 0 && mean_gap > 64.0);
@@ -1229,6 +1232,28 @@ static int fill_delta_pipe(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, i
     const int64_t want_pieces = ctx->d2h_pieces > 0 ? ctx->d2h_pieces : 8;
     const int64_t cpp = std::max<int64_t>(1, (nch + want_pieces - 1) / want_pieces);  // chunks per piece
     const int64_t K = (nch + cpp - 1) / cpp;
+    // chunks shipped as int64 by DMA straight into a pinned destination (evenly spread), the
+    // rest as gaps decoded by the host: the copy engine and the decoders share the host
+    // memory bandwidth
+    const int dma_pct = pinned_dst ? (ctx->d2h_dma >= 0 ? std::min(ctx->d2h_dma, 100) : 0) : 0;
+    std::vector<char> direct(nch, 0);
+    std::vector<int64_t> dmaoff(nch, 0);
+    std::vector<int64_t> todo;  // the decoders' chunks
+    int64_t dma_entries = 0;
+    for (int64_t k = 0; k < nch; ++k) {
+        direct[k] = ((k + 1) * dma_pct / 100) > (k * dma_pct / 100);
+        if (direct[k]) {
+            dmaoff[k] = dma_entries;
+            dma_entries += offsets[cr[k + 1]] - offsets[cr[k]];
+        } else {
+            todo.push_back(k);
+        }
+    }
+    if (dma_entries > 0) {
+        PCG_ALLOC(ctx, ctx->dwide, (size_t)dma_entries * 8);
+        if (!ctx->dma_st) PCG_TRY_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->dma_st, cudaStreamNonBlocking));
+    }
+    const int64_t ntodo = (int64_t)todo.size();
     size_t maxb = 0;
     for (int64_t k = 0; k < nch; ++k)
         maxb = std::max<size_t>(maxb, (size_t)(offsets[cr[k + 1]] - offsets[cr[k]]) * gb);
@@ -1310,7 +1335,24 @@ static int fill_delta_pipe(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, i
         PCG_CHECK_LAUNCH(ctx);
         if (X > 0)
             PCG_TRY_CUDA(ctx, cudaMemcpyAsync(hp.first, ctx->dxval.p, (size_t)X * 4, cudaMemcpyDeviceToHost, s));
+        bool any_direct = false;
+        for (int64_t k = p * cpp; k < std::min(nch, (p + 1) * cpp); ++k) {
+            if (!direct[k]) continue;
+            const int64_t x0 = offsets[cr[k]], x1 = offsets[cr[k + 1]];
+            *launches += launch_widen(ctx->nbr_o.as<int32_t>() + x0, ctx->dwide.as<int64_t>() + dmaoff[k],
+                                      x1 - x0, ctx->sms, s);
+            any_direct = true;
+        }
         PCG_TRY_CUDA(ctx, cudaEventRecord(ctx->piece_ev[p], s));
+        if (any_direct) {
+            PCG_TRY_CUDA(ctx, cudaStreamWaitEvent(ctx->dma_st, ctx->piece_ev[p], 0));
+            for (int64_t k = p * cpp; k < std::min(nch, (p + 1) * cpp); ++k) {
+                if (!direct[k]) continue;
+                const int64_t x0 = offsets[cr[k]], x1 = offsets[cr[k + 1]];
+                PCG_TRY_CUDA(ctx, cudaMemcpyAsync(dst + x0, ctx->dwide.as<int64_t>() + dmaoff[k],
+                                                  (size_t)(x1 - x0) * 8, cudaMemcpyDeviceToHost, ctx->dma_st));
+            }
+        }
         xbytes += X * 4 + (rows + 1) * 8;
         return PCG_OK;
     };
@@ -1341,25 +1383,26 @@ static int fill_delta_pipe(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, i
                 if (e == cudaSuccess) e = cudaEventRecord(ctx->ring_ev[2 * w + slot], st);
                 return e;
             };
-            int64_t issued = w - W;  // last chunk whose copy is queued
+            int64_t issued = w - W;  // last of the decoders' chunks (index into todo) queued
             int slot = 0;
-            for (int64_t k = w; k < nch && !failed.load(); k += W, slot ^= 1) {
-                if (issued < k) {  // not prefetched: wait for its piece, then copy it
+            for (int64_t j = w; j < ntodo && !failed.load(); j += W, slot ^= 1) {
+                const int64_t k = todo[j];
+                if (issued < j) {  // not prefetched: wait for its piece, then copy it
                     while (!piece_ready(k) && !failed.load())  // sleep: leave the core to the
                         std::this_thread::sleep_for(std::chrono::microseconds(10));  // orchestrator
                     if (failed.load() || issue(k, slot) != cudaSuccess) {
                         failed.store(1);
                         break;
                     }
-                    issued = k;
+                    issued = j;
                 }
                 // prefetch the next chunk only if its piece is already out (never wait here)
-                if (k + W < nch && piece_ready(k + W)) {
-                    if (issue(k + W, slot ^ 1) != cudaSuccess) {
+                if (j + W < ntodo && piece_ready(todo[j + W])) {
+                    if (issue(todo[j + W], slot ^ 1) != cudaSuccess) {
                         failed.store(1);
                         break;
                     }
-                    issued = k + W;
+                    issued = j + W;
                 }
                 const int64_t p = k / cpp;
                 // the piece's exceptions and offsets are on the host once its event completed
@@ -1378,9 +1421,11 @@ static int fill_delta_pipe(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, i
             cudaStreamSynchronize(st);
         }
     }
+    if (dma_entries > 0 && cudaStreamSynchronize(ctx->dma_st) != cudaSuccess) failed.store(1);
     if (orc) return orc;
     if (failed.load()) return fail(ctx, PCG_E_CUDA, "pipelined fill / delta copy-out failed");
-    ctx->copy_bytes += (int64_t)nnz * (int64_t)gb + xbytes;  // gaps, exceptions, their offsets
+    // gaps of the decoded chunks, int64 of the DMA chunks, exceptions and their offsets
+    ctx->copy_bytes += (nnz - dma_entries) * (int64_t)gb + dma_entries * 8 + xbytes;
     return PCG_OK;
 }
 
@@ -1676,7 +1721,7 @@ static int fill_impl(pcg_ctx *ctx, bool to_host, int64_t *members, int64_t *offs
                             at.type == cudaMemoryTypeHost;
         cudaGetLastError();
         if (pipe)  // pieces of fill + delta copy-out (default)
-            rc = fill_delta_pipe(ctx, neighbors, offsets, nm, nnz, launches);
+            rc = fill_delta_pipe(ctx, neighbors, offsets, nm, nnz, launches, pinned);
         else if (ctx->d2h_mode == 0 && offsets)  // delta copy-out after the whole fill
             rc = d2h_delta(ctx, neighbors, offsets, nm, nnz);
         else if (pinned && ctx->d2h_mode == 3)

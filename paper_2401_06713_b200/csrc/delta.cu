@@ -56,6 +56,20 @@ __global__ void k_delta(const int32_t *__restrict__ nbr, const int64_t *__restri
 
 }  // namespace
 
+// int32 -> int64 widen of a CSR slice (chunks the pipelined copy-out ships as int64 by DMA)
+__global__ void k_widen(const int32_t *__restrict__ src, int64_t *__restrict__ dst, int64_t count) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < count;
+         x += (int64_t)gridDim.x * blockDim.x)
+        dst[x] = src[x];
+}
+
+int launch_widen(const int32_t *src, int64_t *dst, int64_t count, int sms, cudaStream_t s) {
+    if (count <= 0) return 0;
+    const int64_t grid = std::min<int64_t>((count + 255) / 256, (int64_t)sms * 8);
+    k_widen<<<(unsigned)grid, 256, 0, s>>>(src, dst, count);
+    return 1;
+}
+
 int launch_delta(bool write, bool wide, const int32_t *nbr, const int64_t *rowoff, int64_t rows,
                  void *bytes, int32_t *xcount, const int64_t *xoff, int32_t *xval, int sms,
                  cudaStream_t s) {

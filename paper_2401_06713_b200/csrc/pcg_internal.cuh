@@ -175,6 +175,7 @@ size_t blk_smem_bytes(const BlkArgs &g, int groups);
 void blk_geometry(int64_t n, int threads, int groups, BlkArgs *g);
 int launch_fill_blk(const RowArgs &a, const BlkArgs &g, bool out64, int sms, cudaStream_t s);
 int launch_fill_seg(const RowArgs &a, const SegArgs &g, bool out64, int sms, cudaStream_t s);
+int launch_widen(const int32_t *src, int64_t *dst, int64_t count, int sms, cudaStream_t s);
 int launch_delta(bool write, bool wide, const int32_t *nbr, const int64_t *rowoff, int64_t rows,
                  void *bytes, int32_t *xcount, const int64_t *xoff, int32_t *xval, int sms,
                  cudaStream_t s);
@@ -262,6 +263,9 @@ struct pcg_ctx {
     int d2h_gap16 = 0;  // delta copy-out gap width: 0 auto (mean gap), 1 16-bit, 2 bytes
     int d2h_pipe = 1;   // public build: fill in pieces overlapping the copy-out (0 = off)
     int d2h_pieces = 0; // pieces of the pipelined fill (0 auto)
+    int d2h_dma = -1;   // % of copy-out chunks sent as int64 by DMA into a pinned output (-1 auto)
+    pcg::DevBuf dwide;  // device int64 staging of those chunks
+    cudaStream_t dma_st = nullptr;
     pcg::DevBuf mrow;   // member -> active row (pipelined fill)
     std::vector<cudaEvent_t> piece_ev;
     cudaEvent_t scan_ev = nullptr;

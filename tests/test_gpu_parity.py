@@ -412,12 +412,15 @@ def test_delta_copy_out_matches_widened_copy(n, pct, alpha):
         ctx.option("d2h_mode", 0)
         # (pipelined fill, pieces, chunk ids, gap width): whole-fill copy-out, default pipeline,
         # one piece, many small pieces, a piece per chunk; 16-bit and byte gaps forced
-        for pipe, pieces, chunk, gap16 in [(0, 0, 0, 0), (1, 0, 0, 0), (1, 1, 0, 1), (1, 7, 4096, 2),
-                                           (1, 1000, 2048, 0), (0, 0, 0, 1), (1, 3, 0, 2)]:
+        # and the share of chunks shipped as int64 by DMA (pooled destinations are pinned)
+        for pipe, pieces, chunk, gap16, dma in [(0, 0, 0, 0, 0), (1, 0, 0, 0, -1), (1, 1, 0, 1, 0),
+                                                (1, 7, 4096, 2, 30), (1, 1000, 2048, 0, 50),
+                                                (0, 0, 0, 1, 0), (1, 3, 0, 2, 100)]:
             ctx.option("d2h_pipe", pipe)
             ctx.option("d2h_pieces", pieces)
             ctx.option("d2h_chunk", chunk)
             ctx.option("d2h_gap16", gap16)
+            ctx.option("d2h_dma", dma)
             for _ in range(2):
                 got = b200.build(v, lists)
                 assert np.array_equal(got.graph.offsets, ref[0])
@@ -425,5 +428,6 @@ def test_delta_copy_out_matches_widened_copy(n, pct, alpha):
                 assert np.array_equal(got.graph.neighbors, ref[1])
                 got = None
     finally:
-        for k, d in (("d2h_mode", 0), ("d2h_gap16", 0), ("d2h_pipe", 1), ("d2h_pieces", 0), ("d2h_chunk", 0)):
+        for k, d in (("d2h_mode", 0), ("d2h_gap16", 0), ("d2h_pipe", 1), ("d2h_pieces", 0), ("d2h_chunk", 0),
+                     ("d2h_dma", -1)):
             ctx.option(k, d)

@@ -11,14 +11,15 @@ wl = sys.argv[1] if len(sys.argv) > 1 else "c2"
 view, lists, _ = bench.make_inputs(wl, pinned=True)
 ctx = _native.context(0)
 res = {}
-# configs: pipe:pieces:threads tokens, e.g. 0:0:16 1:6:15
+# configs: pipe:pieces:threads[:dma%] tokens, e.g. 0:0:16 1:8:0:25
 specs = sys.argv[2:] or ["0:0:16", "1:6:16", "1:6:15", "1:12:15", "1:4:15", "1:8:15"]
-configs = [(sp, *map(int, sp.split(":"))) for sp in specs]
+configs = [(sp, *(list(map(int, sp.split(":"))) + [-1])[:4]) for sp in specs]
 for rnd in range(6):
-    for tag, pipe, pieces, thr in configs:
+    for tag, pipe, pieces, thr, dma in configs:
         ctx.option("d2h_pipe", pipe)
         ctx.option("d2h_pieces", pieces)
         ctx.option("d2h_threads", thr)
+        ctx.option("d2h_dma", dma)
         for k in range(3):
             torch.cuda.synchronize(); t0 = time.perf_counter()
             g = b200.build(view, lists)
