@@ -446,11 +446,11 @@ static int prep_device(pcg_ctx *ctx) {
                                    (uint64_t)std::max(1, ctx->L));
             if ((int64_t)m_max * std::max(1, ctx->L) >= (1 << 20)) o.fr = 0;  // umulhi range
             // direct-mapped ownership when the color table fits shared memory next to the
-            // rest (tags: level 6 bits | color 14 bits | member 12 bits), rectangular lists,
-            // and groups of members sharing a smaller color stay small (one level per member)
-            o.dtab_words = (int32_t)((P + 3) & ~3LL);
+            // rest (16-bit member tags, two per word), rectangular lists, and groups of
+            // members sharing a smaller color stay small (one level per member)
+            o.dtab_words = (int32_t)(((P + 1) / 2 + 3) & ~3LL);
             o.l16 = P < 65536 ? 1 : 0;
-            o.direct = (o.fr && ctx->own_direct != 0 && !ctx->ragged && P <= 14336 &&
+            o.direct = (o.fr && ctx->own_direct != 0 && !ctx->ragged && P <= 28672 &&
                         (int64_t)m_max * std::max(1, ctx->lmax - 1) <= 4 * P) ? 1 : 0;
             // measured: staging the lists pays when they are u16 (small palettes); u32 lists
             // next to the hash table cost occupancy (config 3)

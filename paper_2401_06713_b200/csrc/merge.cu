@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
     unsigned short *head = reinterpret_cast<unsigned short *>(osm + HS);  // HS: last coll + 1
     uint32_t *coll = osm + HS + HS / 2;                           // OWN_COLL: slot<<12 | k
     int32_t *link = reinterpret_cast<int32_t *>(coll + OWN_COLL); // OWN_COLL: previous in slot
-    uint32_t *dtab = osm;                                         // direct: P level|c|k tags
+    unsigned short *dtab = reinterpret_cast<unsigned short *>(osm);  // direct: P member tags
     uint32_t *lA = osm + o.dtab_words;                            // direct: losers (c'<<12|k)
     uint32_t *lB = lA + OWN_LCAP;
     int32_t *sid = reinterpret_cast<int32_t *>(osm + (o.direct ? o.dtab_words + 2 * OWN_LCAP
@@ -347,31 +347,32 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
             }
         };
         if (o.direct) {
-            // Leveled direct-mapped ownership: at level 1 every (c' < c, member k) writes the
-            // tag (level, c, k) into slot c' (last writer wins); after a barrier every writer
-            // whose tag was overwritten is a loser: it shares c' with the slot's winner (pair
-            // not owned by c) and retries at the next level with the other losers.  Level by
-            // level each group of members sharing c' yields every pair exactly once.
+            // Leveled direct-mapped ownership: at level 1 every (c' < c, member k) writes k
+            // into slot c' (last writer wins); after a barrier every writer whose k was
+            // overwritten is a loser: it shares c' with the slot's winner (pair not owned by c)
+            // and retries at the next level with the other losers.  Level by level each group
+            // of members sharing c' yields every pair exactly once.  A slot is only read in
+            // the round that just wrote it, and a member's colors are distinct, so the member
+            // index alone identifies the surviving write (16-bit tags, no reset between colors).
             auto clear_pair = [&](int k1, int k2) {
                 atomicAnd(&out[(int64_t)k1 * W + (k2 >> 5)], ~(1u << (k2 & 31)));
                 atomicAnd(&out[(int64_t)k2 * W + (k1 >> 5)], ~(1u << (k1 & 31)));
             };
-            const uint32_t ctag = (uint32_t)c << 12;
             const uint32_t items = (uint32_t)m * (uint32_t)o.L;
             if (tid == 0) nlose = 0;
             for (uint32_t e = tid; e < items; e += OWN_THREADS) {
                 const int k = (int)__umulhi(e, o.l_magic);
                 const int32_t cx = o.l16 ? (int32_t)sL16[e] : sL32[e];
-                if (cx < c) dtab[cx] = (1u << 26) | ctag | (uint32_t)k;
+                if (cx < c) dtab[cx] = (unsigned short)k;
             }
             __syncthreads();
             for (uint32_t e = tid; e < items; e += OWN_THREADS) {
                 const int k = (int)__umulhi(e, o.l_magic);
                 const int32_t cx = o.l16 ? (int32_t)sL16[e] : sL32[e];
                 if (cx < c) {
-                    const uint32_t w = dtab[cx];
-                    if (w != ((1u << 26) | ctag | (uint32_t)k)) {
-                        clear_pair(k, (int)(w & 0xfffu));
+                    const int w = dtab[cx];
+                    if (w != k) {
+                        clear_pair(k, w);
                         const int q = atomicAdd(&nlose, 1);
                         if (q < OWN_LCAP) lA[q] = ((uint32_t)cx << 12) | (uint32_t)k;
                         else overflow = 2;
@@ -389,13 +390,13 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
                 __syncthreads();
                 if (tid == 0) nlose = 0;
                 for (int q = tid; q < nl; q += OWN_THREADS)
-                    dtab[src[q] >> 12] = (level << 26) | ctag | (src[q] & 0xfffu);
+                    dtab[src[q] >> 12] = (unsigned short)(src[q] & 0xfffu);
                 __syncthreads();
                 for (int q = tid; q < nl; q += OWN_THREADS) {
-                    const uint32_t w = dtab[src[q] >> 12];
+                    const int w = dtab[src[q] >> 12];
                     const int k = (int)(src[q] & 0xfffu);
-                    if (w != ((level << 26) | ctag | (uint32_t)k)) {
-                        clear_pair(k, (int)(w & 0xfffu));
+                    if (w != k) {
+                        clear_pair(k, w);
                         dst[atomicAdd(&nlose, 1)] = src[q];
                     }
                 }
