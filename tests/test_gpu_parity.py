@@ -312,6 +312,33 @@ def test_commute_count_both_kernels_vs_oracle(n, q, k1_algo):
         assert np.array_equal(gc.graph.neighbors[gc.graph.offsets[i]:gc.graph.offsets[i + 1]], row)
 
 
+@pytest.mark.parametrize("n,pct", [(40000, 50.0), (60000, 45.0)])
+def test_owned_direct_table_large_palette(n, pct):
+    """Palettes between 14336 and 28672 colors take the 16-bit direct ownership table: the CSR
+    must equal the hash-table path's, and sampled rows the oracle's."""
+    from oracle.oracle import OracleInstance
+
+    v = pauli_view(n, 32, 5)
+    lists = random_lists(v, pct=pct, seed=2)
+    assert 14336 < lists.palette_size <= 28672
+    ctx = _native.context()
+    try:
+        ctx.option("own_direct", 1)
+        a = b200.build(v, lists)
+        want = (sha(a.graph.offsets), sha(a.graph.neighbors), a.view_edges_scanned)
+        nb, off = a.graph.neighbors.copy(), a.graph.offsets.copy()
+        a = None
+        ctx.option("own_direct", 0)
+        b = b200.build(v, lists)
+        assert (sha(b.graph.offsets), sha(b.graph.neighbors), b.view_edges_scanned) == want
+    finally:
+        ctx.option("own_direct", 1)
+    inst = OracleInstance(v.backing.words, v.active, lists)
+    for i in (0, n // 2, n - 1):
+        row, _ = inst.row(i)
+        assert np.array_equal(nb[off[i]:off[i + 1]], row)
+
+
 def test_full_size_config2_properties():
     """BASELINE config 2 (100k x 32q): the oracle cannot build it in test time, so check
     size-independent properties: commuting-pair total against the oracle's popcount sweep,
