@@ -429,8 +429,9 @@ static int prep_device(pcg_ctx *ctx) {
     if (ctx->masked) {
         PCG_ALLOC(ctx, ctx->masks, std::max<size_t>(mask_bytes, 16));
         b.masks = ctx->masks.as<uint32_t>();
+        OwnArgs own{};
         if (ctx->owned) {
-            OwnArgs o{};
+            OwnArgs &o = own;
             o.lrel = ctx->lrel.as<int32_t>();
             o.loff = ctx->ragged ? ctx->loff.as<int64_t>() : nullptr;
             o.L = ctx->L;
@@ -455,6 +456,19 @@ static int prep_device(pcg_ctx *ctx) {
             // measured: staging the lists pays when they are u16 (small palettes); u32 lists
             // next to the hash table cost occupancy (config 3)
             o.stage_lists = (!ctx->ragged && o.l16) ? 1 : 0;
+            // shared memory: big buckets x long lists (e.g. 500k ids, P' = 2.5%, alpha = 3:
+            // ~1.7k members x 39 colors) do not fit with staged lists; the direct table reads
+            // the staged lists, so it goes too; if even the hash table does not fit, the
+            // bucket masks without ownership (dedupe in the row passes) take over
+            const size_t smem_cap = 227u * 1024u;
+            if (owned_masks_smem(o, ctx->kw) > smem_cap) {
+                o.stage_lists = 0;
+                o.direct = 0;
+            }
+            if (owned_masks_smem(o, ctx->kw) > smem_cap) ctx->owned = false;
+        }
+        if (ctx->owned) {
+            OwnArgs &o = own;
             PCG_TRY_CUDA(ctx, cudaMemsetAsync(o.overflow, 0, 4, s));
             const bool want_runs = ctx->fill_algo == 4;  // run lengths only feed the runs fill
             b.runlen = nullptr;

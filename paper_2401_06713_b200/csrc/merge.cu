@@ -1065,10 +1065,14 @@ int run_fill_runs(const RowArgs &a, const RunArgs &r, int sms, cudaStream_t s) {
     return 1;
 }
 
+size_t owned_smem(const OwnArgs &o, int kw) {
+    return (size_t)(o.hash_slots + o.hash_slots / 2 + 2 * OWN_COLL + o.m_cap + (size_t)o.m_cap * kw) * 4;
+}
+
 template <int KW>
 int run_owned(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s) {
     int per_sm = 0;
-    const size_t smem = (size_t)(o.hash_slots + o.hash_slots / 2 + 2 * OWN_COLL + o.m_cap + o.m_cap * b.kw) * 4;
+    const size_t smem = owned_smem(o, b.kw);
     cudaFuncSetAttribute(k_owned_masks<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_owned_masks<KW>, OWN_THREADS, smem);
     if (per_sm < 1) per_sm = 1;
@@ -1077,14 +1081,18 @@ int run_owned(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s) {
     return 1;
 }
 
-template <int KW>
-int run_owned_fr(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s) {
-    int per_sm = 0;
+size_t owned_fr_smem(const OwnArgs &o, int kw) {
     const size_t state = o.direct ? (size_t)o.dtab_words + 2 * OWN_LCAP
                                   : (size_t)o.hash_slots + o.hash_slots / 2 + 2 * OWN_COLL;
     const size_t lists = o.stage_lists ? (size_t)o.m_cap * o.L * (o.l16 ? 2 : 4) : 0;
-    const size_t smem = (state + ((o.m_cap + 3) & ~3) + 8 * KW * 16 + 32 * KW +
-                         (size_t)o.m_cap * KW) * 4 + ((lists + 15) & ~(size_t)15);
+    return (state + ((o.m_cap + 3) & ~3) + 8 * (size_t)kw * 16 + 32 * (size_t)kw + (size_t)o.m_cap * kw) * 4 +
+           ((lists + 15) & ~(size_t)15);
+}
+
+template <int KW>
+int run_owned_fr(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s) {
+    int per_sm = 0;
+    const size_t smem = owned_fr_smem(o, KW);
     cudaFuncSetAttribute(k_owned_fr<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_owned_fr<KW>, OWN_THREADS, smem);
     if (per_sm < 1) per_sm = 1;
@@ -1108,6 +1116,12 @@ int run_merge(const RowArgs &a, const MergeArgs &g, int sms, cudaStream_t s) {
 }
 
 }  // namespace
+
+// dynamic shared memory the owned-mask kernel launch_owned_masks picks would request
+size_t owned_masks_smem(const OwnArgs &o, int kw) {
+    if (o.fr && (kw == 2 || kw == 4 || kw == 6 || kw == 8)) return owned_fr_smem(o, kw);
+    return owned_smem(o, kw);
+}
 
 int launch_owned_masks(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s) {
     if (o.fr) {

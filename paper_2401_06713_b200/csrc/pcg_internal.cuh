@@ -159,6 +159,7 @@ int launch_commute_fr2_items(const uint32_t *B, const uint32_t *H, int32_t kw, i
 int launch_rows(const RowArgs &a, bool fill, bool out64, int sms, cudaStream_t s);
 int launch_bucket_layout(const BucketArgs &b, int64_t entries, cudaStream_t s);
 int launch_bucket_masks(const BucketArgs &b, int sms, cudaStream_t s);
+size_t owned_masks_smem(const OwnArgs &o, int kw);
 int launch_owned_masks(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s);
 int launch_count_owned(const RowArgs &a, int sms, cudaStream_t s);
 int launch_fill_merge(const RowArgs &a, const MergeArgs &g, bool out64, int sms, cudaStream_t s);

@@ -339,6 +339,26 @@ def test_owned_direct_table_large_palette(n, pct):
         assert np.array_equal(nb[off[i]:off[i + 1]], row)
 
 
+@pytest.mark.parametrize("pct,alpha", [(3.0, 3.03), (0.75, 3.03)])
+def test_owned_masks_shared_memory_fallbacks(pct, alpha):
+    """Big buckets x long lists: the owned-mask kernel's shared memory does not fit with staged
+    lists (P=600, L=30: ~1000 members) or at all (P=150, L=30: ~4000 members); the build
+    drops list staging / ownership instead of failing the launch."""
+    from oracle.oracle import OracleInstance
+
+    n = 20000
+    v = pauli_view(n, 32, 8)
+    lists = random_lists(v, pct=pct, alpha=alpha, seed=4)
+    assert lists.array.shape[1] == 30
+    gc = b200.build(v, lists)
+    inst = OracleInstance(v.backing.words, v.active, lists)
+    assert gc.view_edges_scanned == inst.commute_count()
+    nb, off = gc.graph.neighbors, gc.graph.offsets
+    for i in (0, 7777, n - 1):
+        row, _ = inst.row(i)
+        assert np.array_equal(nb[off[i]:off[i + 1]], row)
+
+
 def test_full_size_config2_properties():
     """BASELINE config 2 (100k x 32q): the oracle cannot build it in test time, so check
     size-independent properties: commuting-pair total against the oracle's popcount sweep,

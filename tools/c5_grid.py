@@ -1,0 +1,49 @@
+"""Config 5 (500k x 64q) palette/list grid on one B200: device build time and |E_c| per cell
+(P' in {1, 2.5, ..., 20}, alpha in {0.5, ..., 4.5}, seed 0).  The densest corner
+(P'=1, alpha=4.5: ~3.2e10 conflict edges, a 253 GB CSR) goes through the public build with an
+edge budget and must raise the reference's EdgeBudgetExceededError before allocating."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import paper_2401_06713_b200 as b200
+from paper_2401_06713_b200 import _native
+from paper_2401_06713_b200.conflict import stage
+from paper_2401_06713_b200.errors import EdgeBudgetExceededError
+
+n, q = 500_000, 64
+t0 = time.time()
+view = b200.pauli_view(b200.PauliSet.from_strings(b200.random_pauli_strings(n, q, seed=0)))
+print(f"inputs {time.time() - t0:.1f} s", flush=True)
+ctx = _native.context()
+pairs = n * (n - 1) // 2
+cells = [(12.5, 2.0), (20.0, 0.5), (1.0, 0.5), (20.0, 4.5), (5.0, 2.0), (2.5, 3.0), (10.0, 1.0)]
+print("| P' % | alpha | P | L | |E_c| | device build | pairs/s |")
+print("|---|---|---|---|---|---|---|")
+for pct, alpha in cells:
+    plan = b200.plan_iteration(1, n, b200.PaletteParams(pct, alpha, seed=0))
+    lists = b200.assign_random_lists(plan, view.active, 0)
+    stage(view, lists, ctx)
+    best = None
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        c, _ = ctx.build_device()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t
+        best = dt if best is None else min(best, dt)
+    print(f"| {pct} | {alpha} | {plan.palette_size} | {plan.list_size} | {c.deg_sum // 2:.3e} | "
+          f"{best * 1e3:.1f} ms | {pairs / best:.2e} |", flush=True)
+# densest corner: budget error from the count pass, nothing allocated for the CSR
+plan = b200.plan_iteration(1, n, b200.PaletteParams(1.0, 4.5, seed=0))
+lists = b200.assign_random_lists(plan, view.active, 0)
+t = time.perf_counter()
+try:
+    b200.build(view, lists, edge_budget=4_000_000_000)
+    print("P'=1 alpha=4.5: no error (unexpected)")
+except EdgeBudgetExceededError as e:
+    print(f"P'=1 alpha=4.5 (P={plan.palette_size}, L={plan.list_size}): EdgeBudgetExceededError "
+          f"projected={e.projected:.3e} budget={e.budget} after {time.perf_counter() - t:.2f} s")
