@@ -359,6 +359,31 @@ def test_owned_masks_shared_memory_fallbacks(pct, alpha):
         assert np.array_equal(nb[off[i]:off[i + 1]], row)
 
 
+@pytest.mark.parametrize("n,pct,alpha", [(6000, 3.0, 30.0), (20000, 3.0, 30.0)])
+def test_aggressive_lists(n, pct, alpha):
+    """SURVEY's aggressive corner (alpha = 30): lists of hundreds of colors (no ownership, no
+    segmented fill) and, at n = 6000, lists equal to the whole palette (L = P = 180)."""
+    from oracle.oracle import OracleInstance
+
+    v = pauli_view(n, 32, 9)
+    lists = random_lists(v, pct=pct, alpha=alpha, seed=6)
+    L = lists.array.shape[1]
+    assert L > 64
+    gc = b200.build(v, lists)
+    if n <= 6000:
+        assert L == lists.palette_size
+        want = oracle_builder(v, lists)
+        assert np.array_equal(gc.graph.offsets, want.graph.offsets)
+        assert np.array_equal(gc.graph.neighbors, want.graph.neighbors)
+        return
+    inst = OracleInstance(v.backing.words, v.active, lists)
+    assert gc.view_edges_scanned == inst.commute_count()
+    nb, off = gc.graph.neighbors, gc.graph.offsets
+    for i in (0, n // 2, n - 1):
+        row, _ = inst.row(i)
+        assert np.array_equal(nb[off[i]:off[i + 1]], row)
+
+
 def test_full_size_config2_properties():
     """BASELINE config 2 (100k x 32q): the oracle cannot build it in test time, so check
     size-independent properties: commuting-pair total against the oracle's popcount sweep,
