@@ -151,6 +151,13 @@ int pcg_assign_lists(pcg_ctx *ctx, const int64_t *active, int64_t n, uint64_t ba
 int pcg_color_dynamic(int64_t nm, const int64_t *offsets, const int64_t *neighbors,
                       const int64_t *list_data, const int64_t *list_off, uint64_t *rng6,
                       int64_t *color_of, int64_t *removal_ops);
+/* Same coloring (same draws, same result) with each step's neighbor scan split across
+ * `threads` host threads (0: up to 16) for rows of at least `par_min_deg` entries (-1: 512);
+ * the hits are applied in row order by the calling thread.  pcg_color_dynamic = (0, -1). */
+int pcg_color_dynamic_mt(int64_t nm, const int64_t *offsets, const int64_t *neighbors,
+                         const int64_t *list_data, const int64_t *list_off, uint64_t *rng6,
+                         int64_t *color_of, int64_t *removal_ops, int32_t threads,
+                         int64_t par_min_deg);
 
 /*
  * Exhaustive properness check of a coloring (validation.py:41-131, exhaustive mode; the

@@ -154,6 +154,35 @@ def test_native_list_coloring_matches_python(seed):
         assert r1.integers(1 << 30) == r2.integers(1 << 30)
 
 
+@pytest.mark.parametrize("threads,par_min", [(4, 1), (3, 16), (16, 64)])
+def test_native_list_coloring_threaded_scan(threads, par_min):
+    """The threaded neighbor scan (pcg_color_dynamic_mt) gives the sequential scan's coloring,
+    removal count and generator state, on graphs whose rows are far above the threshold, and
+    the sequential scan matches the Python restatement."""
+    from paper_2401_06713_b200 import list_coloring as lc
+
+    for n, q, pct, alpha, seed in ((3000, 16, 12.5, 2.0, 0), (2500, 12, 4.0, 3.0, 9)):
+        v = pauli_view(n, q, seed + 31)
+        plan = b200.plan_iteration(1, n, b200.PaletteParams(pct, alpha, seed))
+        lists = b200.assign_random_lists(plan, v.active, seed)
+        gc = oracle_builder(v, lists)
+        assert np.diff(gc.graph.offsets).max() > 4 * par_min
+        out = []
+        try:
+            for thr, pm in ((1, -1), (threads, par_min)):
+                lc.NATIVE_THREADS, lc.NATIVE_PAR_MIN_DEG = thr, pm
+                r = np.random.default_rng(np.random.SeedSequence([seed, 1, 0xC01]))
+                o = lc.color_dynamic(gc, lists, r)
+                out.append((o.colored, list(o.uncolored), o.removal_ops, r.bit_generator.state))
+        finally:
+            lc.NATIVE_THREADS, lc.NATIVE_PAR_MIN_DEG = 0, -1
+        assert out[0] == out[1]
+        if n <= 2500:
+            r = np.random.default_rng(np.random.SeedSequence([seed, 1, 0xC01]))
+            p = lc.color_dynamic_py(gc, lists, r)
+            assert p.colored == out[0][0] and p.removal_ops == out[0][2]
+
+
 def test_native_list_coloring_ragged_lists(golden_cases):
     from paper_2401_06713_b200 import list_coloring as lc
 
