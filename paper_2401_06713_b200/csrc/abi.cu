@@ -1183,11 +1183,12 @@ static int d2h_delta(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, int64_t
             if (e == cudaSuccess) e = cudaEventRecord(ctx->ring_ev[2 * w + slot], st);
             return e;
         };
+        const size_t Wt = (size_t)omp_get_num_threads();  // the team may be smaller than W
         int slot = 0;
         if ((size_t)w < nch && issue(w, 0) != cudaSuccess) failed = 1;
         if (cudaEventSynchronize(ready) != cudaSuccess) failed = 1;  // exceptions on the host
-        for (size_t k = w; k < nch && !failed; k += W, slot ^= 1) {
-            if (k + W < nch && issue(k + W, slot ^ 1) != cudaSuccess) failed = 1;
+        for (size_t k = w; k < nch && !failed; k += Wt, slot ^= 1) {
+            if (k + Wt < nch && issue(k + Wt, slot ^ 1) != cudaSuccess) failed = 1;
             if (cudaEventSynchronize(ctx->ring_ev[2 * w + slot]) != cudaSuccess) {
                 failed = 1;
                 break;
@@ -1371,21 +1372,26 @@ static int fill_delta_pipe(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, i
         return PCG_OK;
     };
 
-#pragma omp parallel num_threads(W + 1)
+    // orchestrator: pieces in order on the build stream (its own thread, so it exists whatever
+    // team size OpenMP grants the decoders)
+    std::thread orch([&] {
+        cudaSetDevice(ctx->device);
+        for (int64_t p = 0; p < K && !failed.load(); ++p) {
+            const int rc = run_piece(p);
+            if (rc) {
+                orc = rc;
+                failed.store(1);
+            }
+            ready.store(p + 1, std::memory_order_release);
+        }
+        ready.store(K, std::memory_order_release);
+    });
+#pragma omp parallel num_threads(W)
     {
         const int w = omp_get_thread_num();
+        const int Wt = omp_get_num_threads();  // the team may be smaller than W
         cudaSetDevice(ctx->device);
-        if (w == W) {  // orchestrator: pieces in order on the build stream
-            for (int64_t p = 0; p < K && !failed.load(); ++p) {
-                const int rc = run_piece(p);
-                if (rc) {
-                    orc = rc;
-                    failed.store(1);
-                }
-                ready.store(p + 1, std::memory_order_release);
-            }
-            ready.store(K, std::memory_order_release);
-        } else {  // decoder w: chunks w, w+W, ... double-buffered on its own stream
+        {  // decoder w: chunks w, w+Wt, ... double-buffered on its own stream
             cudaStream_t st = ctx->ring_st[w];
             auto piece_ready = [&](int64_t k) { return ready.load(std::memory_order_acquire) > k / cpp; };
             auto issue = [&](int64_t k, int slot) -> cudaError_t {
@@ -1397,9 +1403,9 @@ static int fill_delta_pipe(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, i
                 if (e == cudaSuccess) e = cudaEventRecord(ctx->ring_ev[2 * w + slot], st);
                 return e;
             };
-            int64_t issued = w - W;  // last of the decoders' chunks (index into todo) queued
+            int64_t issued = w - Wt;  // last of the decoders' chunks (index into todo) queued
             int slot = 0;
-            for (int64_t j = w; j < ntodo && !failed.load(); j += W, slot ^= 1) {
+            for (int64_t j = w; j < ntodo && !failed.load(); j += Wt, slot ^= 1) {
                 const int64_t k = todo[j];
                 if (issued < j) {  // not prefetched: wait for its piece, then copy it
                     while (!piece_ready(k) && !failed.load())  // sleep: leave the core to the
@@ -1411,12 +1417,12 @@ static int fill_delta_pipe(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, i
                     issued = j;
                 }
                 // prefetch the next chunk only if its piece is already out (never wait here)
-                if (j + W < ntodo && piece_ready(todo[j + W])) {
-                    if (issue(todo[j + W], slot ^ 1) != cudaSuccess) {
+                if (j + Wt < ntodo && piece_ready(todo[j + Wt])) {
+                    if (issue(todo[j + Wt], slot ^ 1) != cudaSuccess) {
                         failed.store(1);
                         break;
                     }
-                    issued = j + W;
+                    issued = j + Wt;
                 }
                 const int64_t p = k / cpp;
                 // the piece's exceptions and offsets are on the host once its event completed
@@ -1435,6 +1441,7 @@ static int fill_delta_pipe(pcg_ctx *ctx, int64_t *dst, const int64_t *offsets, i
             cudaStreamSynchronize(st);
         }
     }
+    orch.join();
     if (dma_entries > 0 && cudaStreamSynchronize(ctx->dma_st) != cudaSuccess) failed.store(1);
     if (orc) return orc;
     if (failed.load()) return fail(ctx, PCG_E_CUDA, "pipelined fill / delta copy-out failed");
@@ -1524,10 +1531,11 @@ static int d2h_widen(pcg_ctx *ctx, int64_t *dst, const int32_t *src, size_t coun
             if (e == cudaSuccess) e = cudaEventRecord(ctx->ring_ev[2 * w + slot], st);
             return e;
         };
+        const size_t Wt = (size_t)omp_get_num_threads();  // the team may be smaller than W
         int slot = 0;
         if ((size_t)w < nch && issue(w, 0) != cudaSuccess) failed = 1;
-        for (size_t k = w; k < nch && !failed; k += W, slot ^= 1) {
-            if (k + W < nch && issue(k + W, slot ^ 1) != cudaSuccess) failed = 1;
+        for (size_t k = w; k < nch && !failed; k += Wt, slot ^= 1) {
+            if (k + Wt < nch && issue(k + Wt, slot ^ 1) != cudaSuccess) failed = 1;
             if (cudaEventSynchronize(ctx->ring_ev[2 * w + slot]) != cudaSuccess) {
                 failed = 1;
                 break;

@@ -465,6 +465,30 @@ def test_pinned_direct_copy_matches(golden_ref):
         gc = None
 
 
+@pytest.mark.parametrize("limit", ["2", "1"])
+def test_copy_out_with_a_small_openmp_team(golden_ref, limit):
+    """The copy-out's decoders stride by the team OpenMP actually grants (OMP_THREAD_LIMIT
+    below the requested 15-16 threads) and the pipeline's orchestrator is its own thread."""
+    import os
+    import subprocess
+    import sys
+
+    g = golden_ref["builds_hashed"]["q32_n20000"]
+    code = (
+        "import sys, hashlib, numpy as np; sys.path.insert(0, 'tests'); "
+        "import paper_2401_06713_b200 as b200; from conftest import pauli_view, random_lists; "
+        "v = pauli_view(20000, 32, 0); gc = b200.build(v, random_lists(v, seed=0)); "
+        "h = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]; "
+        "print(h(gc.graph.offsets), h(gc.graph.neighbors))"
+    )
+    env = dict(os.environ, OMP_THREAD_LIMIT=limit)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                         text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.split()[-2:] == [g["offsets_sha"], g["neighbors_sha"]]
+
+
 @pytest.mark.parametrize("n,pct,alpha", [(3000, 12.5, 2.0), (40000, 40.0, 0.6), (70000, 25.0, 1.0)])
 def test_delta_copy_out_matches_widened_copy(n, pct, alpha):
     """The public build ships CSR gaps as bytes (escapes to an exception list for gaps >= 255
