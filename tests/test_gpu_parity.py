@@ -465,6 +465,39 @@ def test_pinned_direct_copy_matches(golden_ref):
         gc = None
 
 
+def test_concurrent_builds_from_threads(golden_ref):
+    """tuner.sweep(cell_workers>1) calls run() from several Python threads (tuner.py:138-141):
+    each thread gets its own context and stream, the GIL is released during the native calls,
+    and the pooled host buffers are never shared between live graphs."""
+    import threading
+
+    names = ["q32_n5000", "q32_n10000", "q32_n20000"]
+    inputs = {}
+    for nm in names:
+        n = int(nm.split("_n")[1])
+        v = pauli_view(n, 32, 0)
+        inputs[nm] = (v, random_lists(v, seed=0))
+    got, errors = {}, []
+
+    def work(nm):
+        try:
+            for _ in range(2):
+                gc = b200.build(*inputs[nm])
+                got.setdefault(nm, []).append((sha(gc.graph.offsets), sha(gc.graph.neighbors)))
+        except Exception as e:  # noqa: BLE001  (reported below)
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=work, args=(nm,)) for nm in names]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    for nm in names:
+        g = golden_ref["builds_hashed"][nm]
+        assert got[nm] == [(g["offsets_sha"], g["neighbors_sha"])] * 2
+
+
 @pytest.mark.parametrize("limit", ["2", "1"])
 def test_copy_out_with_a_small_openmp_team(golden_ref, limit):
     """The copy-out's decoders stride by the team OpenMP actually grants (OMP_THREAD_LIMIT
