@@ -301,7 +301,7 @@ def bench_gpu(args) -> None:
     fill_bytes = (2 * edges) * 4 + (members + 1) * 8 + members * 8 + n * plan.list_size * 4 + words_b
     achieved = fill_bytes / (fill_ms * 1e-3) / 1e9
     # the fill kernel the native layer picks for this size (abi.cu fill_rows_device)
-    fill_kernel = "k_fill_blk" if n <= 131072 else "k_fill_seg"
+    fill_kernel = "k_fill_blk" if n <= 131072 else "k_fill_bins"
     # the commuting-pair sweep against the survey's POPC-issue bound (1 POPC / pair / clk)
     sm_mhz = (clocks.summary().get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0))
     popc_bound = 148 * 16 * sm_mhz * 1e6

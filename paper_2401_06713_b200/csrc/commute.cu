@@ -437,8 +437,7 @@ int run_fr2(const uint32_t *B, const uint32_t *H, int64_t n, const int64_t *item
             int64_t njb, int32_t ichunk, int64_t item0, int64_t item1,
             unsigned long long *anti, int sms, cudaStream_t s) {
     const size_t smem = fr2_smem<KW>();
-    cudaFuncSetAttribute(k_commute_fr2<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    allow_max_smem(k_commute_fr2<KW>);
     const int grid = occupancy_grid(k_commute_fr2<KW>, FR_WARPS * 32, smem, sms, item1 - item0);
     k_commute_fr2<KW><<<grid, FR_WARPS * 32, smem, s>>>(B, H, n, item_start, njb, ichunk, item0,
                                                        item1, anti);
@@ -450,8 +449,7 @@ int run_fr(const uint32_t *B, const uint32_t *H, int64_t n, const int64_t *item_
            int64_t njb, int32_t ichunk, int64_t item0, int64_t item1,
            unsigned long long *anti, int sms, cudaStream_t s) {
     const size_t smem = fr_smem<KW>();
-    cudaFuncSetAttribute(k_commute_fr<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    allow_max_smem(k_commute_fr<KW>);
     const int grid = occupancy_grid(k_commute_fr<KW>, FR_WARPS * 32, smem, sms, item1 - item0);
     k_commute_fr<KW><<<grid, FR_WARPS * 32, smem, s>>>(B, H, n, item_start, njb, ichunk, item0,
                                                       item1, anti);

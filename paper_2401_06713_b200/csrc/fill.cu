@@ -295,7 +295,7 @@ int run_seg(const RowArgs &a, const SegArgs &g, int sms, cudaStream_t s) {
     const int warps = std::max(1, std::min(SEG_MAX_WARPS, g.warps));
     const size_t smem = (size_t)g.warp_words * 4 * warps;
     auto kern = k_fill_seg<OutT, MULTI, COMPACT>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_max_smem(kern);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem);
     if (per_sm < 1) per_sm = 1;

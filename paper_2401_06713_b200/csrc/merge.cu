@@ -795,7 +795,7 @@ template <typename OutT>
 int run_coop(const RowArgs &a, int sms, cudaStream_t s) {
     const size_t per_warp = (size_t)((a.window >> 5) + COOP_STAGE + 4 * a.slot_cap) * 4;
     const size_t smem = per_warp * COOP_WARPS;
-    cudaFuncSetAttribute(k_fill_coop<OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_max_smem(k_fill_coop<OutT>);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fill_coop<OutT>, COOP_WARPS * 32, smem);
     if (per_sm < 1) per_sm = 1;
@@ -1054,7 +1054,7 @@ template <typename OutT>
 int run_fill_runs(const RowArgs &a, const RunArgs &r, int sms, cudaStream_t s) {
     const size_t per_warp = ((size_t)2 * r.cap + (a.window >> 5) + 32 + COOP_STAGE + 4) * 4;
     const size_t smem = per_warp * FR_W;
-    cudaFuncSetAttribute(k_fill_runs<OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_max_smem(k_fill_runs<OutT>);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fill_runs<OutT>, FR_W * 32, smem);
     if (per_sm < 1) per_sm = 1;
@@ -1073,7 +1073,7 @@ template <int KW>
 int run_owned(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s) {
     int per_sm = 0;
     const size_t smem = owned_smem(o, b.kw);
-    cudaFuncSetAttribute(k_owned_masks<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_max_smem(k_owned_masks<KW>);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_owned_masks<KW>, OWN_THREADS, smem);
     if (per_sm < 1) per_sm = 1;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * sms * 4, b.P));
@@ -1093,7 +1093,7 @@ template <int KW>
 int run_owned_fr(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s) {
     int per_sm = 0;
     const size_t smem = owned_fr_smem(o, KW);
-    cudaFuncSetAttribute(k_owned_fr<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_max_smem(k_owned_fr<KW>);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_owned_fr<KW>, OWN_THREADS, smem);
     if (per_sm < 1) per_sm = 1;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * sms * 4, b.P));
@@ -1104,7 +1104,7 @@ int run_owned_fr(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s)
 template <typename OutT>
 int run_merge(const RowArgs &a, const MergeArgs &g, int sms, cudaStream_t s) {
     const size_t smem = (size_t)MERGE_WARPS * (2 * g.cap + 68) * 4;
-    cudaFuncSetAttribute(k_fill_merge<OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_max_smem(k_fill_merge<OutT>);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fill_merge<OutT>, MERGE_WARPS * 32, smem);
     if (per_sm < 1) per_sm = 1;

@@ -12,6 +12,30 @@
 
 namespace pcg {
 
+// Every launcher raises a kernel's dynamic shared memory cap to the most the kernel can take
+// (the device's opt-in maximum minus the kernel's static shared memory: the same value from
+// every thread), never to the size of its own launch: a per-launch cap races between host
+// threads launching the same kernel with different sizes (one thread's smaller cap lands just
+// before the other's launch: invalid argument).  The cap is not an allocation; occupancy
+// follows each launch's actual request.
+template <typename F>
+inline void allow_max_smem(F kern) {
+    static const int optin = [] {
+        int d = 0, v = 0;
+        cudaGetDevice(&d);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, d);
+        return v;
+    }();
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             optin - (int)fa.sharedSizeBytes) != cudaSuccess)
+        cudaGetLastError();  // the launch itself reports a request above the cap
+}
+
 // ---------------------------------------------------------------------------
 // Device memory: grow-only buffers owned by one context.
 // ---------------------------------------------------------------------------
@@ -109,6 +133,15 @@ struct BlkArgs {
     const int32_t *bnd;    // (P, nwin+1) members of each bucket below each window start
 };
 
+struct BinArgs {
+    int32_t threads;       // threads per CTA (one row per CTA)
+    int32_t shift;         // bins of 2^shift ids
+    int32_t nbins;
+    int32_t ecap;          // admitted ids per row held in shared memory (>= longest row)
+    int32_t dcap;          // descriptor slots (multiple of 8)
+    int32_t lcap;          // color slots (>= longest list)
+};
+
 struct MergeArgs {
     int32_t cap;           // ids per warp buffer; longer rows go to the bitmap fill
     int32_t *heavy;        // out: rows longer than cap
@@ -172,6 +205,9 @@ int launch_fill_coop(const RowArgs &a, bool out64, int sms, cudaStream_t s);
 void seg_geometry(int64_t n, int64_t max_bits, int32_t *wb, int32_t *nwin, int32_t *seg);
 int launch_window_bounds(const int32_t *bstart, const int32_t *bpos, const int32_t *bmemp,
                          int64_t P, int nwin, int32_t wb, int32_t *bnd, cudaStream_t s);
+size_t bins_smem_bytes(const BinArgs &g);
+void bins_geometry(int64_t n, double mean_deg, int threads, BinArgs *g);
+int launch_fill_bins(const RowArgs &a, const BinArgs &g, bool out64, int sms, cudaStream_t s);
 size_t blk_smem_bytes(const BlkArgs &g, int groups);
 void blk_geometry(int64_t n, int threads, int groups, BlkArgs *g);
 int launch_fill_blk(const RowArgs &a, const BlkArgs &g, bool out64, int sms, cudaStream_t s);
@@ -212,8 +248,9 @@ struct pcg_ctx {
     int window = 0;     // K2 window bits (0 auto)
     int fr_ichunk = 0;  // four-Russians i-chunk (0 auto)
     int merge_cap = 0;  // fill-merge buffer cap (0 auto; testing knob)
-    int fill_algo = 0;  // owned masks: 0 auto (block fill up to 128K ids, else segmented),
-                        // 5 block fill (CTA per row), 6 segmented fill (warp-decoded words,
+    int fill_algo = 0;  // owned masks: 0 auto (block fill up to 128K ids, else the bins fill
+                        // when the longest row fits its list, else segmented), 7 bins fill
+                        // (counting sort per row), 5 block fill (CTA per row), 6 segmented fill (warp-decoded words,
                         // lane-segment harvest), 3 lane-per-bucket bitmap fill,
                         // 1 cooperative bitmap, 2 merge, 4 TMA-staged owned runs
     int seg_bits = 0;   // segmented fill: max window bits per warp (0 auto)
@@ -272,6 +309,8 @@ struct pcg_ctx {
     cudaEvent_t scan_ev = nullptr;
     std::vector<std::pair<int32_t *, size_t>> hxpiece;  // pinned exceptions per piece
     int blk_threads = 0, blk_groups = 0, blk_dcap = 0, blk_ecap = 0;  // block fill geometry (0 = auto)
+    int bins_threads = 0;  // bins fill: threads per CTA (0 = auto)
+    int bins_shift = 0;    // bins fill: bin width exponent delta from auto (testing/tuning)
     int k1_async = 0;                          // K1 on a side stream, result collected later
     bool k1_pending = false;
     cudaStream_t k1_stream = nullptr;

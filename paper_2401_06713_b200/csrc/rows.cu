@@ -498,7 +498,7 @@ size_t masked_warp_bytes(const RowArgs &a) {
 template <typename Kern>
 int launch_row_kernel(Kern k, const RowArgs &a, size_t per_warp, int sms, cudaStream_t s) {
     const size_t smem = per_warp * RW_WARPS;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_max_smem(k);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, RW_WARPS * 32, smem);
     if (per_sm < 1) per_sm = 1;

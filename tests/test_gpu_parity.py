@@ -79,8 +79,9 @@ def test_merge_heavy_rows_fallback(golden_cases, cap):
         ctx.option("k2_mode", 0)
 
 
-@pytest.mark.parametrize("fill_algo", [0, 1, 2, 3, 4, 5, 6],
-                         ids=["auto", "coop", "merge", "lane-bitmap", "runs-tma", "block", "segmented"])
+@pytest.mark.parametrize("fill_algo", [0, 1, 2, 3, 4, 5, 6, 7],
+                         ids=["auto", "coop", "merge", "lane-bitmap", "runs-tma", "block", "segmented",
+                              "bins"])
 def test_owned_fill_variants(golden_cases, fill_algo):
     ctx = _native.context()
     ctx.option("k2_mode", 3)
@@ -158,6 +159,28 @@ def test_block_fill_geometry(golden_cases, golden_ref, threads, groups, dcap, ec
                 g["offsets_sha"], g["neighbors_sha"])
     finally:
         for k in ("fill_algo", "blk_threads", "blk_groups", "blk_dcap", "blk_ecap"):
+            ctx.option(k, 0)
+
+
+@pytest.mark.parametrize("threads,dcap", [(32, 0), (128, 8), (256, 0), (1024, 24)])
+def test_bins_fill_geometry(golden_cases, golden_ref, threads, dcap):
+    """Bins fill (counting sort per row): CTA size and descriptor chunking must not change a
+    single entry."""
+    ctx = _native.context()
+    ctx.option("fill_algo", 7)
+    ctx.option("bins_threads", threads)
+    ctx.option("blk_dcap", dcap)
+    try:
+        for case in golden_cases:
+            case.check(b200.build(case.view, case.lists))
+        for n in (10000, 20000):
+            g = golden_ref["builds_hashed"][f"q32_n{n}"]
+            v = pauli_view(n, 32, 0)
+            gc = b200.build(v, random_lists(v, seed=0))
+            assert (sha(gc.graph.offsets), sha(gc.graph.neighbors)) == (
+                g["offsets_sha"], g["neighbors_sha"])
+    finally:
+        for k in ("fill_algo", "bins_threads", "blk_dcap"):
             ctx.option(k, 0)
 
 

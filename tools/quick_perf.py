@@ -28,6 +28,8 @@ ap.add_argument("--own-direct", type=int, default=1)
 ap.add_argument("--blk-threads", type=int, default=0)
 ap.add_argument("--blk-groups", type=int, default=0)
 ap.add_argument("--blk-ecap", type=int, default=0)
+ap.add_argument("--bins-threads", type=int, default=0)
+ap.add_argument("--bins-shift", type=int, default=0)
 ap.add_argument("--check", action="store_true", help="compare the CSR with fill_algo 3")
 a = ap.parse_args()
 
@@ -49,6 +51,8 @@ ctx.option("own_direct", a.own_direct)
 ctx.option("blk_threads", a.blk_threads)
 ctx.option("blk_groups", a.blk_groups)
 ctx.option("blk_ecap", a.blk_ecap)
+ctx.option("bins_threads", a.bins_threads)
+ctx.option("bins_shift", a.bins_shift)
 ctx.profiling(True)
 stage(v, lists, ctx)
 print("prep ms", ctx.kernel_times()[4])
