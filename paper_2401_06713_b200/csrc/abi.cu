@@ -14,6 +14,7 @@
 #include <chrono>
 #include <thread>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <vector>
 
@@ -178,6 +179,7 @@ int pcg_destroy(pcg_ctx *ctx) {
     release(ctx->dxoff);
     release(ctx->dxval);
     release(ctx->mrow);
+    if (ctx->hs) cudaFreeHost(ctx->hs);
     release(ctx->dwide);
     if (ctx->dma_st) cudaStreamDestroy(ctx->dma_st);
     for (auto &e : ctx->piece_ev) cudaEventDestroy(e);
@@ -307,6 +309,16 @@ static void k1_join(pcg_ctx *ctx) {
     if (ctx->k1_pending && ctx->k1_done) cudaStreamWaitEvent(ctx->stream, ctx->k1_done, 0);
 }
 
+// Small device -> host readbacks (sizes, flags, totals) land in pinned scratch: a copy into
+// pageable stack memory is a staged, much slower transfer on the critical path of each build.
+static unsigned char *pinned_scratch(pcg_ctx *ctx) {
+    if (!ctx->hs && cudaHostAlloc(reinterpret_cast<void **>(&ctx->hs), 512, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        ctx->hs = nullptr;
+    }
+    return ctx->hs;
+}
+
 static BucketArgs bucket_args(const pcg_ctx *ctx) {
     BucketArgs b{};
     b.P = ctx->P;
@@ -325,6 +337,39 @@ static BucketArgs bucket_args(const pcg_ctx *ctx) {
     return b;
 }
 
+// PCG_TRACE_PREP=1: device timestamps between the prep stages, printed to stderr (diagnostic)
+struct PrepTrace {
+    bool on = false;
+    cudaEvent_t ev[12] = {};
+    double host[12] = {};
+    const char *name[12] = {};
+    int k = 0;
+    explicit PrepTrace(cudaStream_t s) : st(s) {
+        const char *e = getenv("PCG_TRACE_PREP");
+        on = e && e[0] == '1';
+    }
+    void mark(const char *what) {
+        if (!on || k >= 12) return;
+        if (!ev[k]) cudaEventCreate(&ev[k]);
+        cudaEventRecord(ev[k], st);
+        host[k] = std::chrono::duration<double, std::micro>(
+                      std::chrono::steady_clock::now().time_since_epoch()).count();
+        name[k++] = what;
+    }
+    ~PrepTrace() {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        for (int i = 1; i < k; ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+            fprintf(stderr, "prep %-22s device %8.1f us   host %8.1f us\n", name[i], ms * 1e3,
+                    host[i] - host[i - 1]);
+        }
+        for (int i = 0; i < k; ++i) cudaEventDestroy(ev[i]);
+    }
+    cudaStream_t st;
+};
+
 // K0 on the device-resident raw inputs: vectors, relative lists, color buckets, bucket
 // commute masks (K2a), four-Russians offsets.  Everything a build computes besides the count
 // and fill passes; the benchmark times it as part of every step.
@@ -334,6 +379,8 @@ static int prep_device(pcg_ctx *ctx) {
     const int64_t n_active = ctx->n, entries = ctx->entries, P = ctx->P;
     if (n_active == 0) return PCG_OK;
     if (ctx->prof) cudaEventRecord(ctx->ev[10], s);
+    PrepTrace tr(s);
+    tr.mark("start");
     int rc = encode_vectors(ctx, false);
     if (rc) return rc;
     PCG_ALLOC(ctx, ctx->lrel, (size_t)entries * 4);
@@ -345,6 +392,7 @@ static int prep_device(pcg_ctx *ctx) {
     // (the invalid-code / invalid-color flags are read back with the bucket sizes below:
     // invalid colors are clamped to 0 until then, and the bit planes are not consumed before)
 
+    tr.mark("encode+lists");
     // color buckets: stable radix sort of (color, entry) in row-major entry order, so each
     // bucket lists its rows ascending
     int end_bit = 1;
@@ -363,6 +411,7 @@ static int prep_device(pcg_ctx *ctx) {
                           ctx->cubtmp.p, tmp, ctx->lrel.as<int32_t>(), ctx->keys2.as<int32_t>(),
                           ctx->eidx.as<int32_t>(), ctx->vals2.as<int32_t>(), (int)entries, 0,
                           end_bit, s));
+    tr.mark("radix sort");
     PCG_ALLOC(ctx, ctx->bstart, (size_t)(P + 1) * 4);
     launch_bucket_bounds(ctx->keys2.as<int32_t>(), entries, P, ctx->bstart.as<int32_t>(), s);
     PCG_CHECK_LAUNCH(ctx);
@@ -391,14 +440,19 @@ static int prep_device(pcg_ctx *ctx) {
     int32_t padded_total = 0, m_max = 0;
     int64_t mask_total = 0;
     int32_t bad[2] = {0, 0};
-    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(bad, ctx->bad.p, 8, cudaMemcpyDeviceToHost, s));
-    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&m_max, ctx->bad.as<int32_t>() + 2, 4,
-                                      cudaMemcpyDeviceToHost, s));
-    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&padded_total, ctx->bpos.as<int32_t>() + P, 4,
-                                      cudaMemcpyDeviceToHost, s));
-    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&mask_total, ctx->maskoff.as<int64_t>() + P, 8,
-                                      cudaMemcpyDeviceToHost, s));
+    unsigned char *hs = pinned_scratch(ctx);
+    if (!hs) return fail(ctx, PCG_E_OOM, "pinned scratch allocation failed");
+    // one pinned block: bad flags (8 B) | m_max (4) | padded total (4) | mask words (8)
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(hs, ctx->bad.p, 12, cudaMemcpyDeviceToHost, s));
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(hs + 12, ctx->bpos.as<int32_t>() + P, 4, cudaMemcpyDeviceToHost, s));
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(hs + 16, ctx->maskoff.as<int64_t>() + P, 8, cudaMemcpyDeviceToHost, s));
+    tr.mark("bounds+scans+readback");
     PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+    tr.mark("host sync");
+    memcpy(bad, hs, 8);
+    memcpy(&m_max, hs + 8, 4);
+    memcpy(&padded_total, hs + 12, 4);
+    memcpy(&mask_total, hs + 16, 8);
     if (bad[1]) return fail(ctx, PCG_E_COLOR, "a list color lies outside the palette");
     if (bad[0]) {  // invalid 3-bit codes: exact raw-word predicate
         rc = encode_vectors(ctx, true);
@@ -428,6 +482,7 @@ static int prep_device(pcg_ctx *ctx) {
     BucketArgs b = bucket_args(ctx);
     launch_bucket_layout(b, entries, s);
     PCG_CHECK_LAUNCH(ctx);
+    tr.mark("memset+layout");
     if (ctx->masked) {
         PCG_ALLOC(ctx, ctx->masks, std::max<size_t>(mask_bytes, 16));
         b.masks = ctx->masks.as<uint32_t>();
@@ -522,6 +577,7 @@ static int prep_device(pcg_ctx *ctx) {
         }
     }
 
+    tr.mark("masks (K2a)");
     // four-Russians row offsets
     if (fr_supported(ctx->kw)) {
         PCG_ALLOC(ctx, ctx->H, (size_t)ctx->npad * ctx->kw * 4 * 4);
@@ -530,6 +586,7 @@ static int prep_device(pcg_ctx *ctx) {
         else launch_fr_prep(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
         PCG_CHECK_LAUNCH(ctx);
     }
+    tr.mark("fr prep");
     PCG_ALLOC(ctx, ctx->deg, (size_t)n_active * 4);
     PCG_ALLOC(ctx, ctx->degu, (size_t)n_active * 4);
     ctx->prep_launches = 6 + (bad[0] ? 1 : 0) + (ctx->masked ? 1 : 0) + (fr_supported(ctx->kw) ? 1 : 0);
@@ -807,11 +864,15 @@ static int count_impl(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t r0, 
     }
     unsigned long long h[5];
     int32_t ovf = 0;
-    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(h, ctx->scal.p, 40, cudaMemcpyDeviceToHost, s));
+    unsigned char *hs = pinned_scratch(ctx);
+    if (!hs) return fail(ctx, PCG_E_OOM, "pinned scratch allocation failed");
+    PCG_TRY_CUDA(ctx, cudaMemcpyAsync(hs + 64, ctx->scal.p, 40, cudaMemcpyDeviceToHost, s));
     if (ctx->own_check)
-        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&ovf, ctx->bad.as<int32_t>() + 3, 4,
+        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(hs + 104, ctx->bad.as<int32_t>() + 3, 4,
                                           cudaMemcpyDeviceToHost, s));
     PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
+    memcpy(h, hs + 64, 40);
+    if (ctx->own_check) memcpy(&ovf, hs + 104, 4);
     if (ctx->prof) {
         if (ctx->prep_timed) cudaEventElapsedTime(&ctx->ktimes[4], ctx->ev[10], ctx->ev[11]);
         ctx->prep_timed = false;
@@ -1805,8 +1866,11 @@ extern "C" int pcg_k1_result(pcg_ctx *ctx, int64_t *anticommuting) {
     if (ctx->k1_pending) {
         PCG_TRY_CUDA(ctx, cudaSetDevice(ctx->device));
         unsigned long long a = 0;
-        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&a, ctx->scal.p, 8, cudaMemcpyDeviceToHost, ctx->k1_stream));
+        unsigned char *hs = pinned_scratch(ctx);
+        if (!hs) return fail(ctx, PCG_E_OOM, "pinned scratch allocation failed");
+        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(hs + 128, ctx->scal.p, 8, cudaMemcpyDeviceToHost, ctx->k1_stream));
         PCG_TRY_CUDA(ctx, cudaStreamSynchronize(ctx->k1_stream));
+        memcpy(&a, hs + 128, 8);
         if (ctx->prof) cudaEventElapsedTime(&ctx->ktimes[0], ctx->ev[0], ctx->ev[1]);
         ctx->last.anticommuting = (int64_t)a;
         ctx->k1_pending = false;
