@@ -1696,12 +1696,11 @@ static int fill_rows_device(pcg_ctx *ctx, int64_t r0, int64_t r1, const int32_t 
         if (ctx->blk_dcap > 0) g.dcap = (ctx->blk_dcap + 7) & ~7;  // testing: chunked descriptors
         // admitted-id list: sized for a window of the longest row (+ slack for uneven windows);
         // a window that overflows it re-decodes its descriptors instead
-        // per warp: its share + 25% + one batch of 8 descriptors (256 ids) of slack
+        // the row's list holds a window of the longest row (+25% when windows split rows
+        // unevenly); a window that overflows it re-decodes its descriptors instead
         const int64_t per_win = (int64_t)maxdeg / g.nwin + (g.nwin > 1 ? maxdeg / (4 * g.nwin) : 0);
-        const int nwarps = g.threads / 32;
-        const int64_t capw = std::min<int64_t>(16384 / nwarps, ((per_win * 5 / 4) / nwarps + 256 + 7) & ~7);
-        g.ecap = (int32_t)(capw * nwarps);
-        if (ctx->blk_ecap != 0) g.ecap = ctx->blk_ecap < 0 ? 0 : (ctx->blk_ecap + 8 * nwarps - 1) / (8 * nwarps) * (8 * nwarps);
+        g.ecap = (int32_t)std::min<int64_t>(16384, (per_win + 31) & ~31);
+        if (ctx->blk_ecap != 0) g.ecap = ctx->blk_ecap < 0 ? 0 : (ctx->blk_ecap + 7) & ~7;
         if (blk_smem_bytes(g, g.groups) <= 227u * 1024u) {
             if (g.nwin > 1) {
                 PCG_ALLOC(ctx, ctx->bnd, (size_t)ctx->P * (g.nwin + 1) * 4);

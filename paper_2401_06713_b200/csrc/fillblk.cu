@@ -114,8 +114,10 @@ __device__ __forceinline__ uint32_t blk_swz(uint32_t g) {
 
 struct BlkLayout {
     uint32_t *bm;     // nga*4 words (bitmap, swizzled groups)
-    uint2 *gp;        // nga, same swizzle: (output position of the group, bytes 1..3 = set
-                      // bits in the group's words before word 1..3)
+    uint32_t *gp;     // nga, same swizzle: output position of the group relative to its
+                      // thread's base (bits 21..31) | set bits in the group's words before
+                      // word 1, 2, 3 (7 bits each, cumulative)
+    int32_t *tbase;   // threads: output position of each thread's first group
     int32_t *list;    // ecap: the row's admitted ids in this window (any order)
     int2 *desc;       // dcap descriptors: (bucket position of the word, mask word)
     int32_t *sB;      // lcap: bucket position of the slot's first word in the window
@@ -146,11 +148,13 @@ __device__ __forceinline__ void blk_build_desc(const BlkLayout &L, const uint32_
 // output index (within the window's run of the row) of window-relative id xr
 template <int G>
 __device__ __forceinline__ uint32_t blk_rank(const BlkLayout &L, uint32_t xr) {
-    const uint32_t wi = xr >> 5;
-    const uint32_t pg = blk_swz<G>(wi >> 2);
-    const uint2 g2 = L.gp[pg];
-    const uint32_t wd = L.bm[pg * 4u + (wi & 3u)];
-    return g2.x + __byte_perm(g2.y, 0u, 0x4440u | (wi & 3u)) + __popc(wd & ((1u << (xr & 31)) - 1u));
+    constexpr int LG = G >= 16 ? 4 : G >= 8 ? 3 : G >= 4 ? 2 : G >= 2 ? 1 : 0;
+    const uint32_t wi = xr >> 5, lg = wi >> 2, kq = wi & 3u;
+    const uint32_t pg = blk_swz<G>(lg);
+    const uint32_t e = L.gp[pg];
+    const uint32_t wd = L.bm[pg * 4u + kq];
+    const uint32_t before = kq ? (e >> (7u * (kq - 1u))) & 127u : 0u;
+    return (uint32_t)L.tbase[lg >> LG] + (e >> 21) + before + __popc(wd & ((1u << (xr & 31)) - 1u));
 }
 
 template <typename OutT, int G, bool MULTI, bool COMPACT>
@@ -161,17 +165,17 @@ __global__ void __launch_bounds__(1024) k_fill_blk(RowArgs a, BlkArgs g) {
     const int nga = g.nga;  // bitmap groups (multiple of G)
     BlkLayout L;
     L.bm = sm;
-    L.gp = reinterpret_cast<uint2 *>(L.bm + (size_t)nga * 4);
-    L.list = reinterpret_cast<int32_t *>(L.gp + nga);
-    L.desc = reinterpret_cast<int2 *>(L.list + g.ecap);
+    L.gp = L.bm + (size_t)nga * 4;
+    L.tbase = reinterpret_cast<int32_t *>(L.gp + ((nga + 1) & ~1));  // (8-byte alignment below)
+    L.list = L.tbase + ((NT + 1) & ~1);
+    L.desc = reinterpret_cast<int2 *>(L.list + ((g.ecap + 1) & ~1));
     L.sB = reinterpret_cast<int32_t *>(L.desc + g.dcap);
     L.sR = reinterpret_cast<uint32_t *>(L.sB + g.lcap);
     L.sC = reinterpret_cast<int32_t *>(L.sR + g.lcap);
     L.wt = L.sC + g.lcap;
     const uint32_t bm_s = (uint32_t)__cvta_generic_to_shared(L.bm);
     const uint32_t gp_s = (uint32_t)__cvta_generic_to_shared(L.gp);
-    const int capw = g.ecap / NW;  // list entries per warp
-    int32_t *wlist = L.list + warp * capw;
+    const uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(L.wt + 32);  // list length
     uint4 *bm4 = reinterpret_cast<uint4 *>(L.bm);
     for (int k = tid; k < nga; k += NT) bm4[k] = make_uint4(0u, 0u, 0u, 0u);
 
@@ -218,12 +222,12 @@ __global__ void __launch_bounds__(1024) k_fill_blk(RowArgs a, BlkArgs g) {
                 if (s < Li) L.sC[s] = T + ex;
                 T += tot;
             }
+            if (tid == 0) L.wt[32] = 0;
             __syncthreads();
             if (T == 0) continue;  // uniform: nothing of this row in the window
             const int Tp = (T + 7) & ~7;
             const bool once = Tp <= g.dcap;  // descriptors built once, reused by pass D
-            // ---- B: mark (and collect the admitted ids in the warp's list while they fit)
-            int wn = 0;  // ids this warp admitted
+            // ---- B: mark (and collect the admitted ids in the row's list while they fit)
             for (int cb = 0; cb < Tp; cb += g.dcap) {
                 const int nd = min(Tp - cb, g.dcap);
                 blk_build_desc(L, masks, cb, nd, T, Li);
@@ -237,6 +241,8 @@ __global__ void __launch_bounds__(1024) k_fill_blk(RowArgs a, BlkArgs g) {
                         x[u] = __ldg(bmem_l + (uint32_t)dv.x);
                         mw[u] = (uint32_t)dv.y;
                     }
+                    uint32_t bal[8];
+                    int cnt = 0;
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
                         bool adm = ((mw[u] >> lane) & 1u) != 0u;
@@ -245,10 +251,20 @@ __global__ void __launch_bounds__(1024) k_fill_blk(RowArgs a, BlkArgs g) {
                         const uint32_t wi = xr >> 5;
                         const uint32_t pg = blk_swz<G>(wi >> 2);
                         blk_red_or_if(adm, bm_s + (pg * 4u + (wi & 3u)) * 4u, 1u << (x[u] & 31));
-                        const uint32_t bal = MULTI ? __ballot_sync(0xffffffffu, adm) : mw[u];
-                        const int e = wn + __popc(bal & lt);
-                        if (adm && e < capw) wlist[e] = x[u];
-                        wn += __popc(bal);
+                        bal[u] = MULTI ? __ballot_sync(0xffffffffu, adm) : mw[u];
+                        cnt += __popc(bal[u]);
+                    }
+                    if (g.ecap > 0) {  // one shared reservation per warp batch (lane 0)
+                        uint32_t off = 0;
+                        if (lane == 0 && cnt > 0)
+                            asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(off) : "r"(cnt_s), "r"(cnt) : "memory");
+                        off = __shfl_sync(0xffffffffu, off, 0);
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const uint32_t e = off + __popc(bal[u] & lt);
+                            if (((bal[u] >> lane) & 1u) && e < (uint32_t)g.ecap) L.list[e] = x[u];
+                            off += __popc(bal[u]);
+                        }
                     }
                 }
                 __syncthreads();
@@ -262,34 +278,35 @@ __global__ void __launch_bounds__(1024) k_fill_blk(RowArgs a, BlkArgs g) {
                 if (own_groups) v = blk_lds4(bm_s + blk_swz<G>((uint32_t)(tid * G + j)) * 16u);
                 const uint32_t c0 = __popc(v.x), c1 = c0 + __popc(v.y), c2 = c1 + __popc(v.z);
                 loc[j] = (uint32_t)run;
-                cum[j] = (c0 << 8) | (c1 << 16) | (c2 << 24);
+                cum[j] = c0 | (c1 << 7) | (c2 << 14);
                 run += (int)(c2 + __popc(v.w));
             }
             int wtot;
+            const int ne = L.wt[32];  // (read before the scan reuses the scratch words)
             const int base = blk_scan(run, L.wt, wtot);
+            L.tbase[tid] = base;
             if (own_groups) {
 #pragma unroll
                 for (int j = 0; j < G; ++j)
-                    L.gp[blk_swz<G>((uint32_t)(tid * G + j))] = make_uint2((uint32_t)base + loc[j], cum[j]);
+                    L.gp[blk_swz<G>((uint32_t)(tid * G + j))] = (loc[j] << 21) | cum[j];
             }
             __syncthreads();
             // ---- D: place every admitted member at its output index
-            if (once && wn <= capw) {  // from the warp's own list: every lane holds an entry
-                for (int e0 = lane; e0 < wn; e0 += 128) {
+            if (g.ecap > 0 && ne <= g.ecap) {  // from the list: every lane holds an entry
+                for (int e0 = tid; e0 < ne; e0 += 4 * NT) {
                     int32_t x[4];
                     uint32_t r[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        const int e = e0 + 32 * u;
-                        x[u] = e < wn ? wlist[e] : w0;
+                        const int e = e0 + u * NT;
+                        x[u] = e < ne ? L.list[e] : w0;
                         r[u] = blk_rank<G>(L, (uint32_t)(x[u] - w0));
                     }
 #pragma unroll
                     for (int u = 0; u < 4; ++u)
-                        if (e0 + 32 * u < wn) orow[r[u]] = (OutT)(COMPACT ? __ldg(compact + x[u]) : x[u]);
+                        if (e0 + u * NT < ne) orow[r[u]] = (OutT)(COMPACT ? __ldg(compact + x[u]) : x[u]);
                 }
-            } else {  // list overflow (this warp) or chunked descriptors (all warps):
-                      // decode the warp's descriptors again
+            } else {  // list overflow: decode the descriptors again
                 for (int cb = 0; cb < Tp; cb += g.dcap) {
                     const int nd = min(Tp - cb, g.dcap);
                     if (!once) {
@@ -512,7 +529,9 @@ int run_bins(const RowArgs &a, const BinArgs &g, int sms, cudaStream_t s) {
 
 size_t blk_smem_bytes(const BlkArgs &g, int groups) {
     (void)groups;
-    return (size_t)g.nga * 24 + (size_t)g.ecap * 4 + (size_t)g.dcap * 8 + (size_t)g.lcap * 12 + 96 * 4;
+    return (size_t)g.nga * 16 + (size_t)((g.nga + 1) & ~1) * 4 + (size_t)((g.threads + 1) & ~1) * 4 +
+           (size_t)((g.ecap + 1) & ~1) * 4 + (size_t)g.dcap * 8 +
+           (size_t)g.lcap * 12 + 96 * 4;
 }
 
 // Geometry: `threads` per CTA (multiple of 32), G groups of 128 ids per thread (power of two
