@@ -231,7 +231,9 @@ def bench_gpu(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    # PICASSO_FORCE_SHARDED=1 runs the sharded (torchrun) path with one rank: a one-GPU check
+    # of the N>1 code path
+    if world > 1 or os.environ.get("PICASSO_FORCE_SHARDED") == "1":
         from paper_2401_06713_b200 import distributed as dist_mod
 
         dist_mod.bench_sharded(args)

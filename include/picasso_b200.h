@@ -194,6 +194,9 @@ int pcg_k1_result(pcg_ctx *ctx, int64_t *anticommuting);
  * 2 forces 8-bit). */
 int64_t pcg_last_copy_bytes(const pcg_ctx *ctx);
 
+/* Kernels this context has launched so far (benchmark accounting). */
+int64_t pcg_launch_total(const pcg_ctx *ctx);
+
 #ifdef __cplusplus
 }
 #endif

@@ -92,6 +92,8 @@ def library():
         lib.pcg_k1_result.restype = ctypes.c_int
         lib.pcg_last_copy_bytes.argtypes = [_VP]
         lib.pcg_last_copy_bytes.restype = ctypes.c_int64
+        lib.pcg_launch_total.argtypes = [_VP]
+        lib.pcg_launch_total.restype = ctypes.c_int64
         lib.pcg_stream.argtypes = [_VP]
         lib.pcg_stream.restype = _VP
         for name in ("pcg_create", "pcg_destroy", "pcg_set_inputs", "pcg_count",
@@ -110,7 +112,7 @@ EXPORTED = (
     "pcg_build_device", "pcg_set_profiling", "pcg_kernel_times", "pcg_set_option", "pcg_stream",
     "pcg_degrees_device", "pcg_fill_rows_device", "pcg_prep_device", "pcg_color_dynamic",
     "pcg_assign_lists", "pcg_validate", "pcg_host_register", "pcg_last_copy_bytes",
-    "pcg_k1_result", "pcg_color_dynamic_mt",
+    "pcg_k1_result", "pcg_color_dynamic_mt", "pcg_launch_total",
 )
 
 
@@ -159,6 +161,9 @@ class Context:
         a = _I64(0)
         self._check(self.lib.pcg_k1_result(self.h, ctypes.byref(a)), "pcg_k1_result")
         return int(a.value)
+
+    def launch_total(self) -> int:
+        return int(self.lib.pcg_launch_total(self.h))
 
     def last_copy_bytes(self) -> int:
         return int(self.lib.pcg_last_copy_bytes(self.h))

@@ -669,6 +669,7 @@ extern "C" int pcg_set_inputs(pcg_ctx *ctx, const uint64_t *words, int64_t n_tot
     ctx->staged = true;
     const int rc = prep_device(ctx);
     if (rc) ctx->staged = false;
+    else ctx->launch_total += ctx->prep_launches;
     return rc;
 }
 
@@ -909,7 +910,9 @@ extern "C" int pcg_count(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t r
                          int64_t row_end, pcg_counts *out) {
     if (!ctx) return PCG_E_ARG;
     int launches = 0;
-    return count_impl(ctx, shard, nshards, row_begin, row_end, out, &launches);
+    const int rc = count_impl(ctx, shard, nshards, row_begin, row_end, out, &launches);
+    ctx->launch_total += launches;
+    return rc;
 }
 
 extern "C" int pcg_copy_degrees(pcg_ctx *ctx, int32_t *deg, int32_t *deg_upper) {
@@ -1848,13 +1851,16 @@ static int fill_impl(pcg_ctx *ctx, bool to_host, int64_t *members, int64_t *offs
 extern "C" int pcg_fill(pcg_ctx *ctx, int64_t *members, int64_t *offsets, int64_t *neighbors) {
     if (!ctx) return PCG_E_ARG;
     int launches = 0;
-    return fill_impl(ctx, true, members, offsets, neighbors, &launches);
+    const int rc = fill_impl(ctx, true, members, offsets, neighbors, &launches);
+    ctx->launch_total += launches;
+    return rc;
 }
 
 extern "C" int pcg_count_device(pcg_ctx *ctx, pcg_counts *out, int32_t *launches) {
     if (!ctx) return PCG_E_ARG;
     int l = 0;
     int rc = count_impl(ctx, 0, 1, 0, ctx->n, out, &l);
+    ctx->launch_total += l;
     if (launches) *launches = l;
     return rc;
 }
@@ -1888,6 +1894,7 @@ extern "C" int pcg_build_device(pcg_ctx *ctx, pcg_counts *out, int32_t *launches
     rc = count_impl(ctx, 0, 1, 0, ctx->n, out, &l);
     if (rc) return rc;
     rc = fill_impl(ctx, false, nullptr, nullptr, nullptr, &l);
+    ctx->launch_total += l;
     if (launches) *launches = l;
     if (rc) return rc;
     if (ctx->k1_pending) {
@@ -1903,6 +1910,7 @@ extern "C" int pcg_fill_device(pcg_ctx *ctx, int32_t *launches) {
     if (!ctx) return PCG_E_ARG;
     int l = 0;
     int rc = fill_impl(ctx, false, nullptr, nullptr, nullptr, &l);
+    ctx->launch_total += l;
     if (launches) *launches = l;
     return rc;
 }
@@ -1940,6 +1948,7 @@ extern "C" int pcg_fill_rows(pcg_ctx *ctx, const int32_t *global_deg, int64_t *n
     int l = 0;
     rc = fill_rows_device(ctx, r0, r1, ctx->gdeg.as<int32_t>(), gmax, nm == n, ctx->nbr_o.p,
                           lohi[0], &l);
+    ctx->launch_total += l + 3;  // + the prefix scans and compaction
     if (rc) return rc;
     PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
     return d2h_pipelined(ctx, neighbors, ctx->nbr_o.p, (size_t)cnt * 8);
@@ -1989,17 +1998,22 @@ extern "C" int pcg_fill_rows_device(pcg_ctx *ctx, const int32_t *global_deg_dev,
     int l = 0;
     rc = fill_rows_device(ctx, r0, r1, ctx->gdeg.as<int32_t>(), maxdeg, nm == n, neighbors_dev,
                           lohi[0], &l);
+    ctx->launch_total += l + 3;  // + the prefix scans and compaction
     if (rc) return rc;
     PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
     return PCG_OK;
 }
+
+extern "C" int64_t pcg_launch_total(const pcg_ctx *ctx) { return ctx ? ctx->launch_total : 0; }
 
 extern "C" int pcg_prep_device(pcg_ctx *ctx) {
     if (!ctx) return PCG_E_ARG;
     if (!ctx->staged) return fail(ctx, PCG_E_STATE, "pcg_prep_device before pcg_set_inputs");
     PCG_TRY_CUDA(ctx, cudaSetDevice(ctx->device));
     ctx->counted = false;
-    return prep_device(ctx);
+    const int rc = prep_device(ctx);
+    if (!rc) ctx->launch_total += ctx->prep_launches;
+    return rc;
 }
 
 // Palette lists on the device (rng.py:22-70, driver.py:175-188): active ids in, (n, L) int64

@@ -310,6 +310,7 @@ struct pcg_ctx {
     std::vector<std::pair<int32_t *, size_t>> hxpiece;  // pinned exceptions per piece
     int blk_threads = 0, blk_groups = 0, blk_dcap = 0, blk_ecap = 0;  // block fill geometry (0 = auto)
     unsigned char *hs = nullptr;  // pinned scratch for the small per-build readbacks (512 B)
+    int64_t launch_total = 0;     // kernels launched by this context (pcg_launch_total)
     int bins_threads = 0;  // bins fill: threads per CTA (0 = auto)
     int bins_shift = 0;    // bins fill: bin width exponent delta from auto (testing/tuning)
     int k1_async = 0;                          // K1 on a side stream, result collected later

@@ -24,7 +24,7 @@ from typing import Optional
 
 import numpy as np
 
-from . import _native
+from . import _native, hostpool
 from .conflict import ConflictGraph, _lists_as_csr, _result_types, one_phase_projection
 from .errors import EdgeBudgetExceededError
 
@@ -50,6 +50,17 @@ class NativeEngine:
 
     def degrees(self, rows):
         return self.ctx.degrees(rows)
+
+    def fill_rows_device(self, global_deg, out_ptr):
+        """The rank's CSR slice into a device int64 buffer (None: bounds only)."""
+        import torch
+
+        g = torch.from_numpy(np.ascontiguousarray(global_deg, dtype=np.int32)).cuda()
+        mx = int(global_deg.max()) if global_deg.size else 0
+        torch.cuda.synchronize()  # the upload (torch's stream) before the context's stream reads it
+        lohi = self.ctx.fill_rows_device(g.data_ptr(), mx, out_ptr)
+        torch.cuda.synchronize()
+        return lohi
 
     def fill_rows(self, global_deg, want_values: bool):
         lo, hi = self.ctx.fill_rows(global_deg, None)
@@ -119,20 +130,41 @@ def build_sharded(view, lists, *, edge_budget: Optional[int] = None, threads: in
         gdegu = _all_gather_rows(dist, degu_local.astype(np.int32), ranges, dev)
         raise EdgeBudgetExceededError(one_phase_projection(gdegu, block_pairs, edge_budget),
                                       edge_budget)
-    lo, hi, slice_vals = engine.fill_rows(gdeg, True)
+    device_fill = dev.type == "cuda" and hasattr(engine, "fill_rows_device")
+    if device_fill:  # NCCL: the slice is filled into a device buffer, never crosses PCIe
+        lo, hi = engine.fill_rows_device(gdeg, None)
+    else:
+        lo, hi, slice_vals = engine.fill_rows(gdeg, True)
     # slices are contiguous in rank order; gather their lengths first
     lens = torch.tensor([hi - lo], dtype=torch.int64, device=dev)
     all_lens = [torch.empty_like(lens) for _ in range(world)]
     dist.all_gather(all_lens, lens)
     lens_np = [int(x.item()) for x in all_lens]
     width = max(lens_np) if lens_np else 0
-    t = torch.zeros(width, dtype=torch.int64, device=dev)
-    if hi > lo:
+    t = torch.zeros(max(width, 1), dtype=torch.int64, device=dev)
+    if device_fill:
+        if hi > lo:
+            engine.fill_rows_device(gdeg, t.data_ptr())
+    elif hi > lo:
         t[: hi - lo] = torch.from_numpy(slice_vals).to(dev)
-    parts = [torch.empty_like(t) for _ in range(world)]
-    dist.all_gather(parts, t)
-    nbr = np.concatenate([p[: lens_np[r]].cpu().numpy() for r, p in enumerate(parts)]) \
-        if world else np.zeros(0, np.int64)
+    total_len = sum(lens_np)
+    if device_fill:
+        # all-gather over NVLink, then one DMA of the canonical CSR into the pooled (pinned)
+        # host buffer the single-GPU build also reuses
+        out = torch.empty(world * max(width, 1), dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(out, t)
+        nbr = hostpool.empty_int64(total_len)
+        pos = 0
+        host = torch.from_numpy(nbr)
+        for r in range(world):
+            if lens_np[r]:
+                host[pos:pos + lens_np[r]].copy_(out[r * max(width, 1): r * max(width, 1) + lens_np[r]])
+                pos += lens_np[r]
+    else:
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+        nbr = np.concatenate([p[: lens_np[r]].cpu().numpy() for r, p in enumerate(parts)]) \
+            if world else np.zeros(0, np.int64)
     has = gdeg > 0
     members_ids = active[has]
     offsets = np.zeros(int(has.sum()) + 1, dtype=np.int64)
@@ -194,18 +226,43 @@ def bench_sharded(args) -> None:
     torch.cuda.synchronize()
     dist.barrier()
     times = []
-    for _ in range(args.steps):
-        torch.cuda.synchronize()
-        dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        step()
-        e1.record()
-        e1.synchronize()
-        times.append(e0.elapsed_time(e1))
+    l0 = ctx.launch_total()
+    with bench_mod.ClockSampler(None if args.no_clocks else local) as clocks:
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            step()
+            e1.record()
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+    launches = torch.tensor([ctx.launch_total() - l0], dtype=torch.int64, device=dev)
+    dist.all_reduce(launches)
     t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
+
+    # ---- end to end through the public sharded build (host inputs in, the canonical int64
+    # CSR on every rank out), max over ranks
+    import time
+
+    e2e = []
+    for k in range(1 + args.steps):
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        gc = build_sharded(view, lists)
+        torch.cuda.synchronize()
+        if k >= 1:
+            e2e.append(time.perf_counter() - t0)
+        nnz = int(gc.graph.neighbors.size)
+        members = int(gc.members.size)
+        gc = None
+    te = torch.tensor([statistics.mean(e2e)], dtype=torch.float64, device=dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_s = float(te.item())
+    h2d = view.backing.words.nbytes + view.active.nbytes + lists.array.nbytes
     if rank == 0:
         line = {
             "metric": bench_mod.METRIC, "value": pairs / (ms * 1e-3), "unit": "pairs/s",
@@ -215,8 +272,17 @@ def bench_sharded(args) -> None:
             "config": {"workload": f"{args.workload}: n={n}, P={plan.palette_size}, L={plan.list_size}",
                        "pairs_per_step": pairs,
                        "parallelism": f"pair-space shards x{world} (K1 tiles + K2 row ranges), "
-                                      "NCCL degree all-gather + CSR slice all-gather"},
-            "gpu_launches": None,
+                                      "NCCL degree all-gather + CSR slice all-gather",
+                       "l2": "inputs replicated per rank; no flush (the CSR slices exceed L2)"},
+            "e2e": {"value": pairs / e2e_s, "unit": "pairs/s",
+                    # per rank: its inputs + its slice up for the all-gather; down: its int64
+                    # slice and the gathered canonical CSR (every rank returns the whole graph)
+                    "h2d_bytes_per_step": int(h2d + 8 * nnz // world),
+                    "d2h_bytes_per_step": int(8 * nnz // world + 8 * nnz + 16 * members),
+                    "ms_per_step": 1e3 * e2e_s,
+                    "api": "distributed.build_sharded (every rank returns the canonical CSR)"},
+            "gpu_launches": int(launches.item()),
+            "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

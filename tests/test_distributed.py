@@ -145,3 +145,31 @@ def test_sharded_native_engine_on_one_gpu(world, name):
     cuda:0); the gathered CSR must equal the reference."""
     res = _run(world, name, native=True)
     assert [r[1] for r in res] == ["ok"] * world, res
+
+
+@pytest.mark.gpu
+def test_sharded_build_nccl_device_path(golden_ref):
+    """build_sharded over NCCL (one rank): the slice is filled into a device buffer, gathered
+    on the device and copied once into the pooled host buffer; the CSR must be the golden."""
+    import os
+    import subprocess
+    import sys
+
+    g = golden_ref["builds_hashed"]["q32_n20000"]
+    code = (
+        "import os, sys, hashlib, numpy as np, torch, torch.distributed as dist; "
+        "sys.path.insert(0, 'tests'); "
+        "import paper_2401_06713_b200 as b200; from paper_2401_06713_b200 import distributed as D; "
+        "from conftest import pauli_view, random_lists; "
+        "torch.cuda.set_device(0); dist.init_process_group('nccl'); "
+        "v = pauli_view(20000, 32, 0); gc = D.build_sharded(v, random_lists(v, seed=0)); "
+        "h = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]; "
+        "print(h(gc.graph.offsets), h(gc.graph.neighbors)); dist.destroy_process_group()"
+    )
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0", WORLD_SIZE="1",
+               LOCAL_RANK="0")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                         text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.split()[-2:] == [g["offsets_sha"], g["neighbors_sha"]]
