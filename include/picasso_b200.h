@@ -111,6 +111,8 @@ int pcg_degrees_device(pcg_ctx *ctx, int32_t *deg_dev);
 int pcg_prep_device(pcg_ctx *ctx);
 int pcg_fill_rows_device(pcg_ctx *ctx, const int32_t *global_deg_dev, int32_t maxdeg,
                          int64_t *neighbors_dev, int64_t *slice_begin, int64_t *slice_end);
+/* (With pcg_set_option(ctx, "rows_out32", 1) neighbors_dev receives int32 ids instead: the
+ * sharded build exchanges half the bytes and widens after the all-gather.) */
 
 /* Device-resident timing hooks for the benchmark (no host traffic): re-run count and fill
  * on the inputs already staged; outputs stay in HBM.  *launches receives the number of

@@ -223,6 +223,7 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "blk_ecap")) ctx->blk_ecap = (int)value;
     else if (!strcmp(key, "bins_threads")) ctx->bins_threads = (int)value;
     else if (!strcmp(key, "bins_shift")) ctx->bins_shift = (int)value;
+    else if (!strcmp(key, "rows_out32")) ctx->rows_out32 = (int)value;
     else if (!strcmp(key, "seg_warps")) ctx->seg_warps = (int)value;
     else return fail(ctx, PCG_E_ARG, std::string("unknown option ") + key);
     return PCG_OK;
@@ -1996,8 +1997,10 @@ extern "C" int pcg_fill_rows_device(pcg_ctx *ctx, const int32_t *global_deg_dev,
     *slice_end = lohi[1];
     if (!neighbors_dev || lohi[1] == lohi[0]) return PCG_OK;
     int l = 0;
+    // option "rows_out32": the slice is written as int32 (a sharded build all-gathers half
+    // the bytes and widens after the exchange)
     rc = fill_rows_device(ctx, r0, r1, ctx->gdeg.as<int32_t>(), maxdeg, nm == n, neighbors_dev,
-                          lohi[0], &l);
+                          lohi[0], &l, /*out64=*/ctx->rows_out32 == 0);
     ctx->launch_total += l + 3;  // + the prefix scans and compaction
     if (rc) return rc;
     PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));

@@ -311,6 +311,7 @@ struct pcg_ctx {
     int blk_threads = 0, blk_groups = 0, blk_dcap = 0, blk_ecap = 0;  // block fill geometry (0 = auto)
     unsigned char *hs = nullptr;  // pinned scratch for the small per-build readbacks (512 B)
     int64_t launch_total = 0;     // kernels launched by this context (pcg_launch_total)
+    int rows_out32 = 0;           // pcg_fill_rows_device writes int32 ids (sharded exchange)
     int bins_threads = 0;  // bins fill: threads per CTA (0 = auto)
     int bins_shift = 0;    // bins fill: bin width exponent delta from auto (testing/tuning)
     int k1_async = 0;                          // K1 on a side stream, result collected later

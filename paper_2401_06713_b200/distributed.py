@@ -51,14 +51,18 @@ class NativeEngine:
     def degrees(self, rows):
         return self.ctx.degrees(rows)
 
-    def fill_rows_device(self, global_deg, out_ptr):
-        """The rank's CSR slice into a device int64 buffer (None: bounds only)."""
+    def fill_rows_device(self, global_deg, out_ptr, out32: bool = False):
+        """The rank's CSR slice into a device buffer, int64 or int32 (None: bounds only)."""
         import torch
 
         g = torch.from_numpy(np.ascontiguousarray(global_deg, dtype=np.int32)).cuda()
         mx = int(global_deg.max()) if global_deg.size else 0
         torch.cuda.synchronize()  # the upload (torch's stream) before the context's stream reads it
-        lohi = self.ctx.fill_rows_device(g.data_ptr(), mx, out_ptr)
+        self.ctx.option("rows_out32", 1 if out32 else 0)
+        try:
+            lohi = self.ctx.fill_rows_device(g.data_ptr(), mx, out_ptr)
+        finally:
+            self.ctx.option("rows_out32", 0)
         torch.cuda.synchronize()
         return lohi
 
@@ -141,24 +145,25 @@ def build_sharded(view, lists, *, edge_budget: Optional[int] = None, threads: in
     dist.all_gather(all_lens, lens)
     lens_np = [int(x.item()) for x in all_lens]
     width = max(lens_np) if lens_np else 0
-    t = torch.zeros(max(width, 1), dtype=torch.int64, device=dev)
+    t = torch.zeros(max(width, 1), dtype=torch.int32 if device_fill else torch.int64, device=dev)
     if device_fill:
         if hi > lo:
-            engine.fill_rows_device(gdeg, t.data_ptr())
+            engine.fill_rows_device(gdeg, t.data_ptr(), out32=True)
     elif hi > lo:
         t[: hi - lo] = torch.from_numpy(slice_vals).to(dev)
     total_len = sum(lens_np)
     if device_fill:
-        # all-gather over NVLink, then one DMA of the canonical CSR into the pooled (pinned)
-        # host buffer the single-GPU build also reuses
-        out = torch.empty(world * max(width, 1), dtype=torch.int64, device=dev)
+        # all-gather the int32 slices over NVLink, widen on the device, then one DMA of the
+        # canonical CSR into the pooled (pinned) host buffer the single-GPU build also reuses
+        out = torch.empty(world * max(width, 1), dtype=torch.int32, device=dev)
         dist.all_gather_into_tensor(out, t)
         nbr = hostpool.empty_int64(total_len)
         pos = 0
         host = torch.from_numpy(nbr)
         for r in range(world):
             if lens_np[r]:
-                host[pos:pos + lens_np[r]].copy_(out[r * max(width, 1): r * max(width, 1) + lens_np[r]])
+                seg = out[r * max(width, 1): r * max(width, 1) + lens_np[r]].to(torch.int64)
+                host[pos:pos + lens_np[r]].copy_(seg)
                 pos += lens_np[r]
     else:
         parts = [torch.empty_like(t) for _ in range(world)]
@@ -198,6 +203,7 @@ def bench_sharded(args) -> None:
     ranges = row_ranges(n, world)
     r0, r1 = ranges[rank]
     width = max(b - a for a, b in ranges)
+    ctx.option("rows_out32", 1)  # the timed step exchanges int32 slices
     deg_local = torch.zeros(width, dtype=torch.int32, device=dev)
     gdeg_parts = torch.zeros(world * width, dtype=torch.int32, device=dev)
 
@@ -215,9 +221,9 @@ def bench_sharded(args) -> None:
         all_lens = torch.zeros(world, dtype=torch.int64, device=dev)
         dist.all_gather_into_tensor(all_lens, lens)
         w = int(all_lens.max().item())
-        buf = torch.zeros(max(w, 1), dtype=torch.int64, device=dev)
+        buf = torch.zeros(max(w, 1), dtype=torch.int32, device=dev)  # int32 ids: half the exchange
         ctx.fill_rows_device(gdeg.data_ptr(), mx, buf.data_ptr())
-        out = torch.empty(world * max(w, 1), dtype=torch.int64, device=dev)
+        out = torch.empty(world * max(w, 1), dtype=torch.int32, device=dev)
         dist.all_gather_into_tensor(out, buf)
         return c
 
@@ -243,6 +249,7 @@ def bench_sharded(args) -> None:
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
 
+    ctx.option("rows_out32", 0)
     # ---- end to end through the public sharded build (host inputs in, the canonical int64
     # CSR on every rank out), max over ranks
     import time
@@ -272,13 +279,14 @@ def bench_sharded(args) -> None:
             "config": {"workload": f"{args.workload}: n={n}, P={plan.palette_size}, L={plan.list_size}",
                        "pairs_per_step": pairs,
                        "parallelism": f"pair-space shards x{world} (K1 tiles + K2 row ranges), "
-                                      "NCCL degree all-gather + CSR slice all-gather",
+                                      "NCCL degree all-gather + int32 CSR slice all-gather",
                        "l2": "inputs replicated per rank; no flush (the CSR slices exceed L2)"},
             "e2e": {"value": pairs / e2e_s, "unit": "pairs/s",
-                    # per rank: its inputs + its slice up for the all-gather; down: its int64
-                    # slice and the gathered canonical CSR (every rank returns the whole graph)
-                    "h2d_bytes_per_step": int(h2d + 8 * nnz // world),
-                    "d2h_bytes_per_step": int(8 * nnz // world + 8 * nnz + 16 * members),
+                    # per rank: its inputs and the gathered degrees up; down: the degrees and
+                    # the canonical int64 CSR (every rank returns the whole graph; members and
+                    # offsets are derived on the host from the degrees)
+                    "h2d_bytes_per_step": int(h2d + 4 * n),
+                    "d2h_bytes_per_step": int(8 * nnz + 4 * n),
                     "ms_per_step": 1e3 * e2e_s,
                     "api": "distributed.build_sharded (every rank returns the canonical CSR)"},
             "gpu_launches": int(launches.item()),
