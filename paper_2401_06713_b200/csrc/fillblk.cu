@@ -9,14 +9,17 @@
 //  B. mark: descriptors are materialised in shared memory (thread per descriptor: one mask
 //     word load each, all in flight), then each warp decodes 8 at a time: lane t loads bucket
 //     member 32w+t (one coalesced 128-byte load) and, if its mask bit is set, ORs its bit into
-//     the bitmap (red.shared.or, no return value).
+//     the bitmap (red.shared.or, no return value) and appends the id to the row's list (the
+//     mask word is the ballot; one shared reservation per warp batch).
 //  C. prefix: the bitmap is cut into 128-id groups (4 words); thread t owns G consecutive
-//     groups, popcounts them and a block scan gives every group its output position.
-//     Groups are XOR-swizzled inside each thread's run so the 128-bit loads of a quarter
-//     warp hit distinct banks.
-//  D. place: the descriptors are decoded again; an admitted member's output index is its
-//     group's position + the set bits below it in the group, so every entry is written
-//     straight to its place in the row (ascending ids), with no per-lane extraction loop.
+//     groups, popcounts them and a block scan gives every thread its base; each group keeps
+//     a 4-byte record: its position relative to the thread's base (11 bits) and the set bits
+//     of its first three words (7 bits each, cumulative).  Groups are XOR-swizzled inside
+//     each thread's run so the 128-bit loads of a quarter warp hit distinct banks.
+//  D. place: every listed id's output index is its thread base + its group's record + the
+//     set bits below it in its word, so each entry is written straight to its place in the
+//     row (ascending ids), with no per-lane extraction loop.  A window whose ids overflow the
+//     list decodes its descriptors again instead.
 //  E. clear the bitmap.
 // Rows wider than the window (n > NT*G*128 ids) are cut into windows; a mask word straddling
 // two windows is decoded in both and filtered by id range (per-color window bounds as in the
