@@ -407,6 +407,26 @@ def test_aggressive_lists(n, pct, alpha):
         assert np.array_equal(nb[off[i]:off[i + 1]], row)
 
 
+def test_auto_bins_fill_above_block_range():
+    """n > 128K ids takes the bins fill by default (and the pipelined public copy-out): the
+    commuting-pair count and sampled full rows against the oracle, sortedness and offsets."""
+    from oracle.oracle import OracleInstance
+
+    n = 140_000
+    v = pauli_view(n, 48, 12)
+    lists = random_lists(v, seed=5)
+    gc = b200.build(v, lists)
+    nb, off = gc.graph.neighbors, gc.graph.offsets
+    assert off[0] == 0 and off[-1] == nb.size == 2 * gc.edge_count
+    inst = OracleInstance(v.backing.words, v.active, lists)
+    assert gc.view_edges_scanned == inst.commute_count()
+    rs = np.random.default_rng(3)
+    for i in rs.choice(n, size=6, replace=False):
+        row, _ = inst.row(int(i))
+        assert np.array_equal(nb[off[i]:off[i + 1]], row)
+        assert np.all(np.diff(row) > 0)
+
+
 def test_full_size_config2_properties():
     """BASELINE config 2 (100k x 32q): the oracle cannot build it in test time, so check
     size-independent properties: commuting-pair total against the oracle's popcount sweep,
