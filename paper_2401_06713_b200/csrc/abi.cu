@@ -583,7 +583,9 @@ static int prep_device(pcg_ctx *ctx) {
     if (fr_supported(ctx->kw)) {
         PCG_ALLOC(ctx, ctx->H, (size_t)ctx->npad * ctx->kw * 4 * 4);
         ctx->h_wide = fr_jb(ctx->kw, ctx->k1_wide) == K1_FR_JB2;
-        if (ctx->h_wide) launch_fr_prep2(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
+        ctx->h_fr5 = ctx->k1_algo == 3 && (ctx->kw == 2 || ctx->kw == 4);
+        if (ctx->h_fr5) launch_fr_prep5(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
+        else if (ctx->h_wide) launch_fr_prep2(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
         else launch_fr_prep(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
         PCG_CHECK_LAUNCH(ctx);
     }
@@ -679,6 +681,7 @@ extern "C" int pcg_set_inputs(pcg_ctx *ctx, const uint64_t *words, int64_t n_tot
 // --------------------------------------------------------------------------------------
 static int k1_algo(const pcg_ctx *ctx) {
     if (ctx->k1_algo == 1) return 1;
+    if (ctx->k1_algo == 3 && ctx->h_fr5) return 3;
     if (ctx->k1_algo == 2 && fr_supported(ctx->kw)) return 2;
     return fr_supported(ctx->kw) ? 2 : 1;
 }
@@ -719,8 +722,9 @@ static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, 
                   cudaStream_t s) {
     unsigned long long *anti = ctx->scal.as<unsigned long long>();
     const int64_t n = ctx->n;
-    if (k1_algo(ctx) == 2) {
-        const int64_t JB = ctx->h_wide ? K1_FR_JB2 : K1_FR_JB;
+    if (k1_algo(ctx) >= 2) {
+        const bool fr5 = k1_algo(ctx) == 3;
+        const int64_t JB = (ctx->h_wide && !fr5) ? K1_FR_JB2 : K1_FR_JB;
         const int64_t njb = ctx->npad / JB, ic = fr_ichunk(ctx);
         std::vector<int64_t> start(njb + 1, 0);
         for (int64_t jb = 0; jb < njb; ++jb) {
@@ -745,7 +749,11 @@ static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, 
         PCG_ALLOC(ctx, ctx->items, (size_t)(njb + 1) * 8);
         PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->items.p, start.data(), (size_t)(njb + 1) * 8,
                                           cudaMemcpyHostToDevice, s));
-        if (ctx->h_wide)
+        if (fr5)
+            *launches += launch_commute_fr5_items(ctx->B.as<uint32_t>(), ctx->H.as<uint32_t>(),
+                                                  ctx->kw, n, ctx->items.as<int64_t>(), njb,
+                                                  (int32_t)ic, i0, i1, anti, ctx->sms, s);
+        else if (ctx->h_wide)
             *launches += launch_commute_fr2_items(ctx->B.as<uint32_t>(), ctx->H.as<uint32_t>(),
                                                   ctx->kw, n, ctx->items.as<int64_t>(), njb,
                                                   (int32_t)ic, i0, i1, anti, ctx->sms, s);
@@ -2103,7 +2111,9 @@ extern "C" int pcg_validate(pcg_ctx *ctx, const uint64_t *words, int64_t n_total
     if (fr_supported(ctx->kw)) {
         PCG_ALLOC(ctx, ctx->H, (size_t)ctx->npad * ctx->kw * 4 * 4);
         ctx->h_wide = fr_jb(ctx->kw, ctx->k1_wide) == K1_FR_JB2;
-        if (ctx->h_wide) launch_fr_prep2(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
+        ctx->h_fr5 = ctx->k1_algo == 3 && (ctx->kw == 2 || ctx->kw == 4);
+        if (ctx->h_fr5) launch_fr_prep5(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
+        else if (ctx->h_wide) launch_fr_prep2(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
         else launch_fr_prep(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
         PCG_CHECK_LAUNCH(ctx);
     }

@@ -291,6 +291,154 @@ __global__ void k_fr_prep2(const uint32_t *__restrict__ A, int64_t npad, uint32_
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Four-Russians with 5-bit slices (k1_algo 3): 32-entry tables per slice, so a row costs
+// ceil(K/5) table lookups per 32 partners instead of K/4 (26 instead of 32 at q = 64): fewer
+// shared-memory bytes per pair, the bound of the 4-bit kernels.  Layout as k_commute_fr:
+// entry (slice g, value v, lane t) at word ((g>>1)*32 + v)*64 + (g&1)*32 + t, so a lookup
+// address is one PRMT of the row's 16-bit table row h = (g>>1)*32 + v_g with the lane offset.
+// ---------------------------------------------------------------------------------------
+template <int KW>
+__global__ void k_fr_prep5(const uint32_t *__restrict__ A, int64_t npad, uint32_t *__restrict__ H) {
+    constexpr int K = 32 * KW, NG = (K + 4) / 5, NP = (NG + 1) / 2;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= npad) return;
+    const uint32_t *a = A + i * KW;
+    uint32_t w[KW + 1];
+#pragma unroll
+    for (int k = 0; k < KW; ++k) w[k] = a[k];
+    w[KW] = 0u;
+    uint32_t *h = H + i * (KW * 4);
+#pragma unroll
+    for (int m = 0; m < NP; ++m) {
+        uint32_t hv[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int g = 2 * m + q, b = 5 * g;  // bits [b, b+5) of A_i (zero past K)
+            uint32_t v = 0u;
+            if (g < NG) {
+                const uint64_t win = ((uint64_t)w[(b >> 5) + 1] << 32) | w[b >> 5];
+                v = (uint32_t)(win >> (b & 31)) & 31u;
+            }
+            hv[q] = (uint32_t)m * 32u + v;
+        }
+        h[m] = hv[0] | (hv[1] << 16);
+    }
+}
+
+template <int KW>
+__global__ void __launch_bounds__(FR_WARPS * 32) k_commute_fr5(
+    const uint32_t *__restrict__ B, const uint32_t *__restrict__ H, int64_t n,
+    const int64_t *__restrict__ item_start, int64_t njb, int32_t ichunk, int64_t item0,
+    int64_t item1, unsigned long long *__restrict__ anti) {
+    constexpr int K = 32 * KW;
+    constexpr int NG = (K + 4) / 5, NP = (NG + 1) / 2;  // 5-bit slices, slice pairs
+    constexpr int TBL_WORDS = NP * 32 * 64;
+    constexpr int BT_STRIDE = K + 1;
+    extern __shared__ __align__(16) uint32_t smem[];
+    uint32_t *tbl = smem;
+    uint32_t *bt = smem + TBL_WORDS;  // 32 * BT_STRIDE
+    __shared__ unsigned long long red[FR_WARPS];
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lb0 = (uint32_t)lane * 4u, lb1 = 128u + (uint32_t)lane * 4u;
+    const char *tb = reinterpret_cast<const char *>(tbl);
+
+    const int64_t nitems = item1 - item0;
+    const int64_t my0 = item0 + nitems * blockIdx.x / gridDim.x;
+    const int64_t my1 = item0 + nitems * (blockIdx.x + 1) / gridDim.x;
+    int64_t cur_jb = -1;
+    unsigned long long local = 0;
+
+    for (int64_t it = my0; it < my1; ++it) {
+        int64_t lo = 0, hi = njb;
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (item_start[mid] <= it) lo = mid; else hi = mid;
+        }
+        const int64_t jb = lo, ic = it - item_start[jb];
+        if (jb != cur_jb) {
+            __syncthreads();
+            // phase A: transpose the 1024 partner vectors into bit rows bt[t][k]
+            for (int t = warp; t < 32; t += FR_WARPS) {
+                const uint32_t *bj = B + (jb * K1_FR_JB + 32 * t + lane) * KW;
+                uint32_t v[KW];
+#pragma unroll
+                for (int k = 0; k < KW; ++k) v[k] = __ldg(bj + k);
+#pragma unroll
+                for (int k = 0; k < KW; ++k) {
+                    uint32_t mine = 0;
+#pragma unroll
+                    for (int s = 0; s < 32; ++s) {
+                        const uint32_t word = __ballot_sync(0xffffffffu, (v[k] >> s) & 1u);
+                        if (lane == s) mine = word;
+                    }
+                    bt[t * BT_STRIDE + 32 * k + lane] = mine;
+                }
+            }
+            __syncthreads();
+            // phase B: the 32 XOR combinations of each slice's 5 bit rows (doubling)
+            for (int g = warp; g < NG; g += FR_WARPS) {
+                const uint32_t *row = bt + lane * BT_STRIDE;
+                uint32_t e[32];
+                e[0] = 0u;
+#pragma unroll
+                for (int b = 0; b < 5; ++b) {
+                    const int k = 5 * g + b;
+                    const uint32_t rb = k < K ? row[k] : 0u;
+#pragma unroll
+                    for (int v = 0; v < (1 << b); ++v) e[v | (1 << b)] = e[v] ^ rb;
+                }
+                uint32_t *dst = tbl + (g >> 1) * 32 * 64 + (g & 1) * 32 + lane;
+#pragma unroll
+                for (int v = 0; v < 32; ++v) dst[v * 64] = e[v];
+            }
+            if (NG & 1) {  // the unused odd slice of the last pair: value 0 -> entry 0
+                for (int x = threadIdx.x; x < 32; x += blockDim.x)
+                    tbl[(NP - 1) * 32 * 64 + 32 + x] = 0u;
+            }
+            __syncthreads();
+            cur_jb = jb;
+        }
+        const int64_t jlast = min(n, (jb + 1) * (int64_t)K1_FR_JB);
+        const int64_t i0 = ic * ichunk;
+        const int64_t i1 = min(i0 + ichunk, jlast);
+        const int64_t jbase = jb * K1_FR_JB + 32 * lane;
+        for (int64_t i = i0 + warp; i < i1; i += FR_WARPS) {
+            const uint4 *hp = reinterpret_cast<const uint4 *>(H + i * (KW * 4));
+            uint32_t acc = 0;
+#pragma unroll
+            for (int q = 0; q < (NP + 3) / 4; ++q) {
+                const uint4 hv = __ldg(hp + q);
+                const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    if (4 * q + m < NP) {
+                        const uint32_t ad0 = __byte_perm(hw[m], lb0, 0x5104);
+                        const uint32_t ad1 = __byte_perm(hw[m], lb1, 0x5324);
+                        acc ^= *reinterpret_cast<const uint32_t *>(tb + ad0) ^
+                               *reinterpret_cast<const uint32_t *>(tb + ad1);
+                    }
+                }
+            }
+            uint32_t mask;
+            const int64_t d = i - jbase;
+            if (d < 0) mask = 0xffffffffu;
+            else if (d >= 31) mask = 0u;
+            else mask = ~((2u << d) - 1u);
+            local += __popc(acc & mask);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
+    if (lane == 0) red[warp] = local;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long sacc = 0;
+        for (int w = 0; w < FR_WARPS; ++w) sacc += red[w];
+        if (sacc) atomicAdd(anti, sacc);
+    }
+}
+
 template <int KW>
 __global__ void __launch_bounds__(FR_WARPS * 32) k_commute_fr2(
     const uint32_t *__restrict__ B, const uint32_t *__restrict__ H, int64_t n,
@@ -445,6 +593,24 @@ int run_fr2(const uint32_t *B, const uint32_t *H, int64_t n, const int64_t *item
 }
 
 template <int KW>
+size_t fr5_smem() {
+    constexpr int K = 32 * KW, NG = (K + 4) / 5, NP = (NG + 1) / 2;
+    return (size_t)NP * 32 * 64 * 4 + (size_t)32 * (K + 1) * 4;
+}
+
+template <int KW>
+int run_fr5(const uint32_t *B, const uint32_t *H, int64_t n, const int64_t *item_start,
+            int64_t njb, int32_t ichunk, int64_t item0, int64_t item1,
+            unsigned long long *anti, int sms, cudaStream_t s) {
+    const size_t smem = fr5_smem<KW>();
+    allow_max_smem(k_commute_fr5<KW>);
+    const int grid = occupancy_grid(k_commute_fr5<KW>, FR_WARPS * 32, smem, sms, item1 - item0);
+    k_commute_fr5<KW><<<grid, FR_WARPS * 32, smem, s>>>(B, H, n, item_start, njb, ichunk, item0,
+                                                       item1, anti);
+    return 1;
+}
+
+template <int KW>
 int run_fr(const uint32_t *B, const uint32_t *H, int64_t n, const int64_t *item_start,
            int64_t njb, int32_t ichunk, int64_t item0, int64_t item1,
            unsigned long long *anti, int sms, cudaStream_t s) {
@@ -481,6 +647,28 @@ int launch_commute_direct(const uint32_t *A, const uint32_t *B, int32_t kw, int6
 bool fr_supported(int32_t kw) { return kw == 2 || kw == 4 || kw == 6 || kw == 8; }
 
 int fr_jb(int32_t kw, int wide) { return (wide && (kw == 2 || kw == 4)) ? K1_FR_JB2 : K1_FR_JB; }
+
+int launch_fr_prep5(const uint32_t *A, int32_t kw, int64_t npad, uint32_t *H, cudaStream_t s) {
+    const int tb = 256;
+    const unsigned grid = (unsigned)((npad + tb - 1) / tb);
+    switch (kw) {
+        case 2: k_fr_prep5<2><<<grid, tb, 0, s>>>(A, npad, H); return 1;
+        case 4: k_fr_prep5<4><<<grid, tb, 0, s>>>(A, npad, H); return 1;
+        default: return 0;
+    }
+}
+
+int launch_commute_fr5_items(const uint32_t *B, const uint32_t *H, int32_t kw, int64_t n,
+                             const int64_t *item_start, int64_t njb, int32_t ichunk,
+                             int64_t item0, int64_t item1, unsigned long long *anti, int sms,
+                             cudaStream_t s) {
+    if (item1 <= item0) return 0;
+    switch (kw) {
+        case 2: return run_fr5<2>(B, H, n, item_start, njb, ichunk, item0, item1, anti, sms, s);
+        case 4: return run_fr5<4>(B, H, n, item_start, njb, ichunk, item0, item1, anti, sms, s);
+        default: return 0;
+    }
+}
 
 int launch_fr_prep2(const uint32_t *A, int32_t kw, int64_t npad, uint32_t *H, cudaStream_t s) {
     const int tb = 256;
