@@ -223,6 +223,7 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "blk_ecap")) ctx->blk_ecap = (int)value;
     else if (!strcmp(key, "bins_threads")) ctx->bins_threads = (int)value;
     else if (!strcmp(key, "bins_shift")) ctx->bins_shift = (int)value;
+    else if (!strcmp(key, "bins_maxdeg")) ctx->bins_maxdeg = (int)value;
     else if (!strcmp(key, "rows_out32")) ctx->rows_out32 = (int)value;
     else if (!strcmp(key, "seg_warps")) ctx->seg_warps = (int)value;
     else return fail(ctx, PCG_E_ARG, std::string("unknown option ") + key);
@@ -514,6 +515,16 @@ static int prep_device(pcg_ctx *ctx) {
             // measured: staging the lists pays when they are u16 (small palettes); u32 lists
             // next to the hash table cost occupancy (config 3)
             o.stage_lists = (!ctx->ragged && o.l16) ? 1 : 0;
+            // direct mode: loser lists sized for the expected number of members per color
+            // that share a smaller color with an earlier member, ~ (m (L-1) / 2)^2 / P, x2
+            // headroom (500k ids, P = 25000, L = 26: ~2.3k, beyond the default 1024)
+            {
+                const double half = (double)m_max * std::max(1, ctx->lmax - 1) / 2.0;
+                const double est = half * half / (double)std::max<int64_t>(P, 1);
+                int64_t lc = 1024;
+                while (lc < 2.0 * est && lc < 8192) lc <<= 1;
+                o.lcap = (int32_t)lc;
+            }
             // shared memory: big buckets x long lists (e.g. 500k ids, P' = 2.5%, alpha = 3:
             // ~1.7k members x 39 colors) do not fit with staged lists; the direct table reads
             // the staged lists, so it goes too; if even the hash table does not fit, the
@@ -1675,7 +1686,10 @@ static int fill_rows_device(pcg_ctx *ctx, int64_t r0, int64_t r1, const int32_t 
     // the bins fill (counting sort per row) is the default beyond the block fill's range
     // when the longest row fits its list (1M ids: 23.7 ms vs the segmented fill's 52.8)
     const bool bins_auto = ctx->fill_algo == 0 && ctx->n > 131072;
-    if ((ctx->fill_algo == 7 || bins_auto) && ctx->mask_words < (1LL << 32) && maxdeg <= 8192) {
+    // measured (500k ids): rows up to 16K ids still win with the bins fill (P' = 20%,
+    // alpha = 4.5, mean row 8.5k: 36.9 ms with 384 threads vs the segmented fill's 52.9)
+    const int32_t bins_maxdeg = ctx->bins_maxdeg > 0 ? ctx->bins_maxdeg : 16384;
+    if ((ctx->fill_algo == 7 || bins_auto) && ctx->mask_words < (1LL << 32) && maxdeg <= bins_maxdeg) {
         // bins fill (sparse rows): counting sort of each row's admitted ids
         BinArgs g{};
         const double mean = ctx->n > 0 ? (double)ctx->last.deg_sum / (double)ctx->n : 1.0;

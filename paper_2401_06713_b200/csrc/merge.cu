@@ -21,7 +21,7 @@ namespace {
 
 constexpr int OWN_THREADS = 256;
 constexpr int OWN_COLL = 2048;        // collision list capacity
-constexpr int OWN_LCAP = 1024;        // direct ownership: losers per level
+constexpr int OWN_LCAP = 1024;        // direct ownership: default losers per level (o.lcap)
 constexpr int MERGE_WARPS = 4;
 
 template <int KW>
@@ -213,8 +213,9 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
     int32_t *link = reinterpret_cast<int32_t *>(coll + OWN_COLL); // OWN_COLL: previous in slot
     unsigned short *dtab = reinterpret_cast<unsigned short *>(osm);  // direct: P member tags
     uint32_t *lA = osm + o.dtab_words;                            // direct: losers (c'<<12|k)
-    uint32_t *lB = lA + OWN_LCAP;
-    int32_t *sid = reinterpret_cast<int32_t *>(osm + (o.direct ? o.dtab_words + 2 * OWN_LCAP
+    const int lcap = o.lcap > 0 ? o.lcap : OWN_LCAP;
+    uint32_t *lB = lA + lcap;
+    int32_t *sid = reinterpret_cast<int32_t *>(osm + (o.direct ? o.dtab_words + 2 * lcap
                                                                : HS + HS / 2 + 2 * OWN_COLL));
     uint32_t *T = reinterpret_cast<uint32_t *>(sid + ((o.m_cap + 3) & ~3));  // NIB*16 table
     uint32_t *BT = T + NIB * 16;                                  // 32*KW transposed bits
@@ -374,13 +375,13 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
                     if (w != k) {
                         clear_pair(k, w);
                         const int q = atomicAdd(&nlose, 1);
-                        if (q < OWN_LCAP) lA[q] = ((uint32_t)cx << 12) | (uint32_t)k;
+                        if (q < lcap) lA[q] = ((uint32_t)cx << 12) | (uint32_t)k;
                         else overflow = 2;
                     }
                 }
             }
             __syncthreads();
-            int nl = min(nlose, OWN_LCAP);
+            int nl = min(nlose, lcap);
             uint32_t *src = lA, *dst = lB;
             for (uint32_t level = 2; nl > 0; ++level) {
                 if (level >= 64) {  // a color shared by 64+ members of one bucket: dedupe path
@@ -1082,7 +1083,7 @@ int run_owned(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s) {
 }
 
 size_t owned_fr_smem(const OwnArgs &o, int kw) {
-    const size_t state = o.direct ? (size_t)o.dtab_words + 2 * OWN_LCAP
+    const size_t state = o.direct ? (size_t)o.dtab_words + 2 * (size_t)(o.lcap > 0 ? o.lcap : OWN_LCAP)
                                   : (size_t)o.hash_slots + o.hash_slots / 2 + 2 * OWN_COLL;
     const size_t lists = o.stage_lists ? (size_t)o.m_cap * o.L * (o.l16 ? 2 : 4) : 0;
     return (state + ((o.m_cap + 3) & ~3) + 8 * (size_t)kw * 16 + 32 * (size_t)kw + (size_t)o.m_cap * kw) * 4 +

@@ -100,6 +100,7 @@ struct OwnArgs {
     int32_t dtab_words;    // its size (>= P, multiple of 4)
     int32_t l16;           // members' lists staged as u16 (palette < 65536)
     int32_t stage_lists;   // stage the members' lists in shared memory (direct mode, or u16)
+    int32_t lcap;          // direct mode: losers per level (0: 1024)
 };
 
 struct RunArgs {
@@ -254,7 +255,7 @@ struct pcg_ctx {
     int fr_ichunk = 0;  // four-Russians i-chunk (0 auto)
     int merge_cap = 0;  // fill-merge buffer cap (0 auto; testing knob)
     int fill_algo = 0;  // owned masks: 0 auto (block fill up to 128K ids, else the bins fill
-                        // when the longest row fits its list, else segmented), 7 bins fill
+                        // when the longest row fits its list (16K ids), else segmented), 7 bins fill
                         // (counting sort per row), 5 block fill (CTA per row), 6 segmented fill (warp-decoded words,
                         // lane-segment harvest), 3 lane-per-bucket bitmap fill,
                         // 1 cooperative bitmap, 2 merge, 4 TMA-staged owned runs
@@ -320,6 +321,7 @@ struct pcg_ctx {
     bool h_fr5 = false;           // H holds the 5-bit-slice rows (k1_algo 3)
     int bins_threads = 0;  // bins fill: threads per CTA (0 = auto)
     int bins_shift = 0;    // bins fill: bin width exponent delta from auto (testing/tuning)
+    int bins_maxdeg = 0;   // bins fill: longest row it takes (0 = 16384)
     int k1_async = 0;                          // K1 on a side stream, result collected later
     bool k1_pending = false;
     cudaStream_t k1_stream = nullptr;

@@ -30,12 +30,15 @@ ap.add_argument("--blk-groups", type=int, default=0)
 ap.add_argument("--blk-ecap", type=int, default=0)
 ap.add_argument("--bins-threads", type=int, default=0)
 ap.add_argument("--bins-shift", type=int, default=0)
-ap.add_argument("--check", action="store_true", help="compare the CSR with fill_algo 3")
+ap.add_argument("--bins-maxdeg", type=int, default=0)
+ap.add_argument("--check", action="store_true", help="compare the CSR with the default fill")
+ap.add_argument("--pct", type=float, default=12.5)
+ap.add_argument("--alpha", type=float, default=2.0)
 a = ap.parse_args()
 
 t = time.time()
 v = b200.pauli_view(b200.PauliSet.from_strings(b200.random_pauli_strings(a.n, a.q, seed=0)))
-plan = b200.plan_iteration(1, a.n, b200.PaletteParams(12.5, 2.0, seed=0))
+plan = b200.plan_iteration(1, a.n, b200.PaletteParams(a.pct, a.alpha, seed=0))
 lists = b200.assign_random_lists(plan, v.active, 0)
 print(f"inputs {time.time()-t:.1f}s  P={plan.palette_size} L={plan.list_size}", flush=True)
 ctx = _native.context()
@@ -53,6 +56,7 @@ ctx.option("blk_groups", a.blk_groups)
 ctx.option("blk_ecap", a.blk_ecap)
 ctx.option("bins_threads", a.bins_threads)
 ctx.option("bins_shift", a.bins_shift)
+ctx.option("bins_maxdeg", a.bins_maxdeg)
 ctx.profiling(True)
 stage(v, lists, ctx)
 print("prep ms", ctx.kernel_times()[4])
