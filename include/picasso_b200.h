@@ -129,10 +129,24 @@ int pcg_set_profiling(pcg_ctx *ctx, int32_t on);
 /* The context's CUDA stream (cudaStream_t), so callers can time it with their own events. */
 void *pcg_stream(pcg_ctx *ctx);
 int pcg_kernel_times(pcg_ctx *ctx, float *ms, int32_t n);
-/* Kernel configuration knobs (testing/tuning): 0 = auto.
- *   "k1_algo": 1 = direct LOP3/POPC tiles, 2 = four-Russians smem tables
- *   "k2_mode": 1 = row pass gathers partner vectors, 2 = bucket commute masks
- *   "window": bitmap window of the row pass (ids), "fr_ichunk": rows per K1 work item */
+/* Kernel configuration knobs (testing/tuning; 0 = auto unless noted).  Every setting gives
+ * the same CSR; the defaults are the measured fastest.
+ *   K1 (commuting pairs):  "k1_algo" 1 direct LOP3/POPC tiles, 2 four-Russians 4-bit slices,
+ *                          3 four-Russians 5-bit slices; "k1_wide" 1 (default) 64-bit table
+ *                          entries; "fr_ichunk" rows per work item; "k1_async" 1 runs K1 on a
+ *                          side stream (pcg_k1_result collects it)
+ *   K2 (conflict rows):    "k2_mode" 1 partner gather, 2 bucket masks, 3 owned masks;
+ *                          "own_algo" 0 four-Russians / 1 per-pair masks; "own_direct" 0 forces
+ *                          the hash ownership table; "window" row-pass bitmap (ids)
+ *   fill:                  "fill_algo" 0 auto, 1 cooperative, 2 merge, 3 lane bitmap, 4 TMA
+ *                          runs, 5 block (CTA per row), 6 segmented, 7 bins (counting sort);
+ *                          "blk_threads" "blk_groups" "blk_dcap" "blk_ecap"; "bins_threads"
+ *                          "bins_shift" "bins_maxdeg"; "seg_bits" "seg_warps"; "merge_cap"
+ *   copy-out (pcg_fill):   "d2h_mode" 0 delta gaps (default) / 3 direct / 4 int32 widen;
+ *                          "d2h_pipe" 1 (default) fill in pieces overlapping the copy-out,
+ *                          "d2h_pieces", "d2h_chunk" (ids), "d2h_threads", "d2h_gap16"
+ *                          (1 16-bit, 2 8-bit gaps), "d2h_dma" (% of chunks as int64 DMA)
+ *   sharded:               "rows_out32" 1: pcg_fill_rows_device writes int32 ids */
 int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value);
 
 /*
