@@ -213,6 +213,7 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "d2h_mode")) ctx->d2h_mode = (int)value;
     else if (!strcmp(key, "k1_async")) ctx->k1_async = (int)value;
     else if (!strcmp(key, "k1_wide")) ctx->k1_wide = (int)value;
+    else if (!strcmp(key, "k1_early")) ctx->k1_early = (int)value;
     else if (!strcmp(key, "d2h_gap16")) ctx->d2h_gap16 = (int)value;
     else if (!strcmp(key, "d2h_pipe")) ctx->d2h_pipe = (int)value;
     else if (!strcmp(key, "d2h_pieces")) ctx->d2h_pieces = (int)value;
@@ -339,6 +340,50 @@ static BucketArgs bucket_args(const pcg_ctx *ctx) {
     return b;
 }
 
+static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, int *launches,
+                  cudaStream_t s, unsigned long long *anti);
+
+// four-Russians row offsets of the bit planes (the layout of the selected K1 kernel)
+static int fr_offsets(pcg_ctx *ctx, cudaStream_t s) {
+    if (!fr_supported(ctx->kw)) return PCG_OK;
+    PCG_ALLOC(ctx, ctx->H, (size_t)ctx->npad * ctx->kw * 4 * 4);
+    ctx->h_wide = fr_jb(ctx->kw, ctx->k1_wide) == K1_FR_JB2;
+    ctx->h_fr5 = ctx->k1_algo == 3 && (ctx->kw == 2 || ctx->kw == 4);
+    if (ctx->h_fr5) launch_fr_prep5(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
+    else if (ctx->h_wide) launch_fr_prep2(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
+    else launch_fr_prep(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
+    PCG_CHECK_LAUNCH(ctx);
+    return PCG_OK;
+}
+
+// K1 launched from the input prep, right after the bit planes exist (option "k1_early", with
+// "k1_async"): the commuting-pair sweep then overlaps the bucket sort and the owned masks as
+// well as the count and fill passes.  It accumulates into its own counter (scal[7]); the count
+// pass of the same build (one shard) takes it over instead of launching K1 again.
+static int k1_launch_early(pcg_ctx *ctx, cudaStream_t s) {
+    ctx->k1_early_valid = false;
+    if (!ctx->k1_async || !ctx->k1_early || ctx->n < 2) return PCG_OK;
+    if (!ctx->k1_stream) PCG_TRY_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->k1_stream, cudaStreamNonBlocking));
+    if (!ctx->k1_fork) PCG_TRY_CUDA(ctx, cudaEventCreateWithFlags(&ctx->k1_fork, cudaEventDisableTiming));
+    if (!ctx->k1_done) PCG_TRY_CUDA(ctx, cudaEventCreateWithFlags(&ctx->k1_done, cudaEventDisableTiming));
+    unsigned long long *anti = ctx->scal.as<unsigned long long>() + 7;
+    PCG_TRY_CUDA(ctx, cudaMemsetAsync(anti, 0, 8, s));
+    PCG_TRY_CUDA(ctx, cudaEventRecord(ctx->k1_fork, s));
+    cudaStream_t ks = ctx->k1_stream;
+    PCG_TRY_CUDA(ctx, cudaStreamWaitEvent(ks, ctx->k1_fork, 0));
+    if (ctx->prof) cudaEventRecord(ctx->ev[0], ks);
+    int64_t pairs = 0;
+    int l = 0;
+    int rc = run_k1(ctx, 0, 1, &pairs, &l, ks, anti);
+    if (rc) return rc;
+    ctx->launch_total += l;
+    if (ctx->prof) cudaEventRecord(ctx->ev[1], ks);
+    PCG_TRY_CUDA(ctx, cudaEventRecord(ctx->k1_done, ks));
+    ctx->k1_pending = true;
+    ctx->k1_early_valid = true;
+    return PCG_OK;
+}
+
 // PCG_TRACE_PREP=1: device timestamps between the prep stages, printed to stderr (diagnostic)
 struct PrepTrace {
     bool on = false;
@@ -384,6 +429,10 @@ static int prep_device(pcg_ctx *ctx) {
     PrepTrace tr(s);
     tr.mark("start");
     int rc = encode_vectors(ctx, false);
+    if (rc) return rc;
+    rc = fr_offsets(ctx, s);
+    if (rc) return rc;
+    rc = k1_launch_early(ctx, s);
     if (rc) return rc;
     PCG_ALLOC(ctx, ctx->lrel, (size_t)entries * 4);
     PCG_ALLOC(ctx, ctx->rowof, (size_t)entries * 4);
@@ -457,7 +506,14 @@ static int prep_device(pcg_ctx *ctx) {
     memcpy(&mask_total, hs + 16, 8);
     if (bad[1]) return fail(ctx, PCG_E_COLOR, "a list color lies outside the palette");
     if (bad[0]) {  // invalid 3-bit codes: exact raw-word predicate
+        if (ctx->k1_early_valid) {  // the early K1 read the wrong planes: drop it
+            PCG_TRY_CUDA(ctx, cudaEventSynchronize(ctx->k1_done));
+            ctx->k1_pending = false;
+            ctx->k1_early_valid = false;
+        }
         rc = encode_vectors(ctx, true);
+        if (rc) return rc;
+        rc = fr_offsets(ctx, s);
         if (rc) return rc;
     }
     // bucket masks when they fit comfortably (dense corners with huge buckets use the
@@ -590,17 +646,7 @@ static int prep_device(pcg_ctx *ctx) {
     }
 
     tr.mark("masks (K2a)");
-    // four-Russians row offsets
-    if (fr_supported(ctx->kw)) {
-        PCG_ALLOC(ctx, ctx->H, (size_t)ctx->npad * ctx->kw * 4 * 4);
-        ctx->h_wide = fr_jb(ctx->kw, ctx->k1_wide) == K1_FR_JB2;
-        ctx->h_fr5 = ctx->k1_algo == 3 && (ctx->kw == 2 || ctx->kw == 4);
-        if (ctx->h_fr5) launch_fr_prep5(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
-        else if (ctx->h_wide) launch_fr_prep2(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
-        else launch_fr_prep(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
-        PCG_CHECK_LAUNCH(ctx);
-    }
-    tr.mark("fr prep");
+    tr.mark("(end)");
     PCG_ALLOC(ctx, ctx->deg, (size_t)n_active * 4);
     PCG_ALLOC(ctx, ctx->degu, (size_t)n_active * 4);
     ctx->prep_launches = 6 + (bad[0] ? 1 : 0) + (ctx->masked ? 1 : 0) + (fr_supported(ctx->kw) ? 1 : 0);
@@ -620,6 +666,7 @@ extern "C" int pcg_set_inputs(pcg_ctx *ctx, const uint64_t *words, int64_t n_tot
     ctx->err.clear();
     if (ctx->k1_pending && ctx->k1_done) cudaEventSynchronize(ctx->k1_done);  // planes reused
     ctx->k1_pending = false;
+    ctx->k1_early_valid = false;
     ctx->staged = false;
     ctx->counted = false;
     if (n_active < 0 || n_total < 0 || n_active > n_total || num_qubits < 1 || nwords < 1 ||
@@ -730,8 +777,7 @@ static int64_t direct_pairs(int64_t n, int64_t T, int64_t t0, int64_t t1) {
 }
 
 static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, int *launches,
-                  cudaStream_t s) {
-    unsigned long long *anti = ctx->scal.as<unsigned long long>();
+                  cudaStream_t s, unsigned long long *anti) {
     const int64_t n = ctx->n;
     if (k1_algo(ctx) >= 2) {
         const bool fr5 = k1_algo(ctx) == 3;
@@ -829,7 +875,15 @@ static int count_impl(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t r0, 
         return fail(ctx, PCG_E_ARG, "bad shard or row range");
     PCG_TRY_CUDA(ctx, cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
-    k1_join(ctx);
+    // an early K1 of this build (launched by the prep, own counter) is taken over by a
+    // one-shard count; any other pending K1 is joined first
+    const bool take_early = ctx->k1_early_valid && ctx->k1_async && nshards == 1;
+    if (!take_early) {
+        k1_join(ctx);
+        if (ctx->k1_early_valid) {  // a sharded count: the early sweep is not used
+            ctx->k1_early_valid = false;
+        }
+    }
     pcg_counts c{};
     c.n_active = ctx->n;
     c.raw_words_mode = ctx->raw ? 1 : 0;
@@ -854,7 +908,7 @@ static int count_impl(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t r0, 
     // conflict-row passes and its count is collected later (pcg_k1_result)
     const bool async = ctx->k1_async && nshards == 1;
     cudaStream_t ks = s;
-    if (async) {
+    if (async && !take_early) {
         if (!ctx->k1_stream) PCG_TRY_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->k1_stream, cudaStreamNonBlocking));
         if (!ctx->k1_fork) PCG_TRY_CUDA(ctx, cudaEventCreateWithFlags(&ctx->k1_fork, cudaEventDisableTiming));
         if (!ctx->k1_done) PCG_TRY_CUDA(ctx, cudaEventCreateWithFlags(&ctx->k1_done, cudaEventDisableTiming));
@@ -862,13 +916,19 @@ static int count_impl(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t r0, 
         PCG_TRY_CUDA(ctx, cudaEventRecord(ctx->k1_fork, s));
         PCG_TRY_CUDA(ctx, cudaStreamWaitEvent(ks, ctx->k1_fork, 0));
     }
-    if (ctx->prof) cudaEventRecord(ctx->ev[0], ks);
-    rc = run_k1(ctx, shard, nshards, &pairs, launches, ks);
-    if (rc) return rc;
-    if (ctx->prof) cudaEventRecord(ctx->ev[1], ks);
-    if (async) {
-        PCG_TRY_CUDA(ctx, cudaEventRecord(ctx->k1_done, ks));
-        ctx->k1_pending = true;
+    if (take_early) {
+        pairs = ctx->n * (ctx->n - 1) / 2;  // the whole triangle, already being swept
+        ctx->k1_slot = 7;
+    } else {
+        if (ctx->prof) cudaEventRecord(ctx->ev[0], ks);
+        rc = run_k1(ctx, shard, nshards, &pairs, launches, ks, ctx->scal.as<unsigned long long>());
+        if (rc) return rc;
+        if (ctx->prof) cudaEventRecord(ctx->ev[1], ks);
+        ctx->k1_slot = 0;
+        if (async) {
+            PCG_TRY_CUDA(ctx, cudaEventRecord(ctx->k1_done, ks));
+            ctx->k1_pending = true;
+        }
     }
     if (ctx->prof) cudaEventRecord(ctx->ev[8], s);
     const RowArgs a = row_args(ctx, r0, r1);
@@ -1896,7 +1956,8 @@ extern "C" int pcg_k1_result(pcg_ctx *ctx, int64_t *anticommuting) {
         unsigned long long a = 0;
         unsigned char *hs = pinned_scratch(ctx);
         if (!hs) return fail(ctx, PCG_E_OOM, "pinned scratch allocation failed");
-        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(hs + 128, ctx->scal.p, 8, cudaMemcpyDeviceToHost, ctx->k1_stream));
+        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(hs + 128, ctx->scal.as<unsigned long long>() + ctx->k1_slot, 8,
+                                          cudaMemcpyDeviceToHost, ctx->k1_stream));
         PCG_TRY_CUDA(ctx, cudaStreamSynchronize(ctx->k1_stream));
         memcpy(&a, hs + 128, 8);
         if (ctx->prof) cudaEventElapsedTime(&ctx->ktimes[0], ctx->ev[0], ctx->ev[1]);
@@ -2083,6 +2144,7 @@ extern "C" int pcg_validate(pcg_ctx *ctx, const uint64_t *words, int64_t n_total
     ctx->err.clear();
     if (ctx->k1_pending && ctx->k1_done) cudaEventSynchronize(ctx->k1_done);
     ctx->k1_pending = false;
+    ctx->k1_early_valid = false;
     ctx->staged = false;  // the validator reuses the build's staging buffers
     ctx->counted = false;
     if (n_active < 0 || n_total < 0 || n_active > n_total || num_qubits < 1 || nwords < 1 ||
@@ -2134,7 +2196,7 @@ extern "C" int pcg_validate(pcg_ctx *ctx, const uint64_t *words, int64_t n_total
     PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->scal.p, 0, 64, s));
     int64_t pairs = 0;
     int launches = 0;
-    rc = run_k1(ctx, 0, 1, &pairs, &launches, s);
+    rc = run_k1(ctx, 0, 1, &pairs, &launches, s, ctx->scal.as<unsigned long long>());
     if (rc) return rc;
     // color classes: stable sort of (color, local index)
     const int64_t n = n_active;

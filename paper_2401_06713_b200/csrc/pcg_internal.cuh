@@ -319,6 +319,9 @@ struct pcg_ctx {
     int64_t launch_total = 0;     // kernels launched by this context (pcg_launch_total)
     int rows_out32 = 0;           // pcg_fill_rows_device writes int32 ids (sharded exchange)
     bool h_fr5 = false;           // H holds the 5-bit-slice rows (k1_algo 3)
+    int k1_early = 1;             // with k1_async: launch K1 from the prep (k1_launch_early)
+    bool k1_early_valid = false;  // an early K1 of the staged build is in flight (scal[7])
+    int k1_slot = 0;              // scal word pcg_k1_result reads (0, or 7 for the early K1)
     int bins_threads = 0;  // bins fill: threads per CTA (0 = auto)
     int bins_shift = 0;    // bins fill: bin width exponent delta from auto (testing/tuning)
     int bins_maxdeg = 0;   // bins fill: longest row it takes (0 = 16384)

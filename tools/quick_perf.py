@@ -31,6 +31,8 @@ ap.add_argument("--blk-ecap", type=int, default=0)
 ap.add_argument("--bins-threads", type=int, default=0)
 ap.add_argument("--bins-shift", type=int, default=0)
 ap.add_argument("--bins-maxdeg", type=int, default=0)
+ap.add_argument("--async", dest="k1_async", type=int, default=0)
+ap.add_argument("--early", type=int, default=1)
 ap.add_argument("--check", action="store_true", help="compare the CSR with the default fill")
 ap.add_argument("--pct", type=float, default=12.5)
 ap.add_argument("--alpha", type=float, default=2.0)
@@ -57,6 +59,8 @@ ctx.option("blk_ecap", a.blk_ecap)
 ctx.option("bins_threads", a.bins_threads)
 ctx.option("bins_shift", a.bins_shift)
 ctx.option("bins_maxdeg", a.bins_maxdeg)
+ctx.option("k1_async", a.k1_async)
+ctx.option("k1_early", a.early)
 ctx.profiling(True)
 stage(v, lists, ctx)
 print("prep ms", ctx.kernel_times()[4])
