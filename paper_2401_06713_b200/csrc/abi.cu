@@ -375,8 +375,7 @@ static int k1_launch_early(pcg_ctx *ctx, cudaStream_t s) {
     int64_t pairs = 0;
     int l = 0;
     int rc = run_k1(ctx, 0, 1, &pairs, &l, ks, anti);
-    if (rc) return rc;
-    ctx->launch_total += l;
+    if (rc) return rc;  // (counted in prep_launches)
     if (ctx->prof) cudaEventRecord(ctx->ev[1], ks);
     PCG_TRY_CUDA(ctx, cudaEventRecord(ctx->k1_done, ks));
     ctx->k1_pending = true;
@@ -649,7 +648,8 @@ static int prep_device(pcg_ctx *ctx) {
     tr.mark("(end)");
     PCG_ALLOC(ctx, ctx->deg, (size_t)n_active * 4);
     PCG_ALLOC(ctx, ctx->degu, (size_t)n_active * 4);
-    ctx->prep_launches = 6 + (bad[0] ? 1 : 0) + (ctx->masked ? 1 : 0) + (fr_supported(ctx->kw) ? 1 : 0);
+    ctx->prep_launches = 6 + (bad[0] ? 1 : 0) + (ctx->masked ? 1 : 0) + (fr_supported(ctx->kw) ? 1 : 0) +
+                         (ctx->k1_early_valid ? 1 : 0);  // + the early K1 sweep
     if (ctx->prof) {
         cudaEventRecord(ctx->ev[11], s);
         ctx->prep_timed = true;  // elapsed time read at the next host sync (count pass)
