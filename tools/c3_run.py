@@ -20,3 +20,12 @@ print(f"c3 whole run: {wall:.1f} s, {len(res.iterations)} iterations, {len(set(c
 for r in res.iterations:
     d = r.__dict__ if hasattr(r, "__dict__") else r._asdict()
     print({k: (round(v, 3) if isinstance(v, float) else v) for k, v in d.items()})
+
+# exhaustive properness check of the coloring on the GPU (the reference's validator stops at
+# 20,000 vertices): every commuting pair with equal colors is a violation
+from paper_2401_06713_b200.validation import validate
+
+t0 = time.time()
+rep = validate(view, res, "exhaustive")
+print(f"validate (exhaustive, GPU): proper={rep.proper} violations={rep.violation_count} "
+      f"colors={rep.colors_used} |E|={rep.oracle_edges} in {time.time() - t0:.2f} s", flush=True)
