@@ -132,7 +132,8 @@ int pcg_kernel_times(pcg_ctx *ctx, float *ms, int32_t n);
 /* Kernel configuration knobs (testing/tuning; 0 = auto unless noted).  Every setting gives
  * the same CSR; the defaults are the measured fastest.
  *   K1 (commuting pairs):  "k1_algo" 1 direct LOP3/POPC tiles, 2 four-Russians 4-bit slices,
- *                          3 four-Russians 5-bit slices; "k1_wide" 1 (default) 64-bit table
+ *                          4 four-Russians 6-bit slices (default for q <= 64); "k1_wide" 1
+ *                          (default) 64-bit 4-bit-slice table
  *                          entries; "fr_ichunk" rows per work item; "k1_async" 1 runs K1 on a
  *                          side stream (pcg_k1_result collects it)
  *   K2 (conflict rows):    "k2_mode" 1 partner gather, 2 bucket masks, 3 owned masks;

@@ -38,8 +38,9 @@ def _load():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(
-        os.path.join(_HERE, "conflict_oracle.c")
+    srcs = ("conflict_oracle.c", "bucket_oracle.c")
+    if not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < max(
+        os.path.getmtime(os.path.join(_HERE, s)) for s in srcs
     ):
         build_library()
     lib = ctypes.CDLL(_LIB_PATH)

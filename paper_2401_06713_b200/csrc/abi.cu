@@ -344,13 +344,15 @@ static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, 
                   cudaStream_t s, unsigned long long *anti);
 
 // four-Russians row offsets of the bit planes (the layout of the selected K1 kernel)
+static bool fr6_supported(int32_t kw) { return kw == 2 || kw == 4; }
+
 static int fr_offsets(pcg_ctx *ctx, cudaStream_t s) {
     if (!fr_supported(ctx->kw)) return PCG_OK;
+    // the 6-bit kernel (the default for kw 2/4) reads the bit planes directly
+    if (fr6_supported(ctx->kw) && (ctx->k1_algo == 0 || ctx->k1_algo == 4)) return PCG_OK;
     PCG_ALLOC(ctx, ctx->H, (size_t)ctx->npad * ctx->kw * 4 * 4);
     ctx->h_wide = fr_jb(ctx->kw, ctx->k1_wide) == K1_FR_JB2;
-    ctx->h_fr5 = ctx->k1_algo == 3 && (ctx->kw == 2 || ctx->kw == 4);
-    if (ctx->h_fr5) launch_fr_prep5(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
-    else if (ctx->h_wide) launch_fr_prep2(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
+    if (ctx->h_wide) launch_fr_prep2(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
     else launch_fr_prep(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
     PCG_CHECK_LAUNCH(ctx);
     return PCG_OK;
@@ -737,10 +739,12 @@ extern "C" int pcg_set_inputs(pcg_ctx *ctx, const uint64_t *words, int64_t n_tot
 // --------------------------------------------------------------------------------------
 // count pass
 // --------------------------------------------------------------------------------------
+// 1 direct tiles, 2 four-Russians 4-bit slices, 4 6-bit slices (the default where
+// supported: kw 2/4; k1_algo 3, 5-bit slices, was measured slower and removed)
 static int k1_algo(const pcg_ctx *ctx) {
     if (ctx->k1_algo == 1) return 1;
-    if (ctx->k1_algo == 3 && ctx->h_fr5) return 3;
     if (ctx->k1_algo == 2 && fr_supported(ctx->kw)) return 2;
+    if (fr6_supported(ctx->kw)) return 4;
     return fr_supported(ctx->kw) ? 2 : 1;
 }
 
@@ -780,8 +784,8 @@ static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, 
                   cudaStream_t s, unsigned long long *anti) {
     const int64_t n = ctx->n;
     if (k1_algo(ctx) >= 2) {
-        const bool fr5 = k1_algo(ctx) == 3;
-        const int64_t JB = (ctx->h_wide && !fr5) ? K1_FR_JB2 : K1_FR_JB;
+        const bool fr6 = k1_algo(ctx) == 4;
+        const int64_t JB = (ctx->h_wide && !fr6) ? K1_FR_JB2 : K1_FR_JB;
         const int64_t njb = ctx->npad / JB, ic = fr_ichunk(ctx);
         std::vector<int64_t> start(njb + 1, 0);
         for (int64_t jb = 0; jb < njb; ++jb) {
@@ -806,8 +810,8 @@ static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, 
         PCG_ALLOC(ctx, ctx->items, (size_t)(njb + 1) * 8);
         PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->items.p, start.data(), (size_t)(njb + 1) * 8,
                                           cudaMemcpyHostToDevice, s));
-        if (fr5)
-            *launches += launch_commute_fr5_items(ctx->B.as<uint32_t>(), ctx->H.as<uint32_t>(),
+        if (fr6)
+            *launches += launch_commute_fr6_items(ctx->A.as<uint32_t>(), ctx->B.as<uint32_t>(),
                                                   ctx->kw, n, ctx->items.as<int64_t>(), njb,
                                                   (int32_t)ic, i0, i1, anti, ctx->sms, s);
         else if (ctx->h_wide)
@@ -2184,15 +2188,8 @@ extern "C" int pcg_validate(pcg_ctx *ctx, const uint64_t *words, int64_t n_total
         if (rc) return rc;
     }
     // |E|: the commuting-pair sweep (K1)
-    if (fr_supported(ctx->kw)) {
-        PCG_ALLOC(ctx, ctx->H, (size_t)ctx->npad * ctx->kw * 4 * 4);
-        ctx->h_wide = fr_jb(ctx->kw, ctx->k1_wide) == K1_FR_JB2;
-        ctx->h_fr5 = ctx->k1_algo == 3 && (ctx->kw == 2 || ctx->kw == 4);
-        if (ctx->h_fr5) launch_fr_prep5(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
-        else if (ctx->h_wide) launch_fr_prep2(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
-        else launch_fr_prep(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
-        PCG_CHECK_LAUNCH(ctx);
-    }
+    rc = fr_offsets(ctx, s);
+    if (rc) return rc;
     PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->scal.p, 0, 64, s));
     int64_t pairs = 0;
     int launches = 0;

@@ -291,154 +291,6 @@ __global__ void k_fr_prep2(const uint32_t *__restrict__ A, int64_t npad, uint32_
     }
 }
 
-// ---------------------------------------------------------------------------------------
-// Four-Russians with 5-bit slices (k1_algo 3): 32-entry tables per slice, so a row costs
-// ceil(K/5) table lookups per 32 partners instead of K/4 (26 instead of 32 at q = 64): fewer
-// shared-memory bytes per pair, the bound of the 4-bit kernels.  Layout as k_commute_fr:
-// entry (slice g, value v, lane t) at word ((g>>1)*32 + v)*64 + (g&1)*32 + t, so a lookup
-// address is one PRMT of the row's 16-bit table row h = (g>>1)*32 + v_g with the lane offset.
-// ---------------------------------------------------------------------------------------
-template <int KW>
-__global__ void k_fr_prep5(const uint32_t *__restrict__ A, int64_t npad, uint32_t *__restrict__ H) {
-    constexpr int K = 32 * KW, NG = (K + 4) / 5, NP = (NG + 1) / 2;
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= npad) return;
-    const uint32_t *a = A + i * KW;
-    uint32_t w[KW + 1];
-#pragma unroll
-    for (int k = 0; k < KW; ++k) w[k] = a[k];
-    w[KW] = 0u;
-    uint32_t *h = H + i * (KW * 4);
-#pragma unroll
-    for (int m = 0; m < NP; ++m) {
-        uint32_t hv[2];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int g = 2 * m + q, b = 5 * g;  // bits [b, b+5) of A_i (zero past K)
-            uint32_t v = 0u;
-            if (g < NG) {
-                const uint64_t win = ((uint64_t)w[(b >> 5) + 1] << 32) | w[b >> 5];
-                v = (uint32_t)(win >> (b & 31)) & 31u;
-            }
-            hv[q] = (uint32_t)m * 32u + v;
-        }
-        h[m] = hv[0] | (hv[1] << 16);
-    }
-}
-
-template <int KW>
-__global__ void __launch_bounds__(FR_WARPS * 32) k_commute_fr5(
-    const uint32_t *__restrict__ B, const uint32_t *__restrict__ H, int64_t n,
-    const int64_t *__restrict__ item_start, int64_t njb, int32_t ichunk, int64_t item0,
-    int64_t item1, unsigned long long *__restrict__ anti) {
-    constexpr int K = 32 * KW;
-    constexpr int NG = (K + 4) / 5, NP = (NG + 1) / 2;  // 5-bit slices, slice pairs
-    constexpr int TBL_WORDS = NP * 32 * 64;
-    constexpr int BT_STRIDE = K + 1;
-    extern __shared__ __align__(16) uint32_t smem[];
-    uint32_t *tbl = smem;
-    uint32_t *bt = smem + TBL_WORDS;  // 32 * BT_STRIDE
-    __shared__ unsigned long long red[FR_WARPS];
-
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t lb0 = (uint32_t)lane * 4u, lb1 = 128u + (uint32_t)lane * 4u;
-    const char *tb = reinterpret_cast<const char *>(tbl);
-
-    const int64_t nitems = item1 - item0;
-    const int64_t my0 = item0 + nitems * blockIdx.x / gridDim.x;
-    const int64_t my1 = item0 + nitems * (blockIdx.x + 1) / gridDim.x;
-    int64_t cur_jb = -1;
-    unsigned long long local = 0;
-
-    for (int64_t it = my0; it < my1; ++it) {
-        int64_t lo = 0, hi = njb;
-        while (hi - lo > 1) {
-            const int64_t mid = (lo + hi) >> 1;
-            if (item_start[mid] <= it) lo = mid; else hi = mid;
-        }
-        const int64_t jb = lo, ic = it - item_start[jb];
-        if (jb != cur_jb) {
-            __syncthreads();
-            // phase A: transpose the 1024 partner vectors into bit rows bt[t][k]
-            for (int t = warp; t < 32; t += FR_WARPS) {
-                const uint32_t *bj = B + (jb * K1_FR_JB + 32 * t + lane) * KW;
-                uint32_t v[KW];
-#pragma unroll
-                for (int k = 0; k < KW; ++k) v[k] = __ldg(bj + k);
-#pragma unroll
-                for (int k = 0; k < KW; ++k) {
-                    uint32_t mine = 0;
-#pragma unroll
-                    for (int s = 0; s < 32; ++s) {
-                        const uint32_t word = __ballot_sync(0xffffffffu, (v[k] >> s) & 1u);
-                        if (lane == s) mine = word;
-                    }
-                    bt[t * BT_STRIDE + 32 * k + lane] = mine;
-                }
-            }
-            __syncthreads();
-            // phase B: the 32 XOR combinations of each slice's 5 bit rows (doubling)
-            for (int g = warp; g < NG; g += FR_WARPS) {
-                const uint32_t *row = bt + lane * BT_STRIDE;
-                uint32_t e[32];
-                e[0] = 0u;
-#pragma unroll
-                for (int b = 0; b < 5; ++b) {
-                    const int k = 5 * g + b;
-                    const uint32_t rb = k < K ? row[k] : 0u;
-#pragma unroll
-                    for (int v = 0; v < (1 << b); ++v) e[v | (1 << b)] = e[v] ^ rb;
-                }
-                uint32_t *dst = tbl + (g >> 1) * 32 * 64 + (g & 1) * 32 + lane;
-#pragma unroll
-                for (int v = 0; v < 32; ++v) dst[v * 64] = e[v];
-            }
-            if (NG & 1) {  // the unused odd slice of the last pair: value 0 -> entry 0
-                for (int x = threadIdx.x; x < 32; x += blockDim.x)
-                    tbl[(NP - 1) * 32 * 64 + 32 + x] = 0u;
-            }
-            __syncthreads();
-            cur_jb = jb;
-        }
-        const int64_t jlast = min(n, (jb + 1) * (int64_t)K1_FR_JB);
-        const int64_t i0 = ic * ichunk;
-        const int64_t i1 = min(i0 + ichunk, jlast);
-        const int64_t jbase = jb * K1_FR_JB + 32 * lane;
-        for (int64_t i = i0 + warp; i < i1; i += FR_WARPS) {
-            const uint4 *hp = reinterpret_cast<const uint4 *>(H + i * (KW * 4));
-            uint32_t acc = 0;
-#pragma unroll
-            for (int q = 0; q < (NP + 3) / 4; ++q) {
-                const uint4 hv = __ldg(hp + q);
-                const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
-#pragma unroll
-                for (int m = 0; m < 4; ++m) {
-                    if (4 * q + m < NP) {
-                        const uint32_t ad0 = __byte_perm(hw[m], lb0, 0x5104);
-                        const uint32_t ad1 = __byte_perm(hw[m], lb1, 0x5324);
-                        acc ^= *reinterpret_cast<const uint32_t *>(tb + ad0) ^
-                               *reinterpret_cast<const uint32_t *>(tb + ad1);
-                    }
-                }
-            }
-            uint32_t mask;
-            const int64_t d = i - jbase;
-            if (d < 0) mask = 0xffffffffu;
-            else if (d >= 31) mask = 0u;
-            else mask = ~((2u << d) - 1u);
-            local += __popc(acc & mask);
-        }
-    }
-    for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
-    if (lane == 0) red[warp] = local;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long sacc = 0;
-        for (int w = 0; w < FR_WARPS; ++w) sacc += red[w];
-        if (sacc) atomicAdd(anti, sacc);
-    }
-}
-
 template <int KW>
 __global__ void __launch_bounds__(FR_WARPS * 32) k_commute_fr2(
     const uint32_t *__restrict__ B, const uint32_t *__restrict__ H, int64_t n,
@@ -552,6 +404,139 @@ __global__ void __launch_bounds__(FR_WARPS * 32) k_commute_fr2(
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Four-Russians with 6-bit slices (the default for kw 2/4, q <= 64).  The bound of the
+// 4-bit kernels is shared-memory bytes per pair: one 8-byte entry per 4-bit slice per 64
+// partners = K/32 bytes per pair (4 B at q = 64).  6-bit slices need ceil(K/6) lookups
+// instead of K/4 (22 instead of 32 at q = 64: 2.75 B per pair), but a 64-entry table per
+// slice is 4x the 16-entry one, so the j-block shrinks to 1024 partners (16 lanes x 64)
+// and each half-warp runs its own row: a half-warp reads 16 consecutive 8-byte entries =
+// exactly one 128-byte wavefront, still conflict-free.  Tables: ceil(K/6) x 64 entries x
+// 128 B = 176 KB at K = 128, plus 16.5 KB for the transposed block; one CTA per SM.
+//
+// Entry (slice g, value v, half-lane l) at byte g*8192 + v*128 + 8*l: word 0 = the 32
+// partners 64l..64l+31, word 1 = 64l+32..64l+63.  The table base is aligned to 8 KB, so a
+// lookup address is  base_l | ((A_i >> 6g) & 63) << 7  — one funnel shift and one LOP3
+// straight from the row's bits (no per-row offset array), with g*8192 as the immediate.
+// ---------------------------------------------------------------------------------------
+template <int KW>
+__global__ void __launch_bounds__(FR_WARPS * 32, 1) k_commute_fr6(
+    const uint32_t *__restrict__ A, const uint32_t *__restrict__ B, int64_t n,
+    const int64_t *__restrict__ item_start, int64_t njb, int32_t ichunk, int64_t item0,
+    int64_t item1, unsigned long long *__restrict__ anti) {
+    constexpr int K = 32 * KW;           // bits per vector
+    constexpr int NG = (K + 5) / 6;      // 6-bit slices (the last one narrower)
+    constexpr int JB = K1_FR_JB;         // 1024 partners
+    constexpr int BT_STRIDE = K + 1;
+    extern __shared__ __align__(16) uint32_t smem[];
+    __shared__ unsigned long long red[FR_WARPS];
+    const uint32_t smem_s = (uint32_t)__cvta_generic_to_shared(smem);
+    const uint32_t tbl_s = (smem_s + 8191u) & ~8191u;  // 8 KB aligned table base
+    char *tbl = reinterpret_cast<char *>(smem) + (tbl_s - smem_s);
+    uint32_t *bt = reinterpret_cast<uint32_t *>(tbl + NG * 8192);  // 32 x BT_STRIDE
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int half = lane >> 4, hl = lane & 15;
+    const uint32_t base_l = tbl_s + (uint32_t)hl * 8u;
+
+    const int64_t nitems = item1 - item0;
+    const int64_t my0 = item0 + nitems * blockIdx.x / gridDim.x;
+    const int64_t my1 = item0 + nitems * (blockIdx.x + 1) / gridDim.x;
+    int64_t cur_jb = -1;
+    unsigned long long local = 0;
+
+    for (int64_t it = my0; it < my1; ++it) {
+        int64_t lo = 0, hi = njb;
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (item_start[mid] <= it) lo = mid; else hi = mid;
+        }
+        const int64_t jb = lo, ic = it - item_start[jb];
+        if (jb != cur_jb) {
+            __syncthreads();  // previous tables no longer in use
+            // phase A: transpose the 1024 partner vectors into bit rows bt[t][k], t = 32-group
+            for (int t = warp; t < 32; t += FR_WARPS) {
+                const uint32_t *bj = B + (jb * JB + 32 * t + lane) * KW;
+                uint32_t v[KW];
+#pragma unroll
+                for (int k = 0; k < KW; ++k) v[k] = __ldg(bj + k);
+#pragma unroll
+                for (int k = 0; k < KW; ++k) {
+                    uint32_t mine = 0;
+#pragma unroll
+                    for (int s = 0; s < 32; ++s) {
+                        const uint32_t word = __ballot_sync(0xffffffffu, (v[k] >> s) & 1u);
+                        if (lane == s) mine = word;
+                    }
+                    bt[t * BT_STRIDE + 32 * k + lane] = mine;
+                }
+            }
+            __syncthreads();
+            // phase B: the 64 XOR combinations of each slice's 6 bit rows; warp g-slice, lane
+            // t = 32-partner group (entry word (t & 1) of half-lane t >> 1)
+            for (int g = warp; g < NG; g += FR_WARPS) {
+                const uint32_t *row = bt + lane * BT_STRIDE + 6 * g;
+                uint32_t r[6];
+#pragma unroll
+                for (int b = 0; b < 6; ++b) r[b] = (6 * g + b < K) ? row[b] : 0u;
+                uint32_t *dst = reinterpret_cast<uint32_t *>(tbl + g * 8192) + lane;
+#pragma unroll 8
+                for (int v = 0; v < 64; ++v) {
+                    uint32_t e = 0;
+#pragma unroll
+                    for (int b = 0; b < 6; ++b) e ^= (v >> b & 1) ? r[b] : 0u;
+                    dst[v * 32] = e;
+                }
+            }
+            __syncthreads();
+            cur_jb = jb;
+        }
+        const int64_t jlast = min(n, (jb + 1) * (int64_t)JB);  // exclusive
+        const int64_t i0 = ic * ichunk;
+        const int64_t i1 = min(i0 + ichunk, jlast);
+        const int64_t jbase = jb * JB + 64 * hl;
+        for (int64_t i = i0 + 2 * warp + half; i < i1; i += 2 * FR_WARPS) {
+            uint32_t a[KW + 1];
+            if constexpr (KW == 4) {
+                const uint4 av = __ldg(reinterpret_cast<const uint4 *>(A + i * 4));
+                a[0] = av.x; a[1] = av.y; a[2] = av.z; a[3] = av.w;
+            } else {
+                const uint2 av = __ldg(reinterpret_cast<const uint2 *>(A + i * 2));
+                a[0] = av.x; a[1] = av.y;
+            }
+            a[KW] = 0u;
+            uint32_t acc0 = 0, acc1 = 0;
+#pragma unroll
+            for (int g = 0; g < NG; ++g) {
+                const int o = 6 * g, w = o >> 5, sh = o & 31;
+                // bits o..o+5 of the row, already shifted to bit 7 (the entry stride)
+                uint32_t x;
+                if (sh + 6 <= 32) x = sh >= 7 ? (a[w] >> (sh - 7)) : (a[w] << (7 - sh));
+                else x = __funnelshift_r(a[w], a[w + 1], sh) << 7;
+                const uint32_t ad = (x & 0x1f80u) | base_l;
+                uint32_t e0, e1;
+                asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];"
+                             : "=r"(e0), "=r"(e1) : "r"(ad + (uint32_t)(g * 8192)));
+                acc0 ^= e0;
+                acc1 ^= e1;
+            }
+            // partners j = jbase + s (word 0) and jbase + 32 + s (word 1) with j > i
+            const int64_t d0 = i - jbase, d1 = d0 - 32;
+            const uint32_t m0 = d0 < 0 ? 0xffffffffu : (d0 >= 31 ? 0u : ~((2u << d0) - 1u));
+            const uint32_t m1 = d1 < 0 ? 0xffffffffu : (d1 >= 31 ? 0u : ~((2u << d1) - 1u));
+            local += __popc(acc0 & m0) + __popc(acc1 & m1);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
+    if (lane == 0) red[warp] = local;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long s = 0;
+        for (int w = 0; w < FR_WARPS; ++w) s += red[w];
+        if (s) atomicAdd(anti, s);
+    }
+}
+
 template <typename K>
 int occupancy_grid(K kernel, int threads, size_t smem, int sms, int64_t work) {
     int per_sm = 0;
@@ -593,19 +578,19 @@ int run_fr2(const uint32_t *B, const uint32_t *H, int64_t n, const int64_t *item
 }
 
 template <int KW>
-size_t fr5_smem() {
-    constexpr int K = 32 * KW, NG = (K + 4) / 5, NP = (NG + 1) / 2;
-    return (size_t)NP * 32 * 64 * 4 + (size_t)32 * (K + 1) * 4;
+size_t fr6_smem() {
+    constexpr int K = 32 * KW, NG = (K + 5) / 6;
+    return 8192 + (size_t)NG * 8192 + (size_t)32 * (K + 1) * 4;  // + alignment slack
 }
 
 template <int KW>
-int run_fr5(const uint32_t *B, const uint32_t *H, int64_t n, const int64_t *item_start,
+int run_fr6(const uint32_t *A, const uint32_t *B, int64_t n, const int64_t *item_start,
             int64_t njb, int32_t ichunk, int64_t item0, int64_t item1,
             unsigned long long *anti, int sms, cudaStream_t s) {
-    const size_t smem = fr5_smem<KW>();
-    allow_max_smem(k_commute_fr5<KW>);
-    const int grid = occupancy_grid(k_commute_fr5<KW>, FR_WARPS * 32, smem, sms, item1 - item0);
-    k_commute_fr5<KW><<<grid, FR_WARPS * 32, smem, s>>>(B, H, n, item_start, njb, ichunk, item0,
+    const size_t smem = fr6_smem<KW>();
+    allow_max_smem(k_commute_fr6<KW>);
+    const int grid = occupancy_grid(k_commute_fr6<KW>, FR_WARPS * 32, smem, sms, item1 - item0);
+    k_commute_fr6<KW><<<grid, FR_WARPS * 32, smem, s>>>(A, B, n, item_start, njb, ichunk, item0,
                                                        item1, anti);
     return 1;
 }
@@ -648,24 +633,14 @@ bool fr_supported(int32_t kw) { return kw == 2 || kw == 4 || kw == 6 || kw == 8;
 
 int fr_jb(int32_t kw, int wide) { return (wide && (kw == 2 || kw == 4)) ? K1_FR_JB2 : K1_FR_JB; }
 
-int launch_fr_prep5(const uint32_t *A, int32_t kw, int64_t npad, uint32_t *H, cudaStream_t s) {
-    const int tb = 256;
-    const unsigned grid = (unsigned)((npad + tb - 1) / tb);
-    switch (kw) {
-        case 2: k_fr_prep5<2><<<grid, tb, 0, s>>>(A, npad, H); return 1;
-        case 4: k_fr_prep5<4><<<grid, tb, 0, s>>>(A, npad, H); return 1;
-        default: return 0;
-    }
-}
-
-int launch_commute_fr5_items(const uint32_t *B, const uint32_t *H, int32_t kw, int64_t n,
+int launch_commute_fr6_items(const uint32_t *A, const uint32_t *B, int32_t kw, int64_t n,
                              const int64_t *item_start, int64_t njb, int32_t ichunk,
                              int64_t item0, int64_t item1, unsigned long long *anti, int sms,
                              cudaStream_t s) {
     if (item1 <= item0) return 0;
     switch (kw) {
-        case 2: return run_fr5<2>(B, H, n, item_start, njb, ichunk, item0, item1, anti, sms, s);
-        case 4: return run_fr5<4>(B, H, n, item_start, njb, ichunk, item0, item1, anti, sms, s);
+        case 2: return run_fr6<2>(A, B, n, item_start, njb, ichunk, item0, item1, anti, sms, s);
+        case 4: return run_fr6<4>(A, B, n, item_start, njb, ichunk, item0, item1, anti, sms, s);
         default: return 0;
     }
 }

@@ -185,8 +185,7 @@ int launch_commute_fr_items(const uint32_t *B, const uint32_t *H, int32_t kw, in
                             cudaStream_t s);
 int launch_fr_prep(const uint32_t *A, int32_t kw, int64_t npad, uint32_t *H, cudaStream_t s);
 int fr_jb(int32_t kw, int wide);
-int launch_fr_prep5(const uint32_t *A, int32_t kw, int64_t npad, uint32_t *H, cudaStream_t s);
-int launch_commute_fr5_items(const uint32_t *B, const uint32_t *H, int32_t kw, int64_t n,
+int launch_commute_fr6_items(const uint32_t *A, const uint32_t *B, int32_t kw, int64_t n,
                              const int64_t *item_start, int64_t njb, int32_t ichunk,
                              int64_t item0, int64_t item1, unsigned long long *anti, int sms,
                              cudaStream_t s);
@@ -318,7 +317,6 @@ struct pcg_ctx {
     unsigned char *hs = nullptr;  // pinned scratch for the small per-build readbacks (512 B)
     int64_t launch_total = 0;     // kernels launched by this context (pcg_launch_total)
     int rows_out32 = 0;           // pcg_fill_rows_device writes int32 ids (sharded exchange)
-    bool h_fr5 = false;           // H holds the 5-bit-slice rows (k1_algo 3)
     int k1_early = 1;             // with k1_async: launch K1 from the prep (k1_launch_early)
     bool k1_early_valid = false;  // an early K1 of the staged build is in flight (scal[7])
     int k1_slot = 0;              // scal word pcg_k1_result reads (0, or 7 for the early K1)
