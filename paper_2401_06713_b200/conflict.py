@@ -9,7 +9,9 @@ has the reference's signature, inputs, outputs and errors
   * output   ConflictGraph(members, ExplicitGraph(n_c, offsets, neighbors), edge_count,
              view_edges_scanned) — int64 arrays, canonical CSR (members ascending, rows
              strictly ascending compact ids), bit-identical to the reference;
-  * errors   EdgeBudgetExceededError(projected, budget) before any output is allocated.
+  * errors   EdgeBudgetExceededError(projected, budget) before any output is allocated —
+             the caller's own class when the view comes from the reference package
+             (_error_types), so the reference's handlers and tests catch it.
              Two-phase: projected = exact total (conflict.py:117-118).  One-phase: the
              cumulative count at the first reference pair block whose running total exceeds
              the budget (conflict.py:138-142), reproduced from per-row upper degrees.
@@ -32,7 +34,7 @@ from typing import Optional
 import numpy as np
 
 from . import _native, hostpool
-from .errors import EdgeBudgetExceededError
+from .errors import DeviceError, EdgeBudgetExceededError
 from .graph import ExplicitGraph, pair_chunks
 
 __all__ = ["ConflictGraph", "lists_intersect", "build", "build_reference", "BuildStats"]
@@ -83,11 +85,16 @@ def lists_intersect(a, b) -> bool:
     return False
 
 
-def _result_types(view):
-    """ConflictGraph / ExplicitGraph classes of the caller's package (duck-typed drop-in)."""
+def _caller_package(view):
     mod = type(view).__module__
     pkg = mod.rsplit(".", 1)[0] if "." in mod else mod
-    if pkg and pkg != __package__:
+    return pkg if pkg and pkg != __package__ else None
+
+
+def _result_types(view):
+    """ConflictGraph / ExplicitGraph classes of the caller's package (duck-typed drop-in)."""
+    pkg = _caller_package(view)
+    if pkg:
         try:
             cg = importlib.import_module(pkg + ".conflict").ConflictGraph
             eg = importlib.import_module(pkg + ".graph").ExplicitGraph
@@ -95,6 +102,35 @@ def _result_types(view):
         except (ImportError, AttributeError):
             pass
     return ConflictGraph, ExplicitGraph
+
+
+_device_error_types: dict = {}
+
+
+def _error_types(view):
+    """(EdgeBudgetExceededError, DeviceError) to raise for this caller.
+
+    A caller of the reference package (palettecolor views, e.g. after ``install_into``)
+    gets the reference's own EdgeBudgetExceededError (errors.py:76-84), so its
+    ``except EdgeBudgetExceededError`` (cli.py:446, exit code 4) and its tests'
+    ``pytest.raises`` (test_conflict.py:93-98) catch it; and a DeviceError that also derives
+    from the reference's PaletteColorError root, so ``except PaletteColorError`` sees device
+    failures too.  Callers of this package get this package's classes.
+    """
+    pkg = _caller_package(view)
+    if pkg:
+        try:
+            errs = importlib.import_module(pkg + ".errors")
+            budget = errs.EdgeBudgetExceededError
+            root = errs.PaletteColorError
+        except (ImportError, AttributeError):
+            return EdgeBudgetExceededError, DeviceError
+        dev = _device_error_types.get(root)
+        if dev is None:
+            dev = type("DeviceError", (DeviceError, root), {"__module__": __name__})
+            _device_error_types[root] = dev
+        return budget, dev
+    return EdgeBudgetExceededError, DeviceError
 
 
 def _lists_as_csr(lists, n: int):
@@ -147,13 +183,25 @@ def stage(view, lists, ctx: Optional[_native.Context] = None) -> _native.Context
 def build(view, lists, *, edge_budget: Optional[int] = None, threads: int = 1,
           block_pairs: int = 1 << 20, two_phase: bool = True):
     """Scan all active pairs on the GPU and return the canonical conflict CSR."""
+    budget_error, device_error = _error_types(view)
+    try:
+        return _build(view, lists, edge_budget, block_pairs, two_phase, budget_error)
+    except DeviceError as e:
+        if isinstance(e, device_error):
+            raise
+        raise device_error(*e.args) from e
+
+
+def _build(view, lists, edge_budget, block_pairs, two_phase, budget_error):
     CG, EG = _result_types(view)
-    ctx = stage(view, lists)
+    ctx = _native.context()
     n = view.n_active
-    # the commuting-pair sweep (view_edges_scanned only) runs on a side stream next to the
+    # the commuting-pair sweep (view_edges_scanned only) runs on a side stream, launched by
+    # the input prep as soon as the bit planes exist, next to the bucket prep, the
     # conflict-row passes and the copy-out; its count is collected after the fill
     ctx.option("k1_async", 1)
     try:
+        stage(view, lists, ctx)
         c = ctx.count(0, 1, 0, n)
     finally:
         ctx.option("k1_async", 0)
@@ -163,10 +211,9 @@ def build(view, lists, *, edge_budget: Optional[int] = None, threads: int = 1,
     last_stats.deg_upper_sum = int(c.deg_upper_sum)
     if edge_budget is not None and total > edge_budget:
         if two_phase:
-            raise EdgeBudgetExceededError(total, edge_budget)
+            raise budget_error(total, edge_budget)
         _, degu = ctx.degrees(n)
-        raise EdgeBudgetExceededError(one_phase_projection(degu, block_pairs, edge_budget),
-                                      edge_budget)
+        raise budget_error(one_phase_projection(degu, block_pairs, edge_budget), edge_budget)
     nm = int(c.members_in_range)
     members = np.empty(nm, dtype=np.int64)
     offsets = np.empty(nm + 1, dtype=np.int64)

@@ -213,6 +213,7 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "d2h_mode")) ctx->d2h_mode = (int)value;
     else if (!strcmp(key, "k1_async")) ctx->k1_async = (int)value;
     else if (!strcmp(key, "k1_wide")) ctx->k1_wide = (int)value;
+    else if (!strcmp(key, "k1_lds")) ctx->k1_lds = (int)value;
     else if (!strcmp(key, "k1_early")) ctx->k1_early = (int)value;
     else if (!strcmp(key, "d2h_gap16")) ctx->d2h_gap16 = (int)value;
     else if (!strcmp(key, "d2h_pipe")) ctx->d2h_pipe = (int)value;
@@ -813,7 +814,8 @@ static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, 
         if (fr6)
             *launches += launch_commute_fr6_items(ctx->A.as<uint32_t>(), ctx->B.as<uint32_t>(),
                                                   ctx->kw, n, ctx->items.as<int64_t>(), njb,
-                                                  (int32_t)ic, i0, i1, anti, ctx->sms, s);
+                                                  (int32_t)ic, i0, i1, anti, ctx->sms,
+                                                  ctx->k1_lds == 128 ? 1 : 0, s);
         else if (ctx->h_wide)
             *launches += launch_commute_fr2_items(ctx->B.as<uint32_t>(), ctx->H.as<uint32_t>(),
                                                   ctx->kw, n, ctx->items.as<int64_t>(), njb,

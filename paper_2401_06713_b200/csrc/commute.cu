@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(FR_WARPS * 32) k_commute_fr2(
 // lookup address is  base_l | ((A_i >> 6g) & 63) << 7  — one funnel shift and one LOP3
 // straight from the row's bits (no per-row offset array), with g*8192 as the immediate.
 // ---------------------------------------------------------------------------------------
-template <int KW>
+template <int KW, int RPW>
 __global__ void __launch_bounds__(FR_WARPS * 32, 1) k_commute_fr6(
     const uint32_t *__restrict__ A, const uint32_t *__restrict__ B, int64_t n,
     const int64_t *__restrict__ item_start, int64_t njb, int32_t ichunk, int64_t item0,
@@ -428,6 +428,9 @@ __global__ void __launch_bounds__(FR_WARPS * 32, 1) k_commute_fr6(
     constexpr int NG = (K + 5) / 6;      // 6-bit slices (the last one narrower)
     constexpr int JB = K1_FR_JB;         // 1024 partners
     constexpr int BT_STRIDE = K + 1;
+    constexpr int LPR = 32 / RPW;        // lanes per row
+    constexpr int EB = 128 / LPR;        // bytes per lane lookup (8: LDS.64, 16: LDS.128)
+    constexpr int NW = EB / 4;           // 32-partner words per lane
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ unsigned long long red[FR_WARPS];
     const uint32_t smem_s = (uint32_t)__cvta_generic_to_shared(smem);
@@ -436,8 +439,8 @@ __global__ void __launch_bounds__(FR_WARPS * 32, 1) k_commute_fr6(
     uint32_t *bt = reinterpret_cast<uint32_t *>(tbl + NG * 8192);  // 32 x BT_STRIDE
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int half = lane >> 4, hl = lane & 15;
-    const uint32_t base_l = tbl_s + (uint32_t)hl * 8u;
+    const int grp = lane / LPR, hl = lane % LPR;
+    const uint32_t base_l = tbl_s + (uint32_t)(hl * EB);
 
     const int64_t nitems = item1 - item0;
     const int64_t my0 = item0 + nitems * blockIdx.x / gridDim.x;
@@ -473,7 +476,7 @@ __global__ void __launch_bounds__(FR_WARPS * 32, 1) k_commute_fr6(
             }
             __syncthreads();
             // phase B: the 64 XOR combinations of each slice's 6 bit rows; warp g-slice, lane
-            // t = 32-partner group (entry word (t & 1) of half-lane t >> 1)
+            // t = 32-partner group t (byte 4t of the 128-byte entry)
             for (int g = warp; g < NG; g += FR_WARPS) {
                 const uint32_t *row = bt + lane * BT_STRIDE + 6 * g;
                 uint32_t r[6];
@@ -494,8 +497,8 @@ __global__ void __launch_bounds__(FR_WARPS * 32, 1) k_commute_fr6(
         const int64_t jlast = min(n, (jb + 1) * (int64_t)JB);  // exclusive
         const int64_t i0 = ic * ichunk;
         const int64_t i1 = min(i0 + ichunk, jlast);
-        const int64_t jbase = jb * JB + 64 * hl;
-        for (int64_t i = i0 + 2 * warp + half; i < i1; i += 2 * FR_WARPS) {
+        const int64_t jbase = jb * JB + 32 * NW * hl;
+        for (int64_t i = i0 + RPW * warp + grp; i < i1; i += RPW * FR_WARPS) {
             uint32_t a[KW + 1];
             if constexpr (KW == 4) {
                 const uint4 av = __ldg(reinterpret_cast<const uint4 *>(A + i * 4));
@@ -505,7 +508,9 @@ __global__ void __launch_bounds__(FR_WARPS * 32, 1) k_commute_fr6(
                 a[0] = av.x; a[1] = av.y;
             }
             a[KW] = 0u;
-            uint32_t acc0 = 0, acc1 = 0;
+            uint32_t acc[NW];
+#pragma unroll
+            for (int w = 0; w < NW; ++w) acc[w] = 0u;
 #pragma unroll
             for (int g = 0; g < NG; ++g) {
                 const int o = 6 * g, w = o >> 5, sh = o & 31;
@@ -513,18 +518,27 @@ __global__ void __launch_bounds__(FR_WARPS * 32, 1) k_commute_fr6(
                 uint32_t x;
                 if (sh + 6 <= 32) x = sh >= 7 ? (a[w] >> (sh - 7)) : (a[w] << (7 - sh));
                 else x = __funnelshift_r(a[w], a[w + 1], sh) << 7;
-                const uint32_t ad = (x & 0x1f80u) | base_l;
-                uint32_t e0, e1;
-                asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];"
-                             : "=r"(e0), "=r"(e1) : "r"(ad + (uint32_t)(g * 8192)));
-                acc0 ^= e0;
-                acc1 ^= e1;
+                uint32_t ad;  // (x & 0x1f80) | base_l: one LOP3 (base_l has no bits in 7..12)
+                asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(ad) : "r"(x), "r"(0x1f80u), "r"(base_l));
+                ad += (uint32_t)(g * 8192);
+                if constexpr (NW == 4) {
+                    uint32_t e0, e1, e2, e3;
+                    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(e0), "=r"(e1), "=r"(e2), "=r"(e3) : "r"(ad));
+                    acc[0] ^= e0; acc[1] ^= e1; acc[2] ^= e2; acc[3] ^= e3;
+                } else {
+                    uint32_t e0, e1;
+                    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(e0), "=r"(e1) : "r"(ad));
+                    acc[0] ^= e0; acc[1] ^= e1;
+                }
             }
-            // partners j = jbase + s (word 0) and jbase + 32 + s (word 1) with j > i
-            const int64_t d0 = i - jbase, d1 = d0 - 32;
-            const uint32_t m0 = d0 < 0 ? 0xffffffffu : (d0 >= 31 ? 0u : ~((2u << d0) - 1u));
-            const uint32_t m1 = d1 < 0 ? 0xffffffffu : (d1 >= 31 ? 0u : ~((2u << d1) - 1u));
-            local += __popc(acc0 & m0) + __popc(acc1 & m1);
+            // partners j = jbase + 32w + s with j > i
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                const int64_t d = i - (jbase + 32 * w);
+                const uint32_t m = d < 0 ? 0xffffffffu : (d >= 31 ? 0u : ~((2u << d) - 1u));
+                local += __popc(acc[w] & m);
+            }
         }
     }
     for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
@@ -583,15 +597,15 @@ size_t fr6_smem() {
     return 8192 + (size_t)NG * 8192 + (size_t)32 * (K + 1) * 4;  // + alignment slack
 }
 
-template <int KW>
+template <int KW, int RPW>
 int run_fr6(const uint32_t *A, const uint32_t *B, int64_t n, const int64_t *item_start,
             int64_t njb, int32_t ichunk, int64_t item0, int64_t item1,
             unsigned long long *anti, int sms, cudaStream_t s) {
     const size_t smem = fr6_smem<KW>();
-    allow_max_smem(k_commute_fr6<KW>);
-    const int grid = occupancy_grid(k_commute_fr6<KW>, FR_WARPS * 32, smem, sms, item1 - item0);
-    k_commute_fr6<KW><<<grid, FR_WARPS * 32, smem, s>>>(A, B, n, item_start, njb, ichunk, item0,
-                                                       item1, anti);
+    allow_max_smem(k_commute_fr6<KW, RPW>);
+    const int grid = occupancy_grid(k_commute_fr6<KW, RPW>, FR_WARPS * 32, smem, sms, item1 - item0);
+    k_commute_fr6<KW, RPW><<<grid, FR_WARPS * 32, smem, s>>>(A, B, n, item_start, njb, ichunk,
+                                                            item0, item1, anti);
     return 1;
 }
 
@@ -636,11 +650,18 @@ int fr_jb(int32_t kw, int wide) { return (wide && (kw == 2 || kw == 4)) ? K1_FR_
 int launch_commute_fr6_items(const uint32_t *A, const uint32_t *B, int32_t kw, int64_t n,
                              const int64_t *item_start, int64_t njb, int32_t ichunk,
                              int64_t item0, int64_t item1, unsigned long long *anti, int sms,
-                             cudaStream_t s) {
+                             int wide_loads, cudaStream_t s) {
     if (item1 <= item0) return 0;
-    switch (kw) {
-        case 2: return run_fr6<2>(A, B, n, item_start, njb, ichunk, item0, item1, anti, sms, s);
-        case 4: return run_fr6<4>(A, B, n, item_start, njb, ichunk, item0, item1, anti, sms, s);
+    if (wide_loads) {  // LDS.128, a quarter-warp per row
+        switch (kw) {
+            case 2: return run_fr6<2, 4>(A, B, n, item_start, njb, ichunk, item0, item1, anti, sms, s);
+            case 4: return run_fr6<4, 4>(A, B, n, item_start, njb, ichunk, item0, item1, anti, sms, s);
+            default: return 0;
+        }
+    }
+    switch (kw) {  // LDS.64, a half-warp per row
+        case 2: return run_fr6<2, 2>(A, B, n, item_start, njb, ichunk, item0, item1, anti, sms, s);
+        case 4: return run_fr6<4, 2>(A, B, n, item_start, njb, ichunk, item0, item1, anti, sms, s);
         default: return 0;
     }
 }

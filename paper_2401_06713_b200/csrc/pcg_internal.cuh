@@ -188,7 +188,7 @@ int fr_jb(int32_t kw, int wide);
 int launch_commute_fr6_items(const uint32_t *A, const uint32_t *B, int32_t kw, int64_t n,
                              const int64_t *item_start, int64_t njb, int32_t ichunk,
                              int64_t item0, int64_t item1, unsigned long long *anti, int sms,
-                             cudaStream_t s);
+                             int wide_loads, cudaStream_t s);
 int launch_fr_prep2(const uint32_t *A, int32_t kw, int64_t npad, uint32_t *H, cudaStream_t s);
 int launch_commute_fr2_items(const uint32_t *B, const uint32_t *H, int32_t kw, int64_t n,
                              const int64_t *item_start, int64_t njb, int32_t ichunk,
@@ -248,6 +248,7 @@ struct pcg_ctx {
 
     // options
     int k1_algo = 0;    // 0 auto, 1 direct, 2 four-Russians
+    int k1_lds = 128;   // 6-bit K1 lookup width: 128 (LDS.128, quarter-warp rows) or 64
     int k1_wide = 1;    // four-Russians with 64-bit entries (2048-partner blocks) when kw <= 4
     bool h_wide = false;  // the staged H offsets are in the wide kernel's format
     int window = 0;     // K2 window bits (0 auto)

@@ -39,6 +39,26 @@ def enabled() -> bool:
     return os.environ.get("PICASSO_HOST_POOL", "1") != "0"
 
 
+_probe: "np.ndarray | None" = None
+
+
+def _calibrate() -> int:
+    """sys.getrefcount of a buffer referenced only by a module global, read through a local
+    exactly as empty_int64 reads it (3 on CPython 3.12: the global, the local, the call's
+    argument; interpreters that borrow local references report fewer).  Measured once, so
+    the ownership test does not depend on the interpreter's reference accounting."""
+    global _probe
+    _probe = np.empty(1, dtype=np.int64)
+    with _lock:
+        b = _probe
+        base = sys.getrefcount(b)
+    _probe = None
+    return base
+
+
+_SOLE_OWNER_REFS = _calibrate()
+
+
 def empty_int64(count: int) -> np.ndarray:
     """An int64 array of ``count`` elements (uninitialised), from the pool when large."""
     global _buf
@@ -46,8 +66,8 @@ def empty_int64(count: int) -> np.ndarray:
         return np.empty(count, dtype=np.int64)
     with _lock:
         b = _buf
-        # references: the module global + the local ``b`` + getrefcount's argument
-        if b is not None and b.size >= count and sys.getrefcount(b) <= 3:
+        # only the pool references it: no earlier result (or any view of one) is alive
+        if b is not None and b.size >= count and sys.getrefcount(b) <= _SOLE_OWNER_REFS:
             _pin(b)
             return b[:count]
         # busy or too small: the new buffer becomes the pooled one (a busy old buffer now

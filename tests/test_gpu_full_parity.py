@@ -1,0 +1,93 @@
+"""Full-size parity at the benchmarked and north-star configurations (GPU, default suite).
+
+Every entry of every CSR is compared, through hashes: tests/golden/scale.json holds the
+iteration-1 CSR hashes of configs 2 and 3 (and 4) and whole-run colorings with per-iteration
+CSR hashes, produced by the scale oracle (oracle/bucket_oracle.c, tools/make_golden_scale.py)
+which tests/test_scale_oracle.py pins against the reference's own outputs — including the
+reference's recorded 50k whole run.  The product side goes through the public API
+(paper_2401_06713_b200.build / run -> C ABI -> sm_100a kernels) and hashes its int64 output
+the same way (oracle/scale.py csr_hashes: members/offsets sha + a block hash of the
+neighbors).  Reference: conflict.py:89-167, driver.py:272-385.
+"""
+import json
+import os
+import time
+
+import numpy as np
+import pytest
+
+import paper_2401_06713_b200 as b200
+from conftest import GOLDEN
+from oracle.scale import csr_hashes, sha16
+
+pytestmark = pytest.mark.gpu
+
+CONFIGS = {"c2": (100_000, 32), "c3": (1_000_000, 64), "c4": (4_000_000, 128),
+           "q32_n50000": (50_000, 32)}
+
+
+@pytest.fixture(scope="module")
+def scale_gold():
+    with open(os.path.join(GOLDEN, "scale.json")) as f:
+        return json.load(f)
+
+
+def _view(name):
+    n, q = CONFIGS[name]
+    return b200.pauli_view(b200.PauliSet.from_strings(b200.random_pauli_strings(n, q, seed=0)))
+
+
+def _hashes(gc):
+    return csr_hashes(gc.members, gc.graph.offsets, gc.graph.neighbors, gc.edge_count,
+                      gc.view_edges_scanned)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_iteration1_csr_full_hash(scale_gold, name):
+    want = scale_gold["builds"][name]
+    view = _view(name)
+    assert sha16(view.backing.words.view(np.int64)) == want["words_sha"]
+    plan = b200.plan_iteration(1, view.n_active, b200.PaletteParams(12.5, 2.0, seed=0))
+    lists = b200.assign_random_lists(plan, view.active, 0)  # GPU lists at this size
+    assert sha16(lists.array) == want["lists_sha"]
+    t = time.perf_counter()
+    gc = b200.build(view, lists)
+    dt = time.perf_counter() - t
+    got = _hashes(gc)
+    print(f"{name}: build {dt:.3f} s, |E_c|={gc.edge_count}")
+    for k in ("members_sha", "offsets_sha", "neighbors_bsha", "n_members", "edge_count",
+              "view_edges_scanned"):
+        assert got[k] == want[k], (k, got[k], want[k])
+
+
+@pytest.mark.parametrize("name", ["q32_n50000", "c2", "c3"])
+def test_whole_run_identical_coloring_full_size(scale_gold, name):
+    """The whole Picasso run on the GPU: every residue build's CSR and the final coloring
+    equal the oracle-driven run (q32_n50000: also the reference's own recorded run)."""
+    if name not in scale_gold["runs"]:
+        pytest.skip(f"no golden run for {name}")
+    want = scale_gold["runs"][name]
+    got = []
+
+    def tracing(view, lists, **kw):
+        gc = b200.build(view, lists, **kw)
+        h = _hashes(gc)
+        h.update(n_active=int(view.n_active), active_sha=sha16(view.active),
+                 lists_sha=sha16(lists.array))
+        got.append(h)
+        return gc
+
+    t = time.perf_counter()
+    res = b200.run(_view(name), b200.PaletteParams(12.5, 2.0, seed=0), builder=tracing)
+    print(f"{name}: whole run {time.perf_counter() - t:.1f} s (incl. hashing), "
+          f"{res.total_colors} colors, {len(res.iterations)} iterations")
+    assert len(got) == len(want["builds"])
+    for it, (g, w) in enumerate(zip(got, want["builds"])):
+        for k in g:
+            assert g[k] == w[k], (it + 1, k, g[k], w[k])
+    assert sha16(res.color) == want["color_sha"]
+    assert sha16(res.colored_at) == want["colored_at_sha"]
+    assert res.total_colors == want["colors"]
+    assert len(res.iterations) == want["iterations"]
+    assert res.oracle_edges == want["oracle_edges"]
+    assert res.peak_conflict_edges == want["peak_conflict_edges"]
