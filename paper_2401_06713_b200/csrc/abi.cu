@@ -214,6 +214,8 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "k1_async")) ctx->k1_async = (int)value;
     else if (!strcmp(key, "k1_wide")) ctx->k1_wide = (int)value;
     else if (!strcmp(key, "k1_lds")) ctx->k1_lds = (int)value;
+    else if (!strcmp(key, "own_rows_lo")) ctx->own_lo = value;
+    else if (!strcmp(key, "own_rows_hi")) ctx->own_hi = value;
     else if (!strcmp(key, "k1_early")) ctx->k1_early = (int)value;
     else if (!strcmp(key, "d2h_gap16")) ctx->d2h_gap16 = (int)value;
     else if (!strcmp(key, "d2h_pipe")) ctx->d2h_pipe = (int)value;
@@ -559,6 +561,8 @@ static int prep_device(pcg_ctx *ctx) {
             while (hs < want && hs < 32768) hs <<= 1;
             o.hash_slots = hs;
             o.m_cap = m_max;
+            o.row_lo = (int32_t)std::max<int64_t>(0, std::min(ctx->own_lo, n_active));
+            o.row_hi = (int32_t)(ctx->own_hi < 0 ? n_active : std::min(ctx->own_hi, n_active));
             o.fr = ctx->own_algo == 0 ? 1 : 0;
             o.l_magic = (uint32_t)(((1ull << 32) + (uint64_t)std::max(1, ctx->L) - 1) /
                                    (uint64_t)std::max(1, ctx->L));
@@ -606,6 +610,9 @@ static int prep_device(pcg_ctx *ctx) {
             }
             launch_owned_masks(b, o, ctx->sms, s);
             PCG_CHECK_LAUNCH(ctx);
+            // the per-pair mask kernel (own_algo 1) always writes every row
+            ctx->prep_lo = o.fr ? o.row_lo : 0;
+            ctx->prep_hi = o.fr ? o.row_hi : n_active;
             int64_t runs_total = 0;
             if (want_runs) {  // owned partner runs (padded to 4 ids) for the TMA-staged fill
                 PCG_ALLOC(ctx, ctx->runoff, (size_t)(entries + 1) * 8);
@@ -879,6 +886,9 @@ static int count_impl(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t r0, 
     if (!ctx->staged) return fail(ctx, PCG_E_STATE, "pcg_count before pcg_set_inputs");
     if (nshards < 1 || shard < 0 || shard >= nshards || r0 < 0 || r1 < r0 || r1 > ctx->n)
         return fail(ctx, PCG_E_ARG, "bad shard or row range");
+    if (ctx->owned && r1 > r0 && (r0 < ctx->prep_lo || r1 > ctx->prep_hi))
+        return fail(ctx, PCG_E_STATE, "count rows outside the owned-mask rows of the prep "
+                                      "(options own_rows_lo/own_rows_hi)");
     PCG_TRY_CUDA(ctx, cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
     // an early K1 of this build (launched by the prep, own counter) is taken over by a

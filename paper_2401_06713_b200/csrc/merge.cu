@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
     unsigned short *sL16 = reinterpret_cast<unsigned short *>(sLv);
     int32_t *sL32 = reinterpret_cast<int32_t *>(sLv);
     const bool stage_lists = o.stage_lists != 0;
-    __shared__ int ncoll, overflow, nlose;
+    __shared__ int ncoll, overflow, nlose, nlo, nhi;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NWARPS = OWN_THREADS / 32;
     const uint32_t T_s = (uint32_t)__cvta_generic_to_shared(T);
@@ -247,8 +247,25 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
             ncoll = 0;
             overflow = 0;
         }
-        for (int t = tid; t < m; t += OWN_THREADS) sid[t] = mem[t];
+        if (tid == 0) {
+            nlo = 0;
+            nhi = 0;
+        }
         __syncthreads();
+        {
+            int lo_c = 0, hi_c = 0;
+            for (int t = tid; t < m; t += OWN_THREADS) {
+                const int32_t r = mem[t];
+                sid[t] = r;
+                lo_c += r < o.row_lo;
+                hi_c += r < o.row_hi;
+            }
+            if (lo_c) atomicAdd(&nlo, lo_c);
+            if (hi_c) atomicAdd(&nhi, hi_c);
+        }
+        __syncthreads();
+        // members are ascending: this shard's mask rows are the positions [nlo, nhi)
+        const int k_lo = nlo, k_hi = nhi;
         // stage the members' partner vectors and color lists once (all loads in flight
         // together; every later pass reads shared memory)
         for (int x = tid; x < m * KW; x += OWN_THREADS)
@@ -262,9 +279,9 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
             }
         }
         __syncthreads();
-        // ---- commute masks
-        for (int k0 = 0; k0 < m; k0 += OWN_THREADS) {
-            const int k = k0 + tid;
+        // ---- commute masks (rows of this shard's members only)
+        for (int k0 = k_lo; k0 < k_hi; k0 += OWN_THREADS) {
+            const int k = k0 + tid < k_hi ? k0 + tid : m;  // m: no row
             uint32_t naddr[NIB];
             {
                 uint32_t av[KW];

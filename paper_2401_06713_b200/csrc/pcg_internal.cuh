@@ -101,6 +101,8 @@ struct OwnArgs {
     int32_t l16;           // members' lists staged as u16 (palette < 65536)
     int32_t stage_lists;   // stage the members' lists in shared memory (direct mode, or u16)
     int32_t lcap;          // direct mode: losers per level (0: 1024)
+    int32_t row_lo, row_hi;  // four-Russians kernel: mask rows only for members in [lo, hi)
+                             // (a sharded build's own rows; other rows are left unwritten)
 };
 
 struct RunArgs {
@@ -248,6 +250,9 @@ struct pcg_ctx {
 
     // options
     int k1_algo = 0;    // 0 auto, 1 direct, 2 four-Russians
+    int64_t own_lo = 0, own_hi = -1;  // options own_rows_lo/hi: rows whose owned-mask rows
+                                      // the prep computes (-1: all; sharded builds)
+    int64_t prep_lo = 0, prep_hi = 0; // the range the current masks hold
     int k1_lds = 128;   // 6-bit K1 lookup width: 128 (LDS.128, quarter-warp rows) or 64
     int k1_wide = 1;    // four-Russians with 64-bit entries (2048-partner blocks) when kw <= 4
     bool h_wide = false;  // the staged H offsets are in the wide kernel's format

@@ -2,19 +2,28 @@
 
 SURVEY.md §8(e).  Every rank holds the (small, replicated) inputs and runs:
 
-  1. the commuting-pair sweep over its share of the upper triangle (K1 tile shard
-     rank/world) and the conflict-row count over its contiguous row range (K2);
-  2. all-reduce of the four totals and all-gather of the per-row degrees (n int32);
-  3. the budget check (identical on every rank — same exception everywhere);
-  4. the fill of its own rows, written straight into its slice of the global CSR (global
-     offsets and compact ids come from the gathered degrees);
-  5. all-gather of the slices, in rank order, into the canonical CSR.
+  1. the input prep (encode, color buckets) — replicated, O(n L) — and the owned bucket
+     masks (K2a) for the member rows in its own row range only (options own_rows_lo/hi:
+     the commute-mask rows, the bulk of K2a, divide by the world size);
+  2. the commuting-pair sweep over its share of the upper triangle (K1 work items
+     rank/world) and the conflict-row count over its contiguous row range (K2c);
+  3. all-reduce of the four totals and all-gather of the per-row degrees (4 B per row);
+  4. the budget check (identical on every rank — the same exception everywhere);
+  5. the fill of its own rows (K2f) into a device slice (int32 ids);
+  6. a gather of the slices, in rank order, to the root rank (default), which widens them
+     and copies the canonical int64 CSR to its host once; ``gather="all"`` all-gathers
+     instead (every rank returns the whole graph).
 
 Rows are independent (each GPU generates full rows from the color buckets), so the only
-exchanges are the degree all-gather (4 bytes per row) and the CSR slice all-gather.  With
-``backend="nccl"`` both run on device tensors over NVLink; with gloo (CPU tests) they run on
-host tensors.  The per-rank compute goes through an *engine* (the CUDA context by default;
-tests substitute an oracle-backed engine to check this host logic without a GPU).
+exchanges are the degree all-gather and the slice gather.  With ``backend="nccl"`` both run
+on device tensors over NVLink; with gloo (CPU tests) they run on host tensors.  The per-rank
+compute goes through an *engine* (the CUDA context by default; tests substitute an
+oracle-backed engine to check this host logic without a GPU).
+
+``run_sharded`` is the whole Picasso run on N GPUs (driver.py:272-385, the reference's
+Algorithm 1): every rank takes part in each sharded build, the root colors the conflict
+graph on the host (the list coloring is sequential in its draws) and broadcasts the outcome,
+so every rank ends with the identical coloring — the single-GPU run's and the reference's.
 """
 
 from __future__ import annotations
@@ -25,8 +34,7 @@ from typing import Optional
 import numpy as np
 
 from . import _native, hostpool
-from .conflict import ConflictGraph, _lists_as_csr, _result_types, one_phase_projection
-from .errors import EdgeBudgetExceededError
+from .conflict import _error_types, _lists_as_csr, _result_types, one_phase_projection
 
 
 def row_ranges(n: int, world: int) -> list:
@@ -40,8 +48,16 @@ class NativeEngine:
     def __init__(self, device: Optional[int] = None):
         self.ctx = _native.context(device)
 
-    def set_inputs(self, words, num_qubits, active, data, off, L, base, P):
-        self.ctx.set_inputs(words, num_qubits, active, data, off, L, base, P)
+    def set_inputs(self, words, num_qubits, active, data, off, L, base, P, rows=None):
+        # the owned-mask rows this rank's count and fill will read (the prep runs here)
+        lo, hi = rows if rows is not None else (0, -1)
+        self.ctx.option("own_rows_lo", lo)
+        self.ctx.option("own_rows_hi", hi)
+        try:
+            self.ctx.set_inputs(words, num_qubits, active, data, off, L, base, P)
+        finally:
+            self.ctx.option("own_rows_lo", 0)
+            self.ctx.option("own_rows_hi", -1)
 
     def count(self, shard, nshards, r0, r1):
         c = self.ctx.count(shard, nshards, r0, r1)
@@ -99,27 +115,34 @@ def _all_gather_rows(dist, local: np.ndarray, ranges, dev) -> np.ndarray:
 
 
 def build_sharded(view, lists, *, edge_budget: Optional[int] = None, threads: int = 1,
-                  block_pairs: int = 1 << 20, two_phase: bool = True, engine=None):
+                  block_pairs: int = 1 << 20, two_phase: bool = True, engine=None,
+                  gather: str = "root", root: int = 0):
     """The conflict build of ``conflict.build``, sharded over the default process group.
 
-    Every rank returns the same canonical ConflictGraph (bit-identical to the single-GPU
-    build and to the reference).
+    ``gather="root"``: the root rank returns the canonical ConflictGraph (bit-identical to
+    the single-GPU build and to the reference); the other ranks return its header — the
+    same members, offsets, edge_count and view_edges_scanned, with an empty neighbor array.
+    ``gather="all"``: every rank returns the whole graph.  Budget errors are raised on every
+    rank, with the caller's exception class (conflict._error_types).
     """
     import torch
     import torch.distributed as dist
 
+    if gather not in ("root", "all"):
+        raise ValueError("gather must be 'root' or 'all'")
     rank, world = dist.get_rank(), dist.get_world_size()
     dev = _coll_device(dist)
     engine = engine or NativeEngine()
     CG, EG = _result_types(view)
+    budget_error, _ = _error_types(view)
     words = np.ascontiguousarray(view.backing.words, dtype=np.uint64)
     active = np.ascontiguousarray(view.active, dtype=np.int64)
     n = int(active.size)
     data, off, L = _lists_as_csr(lists, n)
-    engine.set_inputs(words, int(view.backing.num_qubits), active, data, off, L,
-                      int(lists.palette_base), int(lists.palette_size))
     ranges = row_ranges(n, world)
     r0, r1 = ranges[rank]
+    engine.set_inputs(words, int(view.backing.num_qubits), active, data, off, L,
+                      int(lists.palette_base), int(lists.palette_size), rows=(r0, r1))
     c = engine.count(rank, world, r0, r1)
     tot = torch.tensor([c["anticommuting"], c["pairs"], c["deg_sum"], c["members"]],
                        dtype=torch.int64, device=dev)
@@ -130,54 +153,88 @@ def build_sharded(view, lists, *, edge_budget: Optional[int] = None, threads: in
     total = deg_sum // 2
     if edge_budget is not None and total > edge_budget:
         if two_phase:
-            raise EdgeBudgetExceededError(total, edge_budget)
+            raise budget_error(total, edge_budget)
         gdegu = _all_gather_rows(dist, degu_local.astype(np.int32), ranges, dev)
-        raise EdgeBudgetExceededError(one_phase_projection(gdegu, block_pairs, edge_budget),
-                                      edge_budget)
-    device_fill = dev.type == "cuda" and hasattr(engine, "fill_rows_device")
-    if device_fill:  # NCCL: the slice is filled into a device buffer, never crosses PCIe
-        lo, hi = engine.fill_rows_device(gdeg, None)
-    else:
-        lo, hi, slice_vals = engine.fill_rows(gdeg, True)
-    # slices are contiguous in rank order; gather their lengths first
-    lens = torch.tensor([hi - lo], dtype=torch.int64, device=dev)
-    all_lens = [torch.empty_like(lens) for _ in range(world)]
-    dist.all_gather(all_lens, lens)
-    lens_np = [int(x.item()) for x in all_lens]
-    width = max(lens_np) if lens_np else 0
-    t = torch.zeros(max(width, 1), dtype=torch.int32 if device_fill else torch.int64, device=dev)
-    if device_fill:
-        if hi > lo:
-            engine.fill_rows_device(gdeg, t.data_ptr(), out32=True)
-    elif hi > lo:
-        t[: hi - lo] = torch.from_numpy(slice_vals).to(dev)
-    total_len = sum(lens_np)
-    if device_fill:
-        # all-gather the int32 slices over NVLink, widen on the device, then one DMA of the
-        # canonical CSR into the pooled (pinned) host buffer the single-GPU build also reuses
-        out = torch.empty(world * max(width, 1), dtype=torch.int32, device=dev)
-        dist.all_gather_into_tensor(out, t)
-        nbr = hostpool.empty_int64(total_len)
-        pos = 0
-        host = torch.from_numpy(nbr)
-        for r in range(world):
-            if lens_np[r]:
-                seg = out[r * max(width, 1): r * max(width, 1) + lens_np[r]].to(torch.int64)
-                host[pos:pos + lens_np[r]].copy_(seg)
-                pos += lens_np[r]
-    else:
-        parts = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(parts, t)
-        nbr = np.concatenate([p[: lens_np[r]].cpu().numpy() for r, p in enumerate(parts)]) \
-            if world else np.zeros(0, np.int64)
+        raise budget_error(one_phase_projection(gdegu, block_pairs, edge_budget), edge_budget)
     has = gdeg > 0
     members_ids = active[has]
     offsets = np.zeros(int(has.sum()) + 1, dtype=np.int64)
     np.cumsum(gdeg[has].astype(np.int64), out=offsets[1:])
-    assert offsets[-1] == nbr.size == 2 * total
-    assert members_ids.size == members
+    assert members_ids.size == members and offsets[-1] == 2 * total
+    # every slice's length follows from the gathered degrees
+    starts = np.concatenate([[0], np.cumsum(gdeg.astype(np.int64))])
+    lens_np = [int(starts[b] - starts[a]) for a, b in ranges]
+    width = max(max(lens_np, default=0), 1)
+    device_fill = dev.type == "cuda" and hasattr(engine, "fill_rows_device")
+    t = torch.zeros(width, dtype=torch.int32 if device_fill else torch.int64, device=dev)
+    if device_fill:  # NCCL: the slice is filled into a device buffer, never crosses PCIe
+        if lens_np[rank]:
+            engine.fill_rows_device(gdeg, t.data_ptr(), out32=True)
+    else:
+        lo, hi, vals = engine.fill_rows(gdeg, True)
+        assert hi - lo == lens_np[rank]
+        if hi > lo:
+            t[: hi - lo] = torch.from_numpy(vals).to(dev)
+    receive = gather == "all" or rank == root
+    if gather == "all":
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+    else:
+        parts = [torch.empty_like(t) for _ in range(world)] if rank == root else None
+        dist.gather(t, parts, dst=root)
+    if not receive:
+        nbr = np.zeros(0, dtype=np.int64)
+    elif device_fill:
+        # widen on the device, then one copy per slice into the pooled (pinned) host buffer
+        # the single-GPU build also reuses
+        nbr = hostpool.empty_int64(2 * total)
+        host = torch.from_numpy(nbr)
+        pos = 0
+        for r in range(world):
+            if lens_np[r]:
+                host[pos:pos + lens_np[r]].copy_(parts[r][: lens_np[r]].to(torch.int64))
+                pos += lens_np[r]
+    else:
+        nbr = np.concatenate([p[: lens_np[r]].cpu().numpy() for r, p in enumerate(parts)]) \
+            if world else np.zeros(0, np.int64)
+    if receive:
+        assert nbr.size == 2 * total
     return CG(members=members_ids, graph=EG(n=int(members_ids.size), offsets=offsets, neighbors=nbr),
               edge_count=total, view_edges_scanned=pairs - anti)
+
+
+def run_sharded(view, params, *, strategy: str = "dynamic", edge_budget: Optional[int] = None,
+                block_pairs: int = 1 << 20, engine=None, root: int = 0):
+    """The whole Picasso run (driver.run) with every conflict build sharded over the default
+    process group.  The root rank colors each conflict graph (list_coloring, the reference's
+    draw order) and broadcasts the outcome; every rank returns the identical ColoringResult."""
+    import torch.distributed as dist
+
+    from . import driver, list_coloring
+    from .list_coloring import ConflictColoringOutcome
+
+    rank = dist.get_rank()
+
+    def builder(v, lists, **kw):
+        kw.pop("threads", None)
+        return build_sharded(v, lists, engine=engine, gather="root", root=root, **kw)
+
+    def coloring(gc, lists, strategy, seed, iteration):
+        box = [None]
+        if rank == root:
+            o = list_coloring.color_conflict_graph(gc, lists, strategy=strategy, seed=seed,
+                                                   iteration=iteration)
+            ids = np.fromiter(o.colored.keys(), dtype=np.int64, count=len(o.colored))
+            cols = np.fromiter(o.colored.values(), dtype=np.int64, count=len(o.colored))
+            box[0] = (ids, cols, o.uncolored, o.colors_used, o.empties, o.removal_ops)
+        dist.broadcast_object_list(box, src=root)
+        ids, cols, unc, used, empties, removals = box[0]
+        return ConflictColoringOutcome(colored=dict(zip(ids.tolist(), cols.tolist())),
+                                       uncolored=unc, colors_used=used, empties=empties,
+                                       removal_ops=removals)
+
+    return driver.run(view, params, strategy=strategy, edge_budget=edge_budget,
+                      block_pairs=block_pairs, builder=builder, conflict_coloring=coloring)
 
 
 def bench_sharded(args) -> None:
@@ -199,16 +256,19 @@ def bench_sharded(args) -> None:
     n = view.n_active
     pairs = n * (n - 1) // 2
     ctx = _native.context(local)
-    stage(view, lists, ctx)
     ranges = row_ranges(n, world)
     r0, r1 = ranges[rank]
+    # the prep computes the owned-mask rows of this rank's row range only
+    ctx.option("own_rows_lo", r0)
+    ctx.option("own_rows_hi", r1)
+    stage(view, lists, ctx)
     width = max(b - a for a, b in ranges)
     ctx.option("rows_out32", 1)  # the timed step exchanges int32 slices
     deg_local = torch.zeros(width, dtype=torch.int32, device=dev)
     gdeg_parts = torch.zeros(world * width, dtype=torch.int32, device=dev)
 
     def step():
-        # input prep (replicated on every rank) + count of this rank's shard
+        # input prep (buckets replicated, owned masks of this rank's rows) + count of its shard
         ctx.prep_device()
         c = ctx.count(rank, world, r0, r1)
         ctx.degrees_device(deg_local.data_ptr())
@@ -223,8 +283,9 @@ def bench_sharded(args) -> None:
         w = int(all_lens.max().item())
         buf = torch.zeros(max(w, 1), dtype=torch.int32, device=dev)  # int32 ids: half the exchange
         ctx.fill_rows_device(gdeg.data_ptr(), mx, buf.data_ptr())
-        out = torch.empty(world * max(w, 1), dtype=torch.int32, device=dev)
-        dist.all_gather_into_tensor(out, buf)
+        # the slices gathered to the root rank's HBM, in rank order (the canonical CSR)
+        parts = [torch.empty_like(buf) for _ in range(world)] if rank == 0 else None
+        dist.gather(buf, parts, dst=0)
         return c
 
     for _ in range(args.warmup):
@@ -250,21 +311,23 @@ def bench_sharded(args) -> None:
     ms = float(t.item())
 
     ctx.option("rows_out32", 0)
+    ctx.option("own_rows_lo", 0)
+    ctx.option("own_rows_hi", -1)
     # ---- end to end through the public sharded build (host inputs in, the canonical int64
-    # CSR on every rank out), max over ranks
+    # CSR on the root rank's host out), max over ranks
     import time
 
     e2e = []
+    nnz = 0
     for k in range(1 + args.steps):
         torch.cuda.synchronize()
         dist.barrier()
         t0 = time.perf_counter()
-        gc = build_sharded(view, lists)
+        gc = build_sharded(view, lists, gather="root")
         torch.cuda.synchronize()
         if k >= 1:
             e2e.append(time.perf_counter() - t0)
         nnz = int(gc.graph.neighbors.size)
-        members = int(gc.members.size)
         gc = None
     te = torch.tensor([statistics.mean(e2e)], dtype=torch.float64, device=dev)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -275,20 +338,18 @@ def bench_sharded(args) -> None:
             "metric": bench_mod.METRIC, "value": pairs / (ms * 1e-3), "unit": "pairs/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic",
-            "config": {"workload": f"{args.workload}: n={n}, P={plan.palette_size}, L={plan.list_size}",
-                       "pairs_per_step": pairs,
-                       "parallelism": f"pair-space shards x{world} (K1 tiles + K2 row ranges), "
-                                      "NCCL degree all-gather + int32 CSR slice all-gather",
-                       "l2": "inputs replicated per rank; no flush (the CSR slices exceed L2)"},
+            "data": "synthetic", "config": bench_mod.config_for(args.workload, world),
+            "sharding": "K1 work items and K2 row ranges by rank, owned masks of the rank's "
+                        "rows, NCCL degree all-gather + int32 CSR slice gather to rank 0",
             "e2e": {"value": pairs / e2e_s, "unit": "pairs/s",
-                    # per rank: its inputs and the gathered degrees up; down: the degrees and
-                    # the canonical int64 CSR (every rank returns the whole graph; members and
-                    # offsets are derived on the host from the degrees)
+                    # root rank: its inputs and the gathered degrees up; down: the degrees and
+                    # the canonical int64 CSR (members and offsets are derived on the host
+                    # from the degrees)
                     "h2d_bytes_per_step": int(h2d + 4 * n),
                     "d2h_bytes_per_step": int(8 * nnz + 4 * n),
                     "ms_per_step": 1e3 * e2e_s,
-                    "api": "distributed.build_sharded (every rank returns the canonical CSR)"},
+                    "api": "distributed.build_sharded (gather='root': rank 0 returns the "
+                           "canonical CSR)"},
             "gpu_launches": int(launches.item()),
             "clocks": clocks.summary(),
         }

@@ -22,8 +22,11 @@ def _free_port() -> int:
 class OracleEngine:
     """Per-rank engine computing on the CPU oracle (test infrastructure only)."""
 
-    def set_inputs(self, words, num_qubits, active, data, off, L, base, P):
+    def set_inputs(self, words, num_qubits, active, data, off, L, base, P, rows=None):
         from oracle.oracle import OracleInstance
+
+        if rows is not None:
+            self._r0 = rows[0]
         from paper_2401_06713_b200.driver import ColorLists
 
         n = active.size
@@ -63,7 +66,7 @@ class OracleEngine:
         return lo, hi, (self.csr.neighbors[lo:hi].copy() if want else None)
 
 
-def _worker(rank, world, port, name, budget, two_phase, q, native=False):
+def _worker(rank, world, port, name, budget, two_phase, q, native=False, gather="root"):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -90,8 +93,15 @@ def _worker(rank, world, port, name, budget, two_phase, q, native=False):
             eng._r0 = dmod.row_ranges(case.view.n_active, world)[rank][0]
         try:
             gc = dmod.build_sharded(case.view, case.lists, engine=eng, edge_budget=budget,
-                                    two_phase=two_phase)
-            case.check(gc)
+                                    two_phase=two_phase, gather=gather)
+            if gather == "all" or rank == 0:
+                case.check(gc)
+            else:  # the header: everything but the neighbor ids
+                assert gc.graph.neighbors.size == 0
+                assert np.array_equal(gc.members, case.members)
+                assert np.array_equal(gc.graph.offsets, case.offsets)
+                assert gc.edge_count == case.meta["edge_count"]
+                assert gc.view_edges_scanned == case.meta["view_edges_scanned"]
             q.put((rank, "ok", None))
         except EdgeBudgetExceededError as e:
             q.put((rank, "budget", e.projected))
@@ -101,11 +111,15 @@ def _worker(rank, world, port, name, budget, two_phase, q, native=False):
         dist.destroy_process_group()
 
 
-def _run(world, name, budget=None, two_phase=True, native=False):
+def _run(world, name, budget=None, two_phase=True, native=False, gather="root", target=None,
+         args=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, name, budget, two_phase, q, native))
+    target = target or _worker
+    args = args if args is not None else (name, budget, two_phase)
+    extra = (native, gather) if target is _worker else (native,)
+    procs = [ctx.Process(target=target, args=(r, world, port, *args, q, *extra))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -115,10 +129,57 @@ def _run(world, name, budget=None, two_phase=True, native=False):
     return sorted(out)
 
 
-@pytest.mark.parametrize("world,name", [(2, "tc_all_modes_pauli"), (2, "ragged_lists"),
-                                        (3, "induced_subset"), (3, "two_vertices")])
-def test_sharded_build_matches_golden(world, name):
-    res = _run(world, name)
+@pytest.mark.parametrize("world,name,gather", [(2, "tc_all_modes_pauli", "root"),
+                                               (2, "ragged_lists", "all"),
+                                               (3, "induced_subset", "root"),
+                                               (3, "two_vertices", "all"),
+                                               (3, "c1_iter1", "root")])
+def test_sharded_build_matches_golden(world, name, gather):
+    res = _run(world, name, gather=gather)
+    assert [r[1] for r in res] == ["ok"] * world, res
+
+
+def _run_worker(rank, world, port, name, q, native=False):
+    """A whole sharded Picasso run (distributed.run_sharded) on one rank."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import json
+
+        import paper_2401_06713_b200 as b200
+        from conftest import pauli_view, sha
+        from test_distributed import OracleEngine
+        from paper_2401_06713_b200 import distributed as dmod
+
+        with open(os.path.join(ROOT, "tests", "golden", "reference.json")) as f:
+            r = json.load(f)["runs"][name]
+        v = pauli_view(r["n"], r["q"], r["gen_seed"])
+        eng = dmod.NativeEngine(0) if native else OracleEngine()
+        res = dmod.run_sharded(v, b200.PaletteParams(r["palette_pct"], r["alpha"], seed=r["seed"]),
+                               strategy=r["strategy"], engine=eng)
+        ok = (sha(res.color) == r["color_sha"] and res.total_colors == r["colors"]
+              and len(res.iterations) == r["iterations"] and res.oracle_edges == r["oracle_edges"]
+              and res.peak_conflict_edges == r["peak_conflict_edges"])
+        q.put((rank, "ok" if ok else "mismatch", (sha(res.color), res.total_colors)))
+    except Exception as e:  # report, don't hang the other ranks
+        import traceback
+
+        q.put((rank, "error", traceback.format_exc()[-1500:]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,name", [(2, "c1"), (3, "tout_k3"), (2, "static_ldf")])
+def test_sharded_whole_run_identical_coloring(world, name):
+    """Algorithm 1 on N ranks (driver.py:272-385): every residue build sharded, the root colors
+    and broadcasts; every rank ends with the reference's coloring."""
+    res = _run(world, name, target=_run_worker, args=(name,))
     assert [r[1] for r in res] == ["ok"] * world, res
 
 
@@ -139,11 +200,19 @@ def test_row_ranges_cover_rows():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,name", [(2, "c1_iter1"), (3, "induced_subset"), (2, "ragged_lists")])
-def test_sharded_native_engine_on_one_gpu(world, name):
-    """Each rank runs the CUDA K1 tile shard + K2 row shard + sharded fill (all ranks share
-    cuda:0); the gathered CSR must equal the reference."""
-    res = _run(world, name, native=True)
+@pytest.mark.parametrize("world,name,gather", [(2, "c1_iter1", "root"), (3, "induced_subset", "all"),
+                                               (2, "ragged_lists", "root")])
+def test_sharded_native_engine_on_one_gpu(world, name, gather):
+    """Each rank runs the CUDA K1 work-item shard + the owned masks of its rows + K2 row shard
+    + sharded fill (all ranks share cuda:0); the gathered CSR must equal the reference."""
+    res = _run(world, name, native=True, gather=gather)
+    assert [r[1] for r in res] == ["ok"] * world, res
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,name", [(2, "c1"), (3, "tout_k4")])
+def test_sharded_whole_run_native_on_one_gpu(world, name):
+    res = _run(world, name, native=True, target=_run_worker, args=(name,))
     assert [r[1] for r in res] == ["ok"] * world, res
 
 
