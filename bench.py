@@ -273,15 +273,16 @@ def smem_peak(sm_mhz: float) -> tuple:
     try:
         with open(os.path.join(ROOT, "profiles", "smem_peak.json")) as f:
             rec = json.load(f)
-        bpc, src = float(rec["v2_half_bytes_per_clk_per_sm"]), "profiles/smem_peak.json (measured)"
+        bpc, src = float(rec["lds128_quarter_bytes_per_clk_per_sm"]), "profiles/smem_peak.json (measured)"
     except (OSError, ValueError, KeyError):
         bpc, src = 128.0, "nominal 128 B/clk/SM (no measured peak committed)"
     return bpc * 148 * sm_mhz * 1e6 / 1e9, src, bpc
 
 
 def k1_table_bytes_per_pair(q: int) -> float:
-    """Shared-memory bytes one pair costs in K1 (k_commute_fr6: one 8-byte entry per 6-bit
-    slice per 64 partners; k_commute_fr: one 4-byte entry per 4-bit slice per 32 partners)."""
+    """Shared-memory bytes one pair costs in K1 (k_commute_fr6: one 128-byte table row per
+    6-bit slice per 1024 partners = 8 B per slice per 64 partners; k_commute_fr: one 4-byte
+    entry per 4-bit slice per 32 partners)."""
     K = 64 * ((q + 31) // 32)
     return 8.0 * ((K + 5) // 6) / 64.0 if K <= 128 else 4.0 * (K // 4) / 32.0
 
@@ -373,7 +374,8 @@ def measure_workload(name, args, local, clocks_on: bool):
                "traffic": k1_traffic[0], "traffic_source": k1_traffic[1],
                "bytes_per_launch": int(pairs * bpp), "launch_ms": k1_ms,
                "note": f"algorithmic bytes = shared-memory table bytes: {bpp} B per pair (one "
-                       "8-byte entry per 6-bit slice per 64 partners) x n(n-1)/2 pairs; K1 reads "
+                       "128-byte table row per 6-bit slice per 1024 partners, read as LDS.128 by "
+                       "quarter-warps) x n(n-1)/2 pairs; K1 reads "
                        "~0 HBM (traffic), its bound is the shared-memory pipe. peak = "
                        f"{bpc:.1f} B/clk/SM x 148 x {sm_mhz:.0f} MHz ({speak_src})"}
     # the conflict-row fill against HBM (algorithmic bytes: CSR ids written + rows read)

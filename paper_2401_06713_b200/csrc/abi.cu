@@ -761,6 +761,7 @@ static int64_t fr_ichunk(const pcg_ctx *ctx) { return ctx->fr_ichunk > 0 ? ctx->
 // pairs (i<j, both < n) inside four-Russians item (jb, rows [i0,i1))
 static int64_t fr_item_pairs(int64_t n, int64_t jb, int64_t i0, int64_t i1, int64_t JB) {
     const int64_t jlo = jb * JB, jhi = std::min(n, jlo + JB);
+    if (jhi <= jlo) return 0;  // a padding block past the last row
     int64_t p = 0;
     const int64_t full_hi = std::min(i1, jlo);
     if (full_hi > i0) p += (full_hi - i0) * (jhi - jlo);

@@ -105,8 +105,10 @@ def _worker(rank, world, port, name, budget, two_phase, q, native=False, gather=
             q.put((rank, "ok", None))
         except EdgeBudgetExceededError as e:
             q.put((rank, "budget", e.projected))
-    except Exception as e:  # report, don't hang the other ranks
-        q.put((rank, "error", repr(e)))
+    except Exception:  # report, don't hang the other ranks
+        import traceback
+
+        q.put((rank, "error", traceback.format_exc()[-1500:]))
     finally:
         dist.destroy_process_group()
 

@@ -24,18 +24,55 @@ pytestmark = [pytest.mark.gpu,
                                         "(cp -r /root/reference/pkg baseline/_ref/)")]
 
 
+def _recorded_outcome(suite):
+    """The reference's own recorded run of its suite (pkg/test_output.txt): the tests that
+    failed there, and the ACCEPTANCE report lines (the acceptance criteria print measured
+    values; test_criterion_05 and _10 are expected to fail at these sizes, see
+    test_acceptance.py:203-210)."""
+    failed, report = set(), {}
+    with open(os.path.join(REF, "test_output.txt")) as f:
+        for line in f:
+            if line.startswith("FAILED tests/" + suite):
+                failed.add(line.split()[1].split("::")[1])
+            if line.startswith("tests/" + suite) and "ACCEPTANCE" in line:
+                tail = line.split("ACCEPTANCE", 1)[1]
+                report[int(tail.split()[0])] = tail.rsplit("; runtime", 1)[0].strip()
+    return failed, report
+
+
 @pytest.mark.parametrize("suite", ["test_conflict.py", "test_acceptance.py", "test_driver.py"])
 def test_reference_suite_passes_unchanged(suite, tmp_path):
+    """Same outcome as the reference's own run: every test it passed passes, and the two
+    acceptance criteria it fails (by design, at these sizes) fail with identical measured
+    values."""
     count = tmp_path / "count"
     env = dict(os.environ)
     env["PYTHONPATH"] = os.pathsep.join([os.path.join(REF, "src"), os.path.join(ROOT, "tests"), ROOT,
                                          env.get("PYTHONPATH", "")])
     env["PICASSO_DROPIN_COUNT"] = str(count)
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "ref_dropin_plugin",
+    r = subprocess.run([sys.executable, "-m", "pytest", "-v", "-s", "-p", "ref_dropin_plugin",
                         "-p", "no:cacheprovider", "--rootdir", REF, os.path.join(REF, "tests", suite)],
                        cwd=REF, env=env, capture_output=True, text=True, timeout=1800)
-    print(r.stdout[-3000:])
-    assert r.returncode == 0, r.stdout[-5000:] + r.stderr[-3000:]
+    out = r.stdout
+    print(out[-3000:])
+    failed = {ln.split()[1].split("::")[1] for ln in out.splitlines()
+              if ln.startswith("FAILED tests/" + suite)}
+    report = {}
+    for ln in out.splitlines():
+        if "ACCEPTANCE" in ln:
+            tail = ln.split("ACCEPTANCE", 1)[1]
+            report[int(tail.split()[0])] = tail.rsplit("; runtime", 1)[0].strip()
+    want_failed, want_report = _recorded_outcome(suite)
+    assert " error" not in out.splitlines()[-1], out[-5000:] + r.stderr[-3000:]
+    assert failed == want_failed, (failed, want_failed, out[-5000:])
+    timed = (1, 11)  # criteria 1 and 11 report wall times: compare their verdicts only
+    for k, v in want_report.items():
+        got = report.get(k) or ""
+        if k in timed:
+            assert got.split(" - ")[0] == v.split(" - ")[0], (k, got, v)
+        else:
+            assert got == v, (k, got, v)
     served = int(count.read_text())
-    print(f"{suite}: {served} conflict builds served by the CUDA builder")
+    print(f"{suite}: {served} conflict builds served by the CUDA builder; "
+          f"failed as in the reference's own run: {sorted(failed)}")
     assert served > 0
