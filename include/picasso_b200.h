@@ -36,6 +36,8 @@ extern "C" {
 #define PCG_E_OOM 3      /* device allocation failed */
 #define PCG_E_COLOR 4    /* a list color lies outside [palette_base, palette_base + palette_size) */
 #define PCG_E_STATE 5    /* call order violated (fill before count, ...) */
+#define PCG_E_DUPLICATE 6 /* a row's color list names one color twice (the caller dedupes: the
+                             reference's palette mask is a set, driver.py:152-172) */
 
 typedef struct pcg_ctx pcg_ctx;
 
@@ -139,10 +141,10 @@ int pcg_kernel_times(pcg_ctx *ctx, float *ms, int32_t n);
  *   K2 (conflict rows):    "k2_mode" 1 partner gather, 2 bucket masks, 3 owned masks;
  *                          "own_algo" 0 four-Russians / 1 per-pair masks; "own_direct" 0 forces
  *                          the hash ownership table; "window" row-pass bitmap (ids)
- *   fill:                  "fill_algo" 0 auto, 1 cooperative, 2 merge, 3 lane bitmap, 4 TMA
- *                          runs, 5 block (CTA per row), 6 segmented, 7 bins (counting sort);
+ *   fill:                  "fill_algo" 0 auto, 3 lane bitmap, 5 block (CTA per row),
+ *                          6 segmented, 7 bins (counting sort);
  *                          "blk_threads" "blk_groups" "blk_dcap" "blk_ecap"; "bins_threads"
- *                          "bins_shift" "bins_maxdeg"; "seg_bits" "seg_warps"; "merge_cap"
+ *                          "bins_shift" "bins_maxdeg"; "seg_bits" "seg_warps"
  *   copy-out (pcg_fill):   "d2h_mode" 0 delta gaps (default) / 3 direct / 4 int32 widen;
  *                          "d2h_pipe" 1 (default) fill in pieces overlapping the copy-out,
  *                          "d2h_pieces", "d2h_chunk" (ids), "d2h_threads", "d2h_gap16"

@@ -19,7 +19,22 @@ from .errors import DeviceError
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpicasso_b200.so")
 
-PCG_OK, PCG_E_ARG, PCG_E_CUDA, PCG_E_OOM, PCG_E_COLOR, PCG_E_STATE = range(6)
+PCG_OK, PCG_E_ARG, PCG_E_CUDA, PCG_E_OOM, PCG_E_COLOR, PCG_E_STATE, PCG_E_DUPLICATE = range(7)
+
+
+def dedupe_rows(data: np.ndarray, off, L: int, n: int):
+    """Distinct colors of every list row, as a ragged (data, offsets, 0) CSR (ascending)."""
+    if off is None:
+        off = np.arange(n + 1, dtype=np.int64) * L
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(off))
+    order = np.lexsort((data, rows))
+    d, r = data[order], rows[order]
+    keep = np.ones(d.size, dtype=bool)
+    keep[1:] = (d[1:] != d[:-1]) | (r[1:] != r[:-1])
+    lens = np.bincount(r[keep], minlength=n)
+    new_off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens, out=new_off[1:])
+    return np.ascontiguousarray(d[keep], dtype=np.int64), new_off, 0
 
 
 class Counts(ctypes.Structure):
@@ -185,11 +200,20 @@ class Context:
     def set_inputs(self, words: np.ndarray, num_qubits: int, active: np.ndarray,
                    list_data: np.ndarray, list_off: np.ndarray | None, list_len: int,
                    palette_base: int, palette_size: int):
-        self._keep = (words, active, list_data, list_off)
-        rc = self.lib.pcg_set_inputs(
-            self.h, _ptr(words), int(words.shape[0]), int(words.shape[1]), int(num_qubits),
-            _ptr(active), int(active.size), _ptr(list_data), _ptr(list_off), int(list_len),
-            int(palette_base), int(palette_size))
+        for attempt in range(2):
+            self._keep = (words, active, list_data, list_off)
+            rc = self.lib.pcg_set_inputs(
+                self.h, _ptr(words), int(words.shape[0]), int(words.shape[1]), int(num_qubits),
+                _ptr(active), int(active.size), _ptr(list_data), _ptr(list_off), int(list_len),
+                int(palette_base), int(palette_size))
+            if rc != PCG_E_DUPLICATE or attempt:
+                break
+            # a row names a color twice: the reference's palette mask is a set (driver.py:
+            # 152-172, conflict.py:72-78 ANDs mask rows), so the build sees each row's distinct
+            # colors.  The device flags it during the bucket pass; the rows are deduped here
+            # once and staged again (never happens for lists drawn by assign_random_lists).
+            list_data, list_off, list_len = dedupe_rows(list_data, list_off, list_len,
+                                                        int(active.size))
         self._check(rc, "pcg_set_inputs")
 
     def count(self, shard: int = 0, nshards: int = 1, row_begin: int = 0,

@@ -157,8 +157,7 @@ int pcg_destroy(pcg_ctx *ctx) {
                       &ctx->cubtmp, &ctx->deg, &ctx->degu, &ctx->compact, &ctx->rowoff,
                       &ctx->scal, &ctx->bad, &ctx->members_o, &ctx->offsets_o, &ctx->nbr_o,
                       &ctx->gdeg, &ctx->items, &ctx->eidx, &ctx->bpos, &ctx->bmemp,
-                      &ctx->posof, &ctx->maskoff, &ctx->masks, &ctx->heavy, &ctx->runlen,
-                      &ctx->runoff, &ctx->runs, &ctx->bnd, &ctx->vcolor, &ctx->vkeys,
+                      &ctx->posof, &ctx->maskoff, &ctx->masks, &ctx->bnd, &ctx->vcolor, &ctx->vkeys,
                       &ctx->vkeys2, &ctx->vvals, &ctx->vvals2, &ctx->vcnt, &ctx->voff,
                       &ctx->vpairs};
     for (DevBuf *b : bufs) release(*b);
@@ -203,7 +202,6 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "window")) ctx->window = (int)value;
     else if (!strcmp(key, "fr_ichunk")) ctx->fr_ichunk = (int)value;
     else if (!strcmp(key, "k2_mode")) ctx->k2_mode = (int)value;
-    else if (!strcmp(key, "merge_cap")) ctx->merge_cap = (int)value;
     else if (!strcmp(key, "fill_algo")) ctx->fill_algo = (int)value;
     else if (!strcmp(key, "seg_bits")) ctx->seg_bits = (int)value;
     else if (!strcmp(key, "own_algo")) ctx->own_algo = (int)value;
@@ -285,13 +283,6 @@ struct MaskWords {
         if (c >= P) return 0;
         const int64_t m = bstart[c + 1] - bstart[c];
         return m * ((m + 31) / 32);
-    }
-};
-struct PaddedRun {
-    const int32_t *len;
-    int64_t n;
-    __host__ __device__ int64_t operator()(int64_t e) const {
-        return e < n ? (int64_t)((len[e] + 3) & ~3) : 0;
     }
 };
 __global__ void k_bucket_max(const int32_t *bstart, int64_t P, int32_t *out) {
@@ -468,7 +459,8 @@ static int prep_device(pcg_ctx *ctx) {
                           end_bit, s));
     tr.mark("radix sort");
     PCG_ALLOC(ctx, ctx->bstart, (size_t)(P + 1) * 4);
-    launch_bucket_bounds(ctx->keys2.as<int32_t>(), entries, P, ctx->bstart.as<int32_t>(), s);
+    launch_bucket_bounds(ctx->keys2.as<int32_t>(), ctx->vals2.as<int32_t>(), ctx->rowof.as<int32_t>(),
+                         entries, P, ctx->bstart.as<int32_t>(), ctx->bad.as<int32_t>() + 1, s);
     PCG_CHECK_LAUNCH(ctx);
 
     // padded bucket starts and mask offsets (exclusive scans over P+1 colors)
@@ -508,7 +500,8 @@ static int prep_device(pcg_ctx *ctx) {
     memcpy(&m_max, hs + 8, 4);
     memcpy(&padded_total, hs + 12, 4);
     memcpy(&mask_total, hs + 16, 8);
-    if (bad[1]) return fail(ctx, PCG_E_COLOR, "a list color lies outside the palette");
+    if (bad[1] & 2) return fail(ctx, PCG_E_COLOR, "a list color lies outside the palette");
+    if (bad[1] & 4) return fail(ctx, PCG_E_DUPLICATE, "a color list names the same color twice");
     if (bad[0]) {  // invalid 3-bit codes: exact raw-word predicate
         if (ctx->k1_early_valid) {  // the early K1 read the wrong planes: drop it
             PCG_TRY_CUDA(ctx, cudaEventSynchronize(ctx->k1_done));
@@ -601,52 +594,12 @@ static int prep_device(pcg_ctx *ctx) {
         if (ctx->owned) {
             OwnArgs &o = own;
             PCG_TRY_CUDA(ctx, cudaMemsetAsync(o.overflow, 0, 4, s));
-            const bool want_runs = ctx->fill_algo == 4;  // run lengths only feed the runs fill
-            b.runlen = nullptr;
-            if (want_runs) {
-                PCG_ALLOC(ctx, ctx->runlen, (size_t)entries * 4);
-                PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->runlen.p, 0, (size_t)entries * 4, s));
-                b.runlen = ctx->runlen.as<int32_t>();
-            }
             launch_owned_masks(b, o, ctx->sms, s);
             PCG_CHECK_LAUNCH(ctx);
             // the per-pair mask kernel (own_algo 1) always writes every row
             ctx->prep_lo = o.fr ? o.row_lo : 0;
             ctx->prep_hi = o.fr ? o.row_hi : n_active;
-            int64_t runs_total = 0;
-            if (want_runs) {  // owned partner runs (padded to 4 ids) for the TMA-staged fill
-                PCG_ALLOC(ctx, ctx->runoff, (size_t)(entries + 1) * 8);
-                cub::TransformInputIterator<int64_t, PaddedRun, cub::CountingInputIterator<int64_t>> plen(
-                    cidx, PaddedRun{ctx->runlen.as<int32_t>(), entries});
-                size_t t3 = 0;
-                PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, t3, plen,
-                                                                ctx->runoff.as<int64_t>(), entries + 1, s));
-                PCG_ALLOC(ctx, ctx->cubtmp, t3);
-                PCG_TRY_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->cubtmp.p, t3, plen,
-                                                                ctx->runoff.as<int64_t>(), entries + 1, s));
-                PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&runs_total, ctx->runoff.as<int64_t>() + entries, 8,
-                                                  cudaMemcpyDeviceToHost, s));
-            }
-            ctx->runs_ready = false;
             ctx->own_check = true;  // the overflow flag is read back with the count totals
-            if (want_runs) {
-                int32_t ovf = 0;
-                PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&ovf, o.overflow, 4, cudaMemcpyDeviceToHost, s));
-                PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
-                ctx->own_check = false;
-                if (ovf) ctx->owned = false;  // a color's table overflowed: dedupe path
-            }
-            if (ctx->owned && want_runs &&
-                (size_t)runs_total * 4 < free_b / 3) {
-                PCG_ALLOC(ctx, ctx->runs, (size_t)(runs_total + 4) * 4);
-                RunArgs ra{};
-                ra.runlen = ctx->runlen.as<int32_t>();
-                ra.runoff = ctx->runoff.as<int64_t>();
-                ra.runs = ctx->runs.as<int32_t>();
-                launch_write_runs(b, ra, ctx->sms, s);
-                PCG_CHECK_LAUNCH(ctx);
-                ctx->runs_ready = true;
-            }
         }
         if (!ctx->owned) {
             launch_bucket_masks(b, ctx->sms, s);
@@ -847,12 +800,6 @@ static int32_t pick_window(const pcg_ctx *ctx) {
     if (ctx->window > 0) return (int32_t)round_up(ctx->window, 4096);
     const int64_t w = round_up(std::max<int64_t>(ctx->n, 1), 4096);
     return (int32_t)std::min<int64_t>(w, 32768);
-}
-
-static int32_t coop_window(const pcg_ctx *ctx) {
-    if (ctx->window > 0) return (int32_t)round_up(ctx->window, 4096);
-    const int64_t w = round_up(std::max<int64_t>(ctx->n, 1), 4096);
-    return (int32_t)std::min<int64_t>(w, 131072);
 }
 
 static RowArgs row_args(const pcg_ctx *ctx, int64_t r0, int64_t r1) {
@@ -1714,8 +1661,9 @@ static int d2h_widen(pcg_ctx *ctx, int64_t *dst, const int32_t *src, size_t coun
 }
 
 // Fill pass for rows [r0, r1) into `out` (int64, entry index out_base at out[0]).  Owned
-// masks: warp merge of the disjoint runs, rows longer than the merge buffer go through the
-// bitmap row kernel; otherwise the bitmap row kernel for every row.
+// masks: the bins fill (sparse rows, > 128K ids), the block fill (<= 128K ids) or the
+// segmented fill (dense rows); lists longer than 64 colors and the non-owned mask modes take
+// the lane-per-bucket bitmap row kernel.
 static int fill_rows_device(pcg_ctx *ctx, int64_t r0, int64_t r1, const int32_t *deg,
                             int32_t maxdeg, bool identity, void *out, int64_t out_base,
                             int *launches, bool out64, const int32_t *rows_list) {
@@ -1730,34 +1678,6 @@ static int fill_rows_device(pcg_ctx *ctx, int64_t r0, int64_t r1, const int32_t 
     if (!ctx->owned) {
         *launches += launch_rows(a, true, out64, ctx->sms, s);
         PCG_CHECK_LAUNCH(ctx);
-        return PCG_OK;
-    }
-    if (ctx->runs_ready) {  // TMA-staged owned runs (default)
-        RunArgs r{};
-        r.runlen = ctx->runlen.as<int32_t>();
-        r.runoff = ctx->runoff.as<int64_t>();
-        r.runs = ctx->runs.as<int32_t>();
-        const int capmax = ctx->merge_cap > 0 ? ctx->merge_cap : 4096;
-        r.cap = std::min(capmax, (maxdeg + 3 * ctx->lmax + 31) & ~31);
-        PCG_ALLOC(ctx, ctx->heavy, (size_t)std::max<int64_t>(r1 - r0, 1) * 4);
-        r.heavy = ctx->heavy.as<int32_t>();
-        r.nheavy = reinterpret_cast<int32_t *>(ctx->scal.as<unsigned long long>() + 6);
-        PCG_TRY_CUDA(ctx, cudaMemsetAsync(r.nheavy, 0, 4, s));
-        RowArgs fa = a;
-        fa.window = 16384;
-        *launches += launch_fill_runs(fa, r, out64, ctx->sms, s);
-        PCG_CHECK_LAUNCH(ctx);
-        int32_t nh = 0;
-        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&nh, r.nheavy, 4, cudaMemcpyDeviceToHost, s));
-        PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
-        if (nh > 0) {
-            RowArgs h = a;
-            h.rows_list = r.heavy;
-            h.row_begin = 0;
-            h.row_end = nh;
-            *launches += launch_rows(h, true, out64, ctx->sms, s);
-            PCG_CHECK_LAUNCH(ctx);
-        }
         return PCG_OK;
     }
     // the bins fill (counting sort per row) is the default beyond the block fill's range
@@ -1842,39 +1762,9 @@ static int fill_rows_device(pcg_ctx *ctx, int64_t r0, int64_t r1, const int32_t 
             return PCG_OK;
         }
     }
-    if (ctx->fill_algo == 1) {  // cooperative bitmap fill (experimental)
-        a.window = coop_window(ctx);
-        *launches += launch_fill_coop(a, out64, ctx->sms, s);
-        PCG_CHECK_LAUNCH(ctx);
-        return PCG_OK;
-    }
-    if (ctx->fill_algo != 2) {  // lane-per-bucket bitmap fill (default)
-        *launches += launch_rows(a, true, out64, ctx->sms, s);
-        PCG_CHECK_LAUNCH(ctx);
-        return PCG_OK;
-    }
-    const int cap_max = ctx->merge_cap > 0 ? ctx->merge_cap : 6144;
-    MergeArgs g{};
-    g.cap = std::min(cap_max, std::max(32, (maxdeg + 31) & ~31));
-    PCG_ALLOC(ctx, ctx->heavy, (size_t)std::max<int64_t>(r1 - r0, 1) * 4);
-    g.heavy = ctx->heavy.as<int32_t>();
-    g.nheavy = reinterpret_cast<int32_t *>(ctx->scal.as<unsigned long long>() + 6);
-    PCG_TRY_CUDA(ctx, cudaMemsetAsync(g.nheavy, 0, 4, s));
-    *launches += launch_fill_merge(a, g, out64, ctx->sms, s);
+    // lane-per-bucket bitmap fill: lists longer than 64 colors, rows of 64K+ ids
+    *launches += launch_rows(a, true, out64, ctx->sms, s);
     PCG_CHECK_LAUNCH(ctx);
-    if (maxdeg > g.cap) {
-        int32_t nh = 0;
-        PCG_TRY_CUDA(ctx, cudaMemcpyAsync(&nh, g.nheavy, 4, cudaMemcpyDeviceToHost, s));
-        PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
-        if (nh > 0) {
-            RowArgs h = a;
-            h.rows_list = g.heavy;
-            h.row_begin = 0;
-            h.row_end = nh;
-            *launches += launch_rows(h, true, out64, ctx->sms, s);
-            PCG_CHECK_LAUNCH(ctx);
-        }
-    }
     return PCG_OK;
 }
 

@@ -1,4 +1,4 @@
-// Owned bucket masks (K2a), popcount count pass (K2c) and merge fill pass (K2m).
+// Owned bucket masks (K2a) and the popcount count pass (K2c); the fills are in fillblk.cu / fill.cu / rows.cu.
 //
 // Ownership.  A conflict pair {u, v} is admitted through every color the two lists share;
 // k_owned_masks keeps it only in the commute mask of the SMALLEST shared color.  Then each
@@ -22,7 +22,6 @@ namespace {
 constexpr int OWN_THREADS = 256;
 constexpr int OWN_COLL = 2048;        // collision list capacity
 constexpr int OWN_LCAP = 1024;        // direct ownership: default losers per level (o.lcap)
-constexpr int MERGE_WARPS = 4;
 
 template <int KW>
 struct Vec {
@@ -176,13 +175,6 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_masks(BucketArgs b, OwnAr
             }
         }
         __syncthreads();
-        if (b.runlen) {  // owned partners per member: the run lengths of the fill pass
-            for (int k = tid; k < m; k += OWN_THREADS) {
-                int cnt = 0;
-                for (int w = 0; w < W; ++w) cnt += __popc(out[(int64_t)k * W + w]);
-                b.runlen[b.bstart[c] + k] = cnt;
-            }
-        }
         // reset the table and the chain heads this color touched
         for (int x = 4 * tid; x < HS; x += 4 * OWN_THREADS)
             *reinterpret_cast<uint4 *>(table + x) = make_uint4(0u, 0u, 0u, 0u);
@@ -458,13 +450,6 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
             }
         }
         __syncthreads();
-        if (b.runlen) {  // owned partners per member: the run lengths of the runs fill
-            for (int k = tid; k < m; k += OWN_THREADS) {
-                int cnt = 0;
-                for (int w = 0; w < W; ++w) cnt += __popc(out[(int64_t)k * W + w]);
-                b.runlen[b.bstart[c] + k] = cnt;
-            }
-        }
         // reset the hash table and the chain heads this color touched (direct tags carry the
         // color: nothing to reset)
         if (!o.direct) {
@@ -513,576 +498,6 @@ __global__ void k_count_owned(RowArgs a) {
     }
 }
 
-// ---------------------------------------------------------------------------------------
-// K2m: fill by merging the row's disjoint runs (warp per row, shared memory merge path)
-// ---------------------------------------------------------------------------------------
-__device__ __forceinline__ int merge_split(const int32_t *A, int la, const int32_t *B, int lb,
-                                           int d) {
-    int lo = max(0, d - lb), hi = min(d, la);
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (A[mid] < B[d - 1 - mid]) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
-
-template <typename OutT>
-__global__ void __launch_bounds__(MERGE_WARPS * 32) k_fill_merge(RowArgs a, MergeArgs g) {
-    extern __shared__ __align__(16) int32_t msm[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int cap = g.cap;
-    int32_t *buf0 = msm + (size_t)warp * (2 * cap + 68);
-    int32_t *buf1 = buf0 + cap;
-    int32_t *roff = buf1 + cap;  // up to 33 run offsets (+ padding)
-    OutT *out = reinterpret_cast<OutT *>(a.out);
-    const int64_t gw = blockIdx.x * (int64_t)MERGE_WARPS + warp;
-    const int64_t nw = (int64_t)gridDim.x * MERGE_WARPS;
-    for (int64_t i = a.row_begin + gw; i < a.row_end; i += nw) {
-        const int deg = a.deg[i];
-        if (deg == 0) continue;
-        if (deg > cap) {  // too long for shared memory: the bitmap fill handles it
-            if (lane == 0) g.heavy[atomicAdd(g.nheavy, 1)] = (int32_t)i;
-            continue;
-        }
-        const int64_t lo = a.loff ? a.loff[i] : i * a.L;
-        const int Li = (int)((a.loff ? a.loff[i + 1] : lo + a.L) - lo);
-        // ---- decode: runs of the row's colors, ascending member ids where the owned bit is set
-        int fillv = 0;
-        for (int s = 0; s < Li; ++s) {
-            if (lane == 0) roff[s] = fillv;
-            const int c = a.lrel[lo + s];
-            const int m = a.bstart[c + 1] - a.bstart[c];
-            const int W = (m + 31) >> 5;
-            const uint32_t *row = a.masks + a.maskoff[c] + (int64_t)a.posof[lo + s] * W;
-            const int32_t *mem = a.bmemp + a.bpos[c];
-            for (int w0 = 0; w0 < W; w0 += 8) {
-                int32_t v[8];
-                uint32_t mw[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int w = w0 + u;
-                    mw[u] = w < W ? __ldg(row + w) : 0u;
-                    v[u] = (w < W && 32 * w + lane < m) ? __ldg(mem + 32 * w + lane) : 0;
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const bool adm = (mw[u] >> lane) & 1u;
-                    const uint32_t bal = __ballot_sync(0xffffffffu, adm);
-                    if (adm) buf0[fillv + __popc(bal & ((1u << lane) - 1u))] = v[u];
-                    fillv += __popc(bal);
-                }
-            }
-        }
-        if (lane == 0) roff[Li] = fillv;
-        __syncwarp();
-        // ---- merge tree: pairs of runs per level, merge path per lane
-        int R = Li;
-        int32_t *src = buf0, *dst = buf1;
-        while (R > 1) {
-            const int total = roff[R];
-            const int olo = (int)((int64_t)total * lane / 32);
-            const int ohi = (int)((int64_t)total * (lane + 1) / 32);
-            // each lane finds the pair(s) its output range falls in and merges on its own,
-            // so all lanes run their (equal-length) merge loops at the same time
-            int o = olo;
-            while (o < ohi) {
-                int p = 0;  // last pair whose output starts at or before o
-                for (int q = 1; 2 * q < R; ++q)
-                    if (roff[2 * q] <= o) p = q;
-                const int a0 = roff[2 * p], a1 = roff[min(2 * p + 1, R)];
-                const int e = roff[min(2 * p + 2, R)];
-                const int s1 = min(ohi, e);
-                const int32_t *A = src + a0, *B = src + a1;
-                const int la = a1 - a0, lb = e - a1;
-                int ia = merge_split(A, la, B, lb, o - a0);
-                int ib = (o - a0) - ia;
-                int32_t xa = ia < la ? A[ia] : INT_MAX;
-                int32_t xb = ib < lb ? B[ib] : INT_MAX;
-                for (; o < s1; ++o) {
-                    if (xa < xb) {
-                        dst[o] = xa;
-                        ++ia;
-                        xa = ia < la ? A[ia] : INT_MAX;
-                    } else {
-                        dst[o] = xb;
-                        ++ib;
-                        xb = ib < lb ? B[ib] : INT_MAX;
-                    }
-                }
-            }
-            __syncwarp();
-            const int R2 = (R + 1) >> 1;
-            int nr = 0;
-            if (lane <= R2) nr = roff[min(2 * lane, R)];
-            __syncwarp();
-            if (lane <= R2) roff[lane] = nr;
-            __syncwarp();
-            R = R2;
-            int32_t *t = src;
-            src = dst;
-            dst = t;
-        }
-        // ---- coalesced store (compact ids when some rows have no conflicts)
-        const int64_t base = a.rowoff[i] - a.out_base;
-        for (int k = lane; k < deg; k += 32) {
-            const int32_t j = src[k];
-            out[base + k] = (OutT)(a.compact ? a.compact[j] : j);
-        }
-        __syncwarp();
-    }
-}
-
-// ---------------------------------------------------------------------------------------
-// K2f: cooperative bitmap fill with owned masks (warp per row).  The warp walks one color
-// bucket at a time: 32 consecutive members per coalesced load (a whole bucket slice per
-// batch, all loads in flight), admitted members (owned-mask bit) compacted with a ballot, so
-// the ids in lanes 0..k-1 ascend.  Equal bitmap words can then only sit in neighbouring
-// lanes: two shuffles find them; unique words get a plain read-or-write, shared ones an
-// atomic.  Rows come out of the interleaved harvest in ascending order.
-// ---------------------------------------------------------------------------------------
-constexpr int COOP_WARPS = 8;
-constexpr int COOP_BATCH = 8;   // 32-member chunks per load batch
-constexpr int COOP_STAGE = 1024;
-constexpr int UNR_F = 8;    // run elements per lane per round (runs fill)
-
-__device__ __forceinline__ uint32_t c_lds(uint32_t addr) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
-    return v;
-}
-__device__ __forceinline__ void c_sts(uint32_t addr, uint32_t v) {
-    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint4 c_lds4(uint32_t addr) {
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "r"(addr)
-                 : "memory");
-    return v;
-}
-__device__ __forceinline__ void c_sts4(uint32_t addr, uint4 v) {
-    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y),
-                 "r"(v.z), "r"(v.w)
-                 : "memory");
-}
-__device__ __forceinline__ int c_scan(int v, int lane, int &total) {
-    int x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    total = __shfl_sync(0xffffffffu, x, 31);
-    return x - v;
-}
-
-template <typename OutT>
-__global__ void __launch_bounds__(COOP_WARPS * 32) k_fill_coop(RowArgs a) {
-    extern __shared__ __align__(16) uint32_t csm[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int WW = a.window >> 5;
-    uint32_t *bm = csm + (size_t)warp * (WW + COOP_STAGE + 4 * a.slot_cap);
-    int32_t *stage = reinterpret_cast<int32_t *>(bm + WW);
-    int32_t *st = stage + COOP_STAGE;       // cursor
-    int32_t *sm = st + a.slot_cap;          // bucket size
-    int32_t *sb = sm + a.slot_cap;          // bucket base in bmemp
-    int32_t *sw = sb + a.slot_cap;          // mask row offset (words) relative to masks
-    const uint32_t bm_s = (uint32_t)__cvta_generic_to_shared(bm);
-    for (int k = lane; k < WW; k += 32) bm[k] = 0u;
-    __syncwarp();
-    OutT *out = reinterpret_cast<OutT *>(a.out);
-    const uint32_t lt = (1u << lane) - 1u;
-    const int64_t stride = (int64_t)gridDim.x * COOP_WARPS;
-    for (int64_t ri = a.row_begin + (int64_t)blockIdx.x * COOP_WARPS + warp; ri < a.row_end;
-         ri += stride) {
-        const int64_t i = a.rows_list ? (int64_t)a.rows_list[ri] : ri;
-        if (a.deg[i] == 0) continue;
-        const int64_t lo = a.loff ? a.loff[i] : i * a.L;
-        const int Li = (int)((a.loff ? a.loff[i + 1] : lo + a.L) - lo);
-        for (int s = lane; s < Li; s += 32) {
-            const int c = a.lrel[lo + s];
-            const int m = a.bstart[c + 1] - a.bstart[c];
-            st[s] = 0;
-            sm[s] = m;
-            sb[s] = a.bpos[c];
-            sw[s] = (int32_t)(a.maskoff[c] + (int64_t)a.posof[lo + s] * ((m + 31) >> 5));
-        }
-        __syncwarp();
-        int64_t outpos = a.rowoff[i] - a.out_base;
-        for (int32_t w0 = 0; w0 < a.n; w0 += a.window) {
-            const int32_t w1 = (int32_t)min((int64_t)a.n, (int64_t)w0 + a.window);
-            for (int s = 0; s < Li; ++s) {
-                int t = st[s];
-                const int m = sm[s];
-                if (t >= m) continue;
-                const int32_t *mem = a.bmemp + sb[s];
-                const uint32_t *mrow = a.masks + sw[s];
-                bool more = true;
-                while (more) {
-                    int32_t v[COOP_BATCH];
-                    uint32_t mw[COOP_BATCH];
-#pragma unroll
-                    for (int u = 0; u < COOP_BATCH; ++u) {
-                        const int p = t + 32 * u + lane;
-                        const bool ok = p < m;
-                        v[u] = ok ? __ldg(mem + p) : INT_MAX;
-                        mw[u] = ok ? __ldg(mrow + (p >> 5)) : 0u;
-                    }
-#pragma unroll
-                    for (int u = 0; u < COOP_BATCH; ++u) {
-                        if (!more) break;
-                        const int p = t + lane;
-                        const bool in = v[u] < w1;
-                        const int k = __popc(__ballot_sync(0xffffffffu, in));
-                        const bool adm = in && ((mw[u] >> (p & 31)) & 1u);
-                        const uint32_t am = __ballot_sync(0xffffffffu, adm);
-                        const int na = __popc(am);
-                        // lane l < na takes the l-th admitted id (ascending)
-                        const int src = lane < na ? __fns(am, 0, lane + 1) : 0;
-                        const int32_t id = __shfl_sync(0xffffffffu, v[u], src);
-                        const bool act = lane < na;
-                        const uint32_t off = (uint32_t)(id - w0);
-                        const int32_t word = act ? (int32_t)(off >> 5) : -1 - lane;
-                        const int32_t up = __shfl_up_sync(0xffffffffu, word, 1);
-                        const int32_t dn = __shfl_down_sync(0xffffffffu, word, 1);
-                        const bool dup = act && ((lane > 0 && up == word) || (lane < 31 && dn == word));
-                        const uint32_t addr = bm_s + ((off >> 5) << 2);
-                        const uint32_t bit = 1u << (off & 31);
-                        if (act && !dup) c_sts(addr, c_lds(addr) | bit);
-                        if (__any_sync(0xffffffffu, dup)) {
-                            if (dup)
-                                atomicOr(reinterpret_cast<uint32_t *>(__cvta_shared_to_generic(addr)), bit);
-                        }
-                        t += k;
-                        more = (k == 32) && t < m;
-                    }
-                }
-                if (lane == 0) st[s] = t;
-                __syncwarp();
-            }
-            // ---- harvest: interleaved 16-byte chunks, ids staged then stored coalesced
-            const int rows = WW >> 7;
-            int fillv = 0;
-            for (int it = 0; it < rows; ++it) {
-                const int c = it * 32 + lane;
-                const uint32_t addr = bm_s + (uint32_t)c * 16u;
-                const uint4 q4 = c_lds4(addr);
-                const int nb = __popc(q4.x) + __popc(q4.y) + __popc(q4.z) + __popc(q4.w);
-                int total;
-                const int base = c_scan(nb, lane, total);
-                if (total == 0) continue;
-                const bool direct = total > COOP_STAGE;
-                if (fillv > 0 && (direct || fillv + total > COOP_STAGE)) {
-                    __syncwarp();
-                    for (int k = lane; k < fillv; k += 32) out[outpos + k] = (OutT)stage[k];
-                    outpos += fillv;
-                    fillv = 0;
-                    __syncwarp();
-                }
-                if (nb) {
-                    c_sts4(addr, make_uint4(0u, 0u, 0u, 0u));
-                    int64_t pos = direct ? outpos + base : fillv + base;
-                    const uint32_t wv[4] = {q4.x, q4.y, q4.z, q4.w};
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        uint32_t wd = wv[u];
-                        const int32_t jb = w0 + c * 128 + 32 * u;
-                        while (wd) {
-                            const int bb = __ffs(wd) - 1;
-                            wd &= wd - 1u;
-                            const int32_t j = jb + bb;
-                            const int32_t val = a.compact ? a.compact[j] : j;
-                            if (direct) out[pos++] = (OutT)val;
-                            else stage[pos++] = val;
-                        }
-                    }
-                }
-                if (direct) outpos += total;
-                else fillv += total;
-            }
-            __syncwarp();
-            for (int k = lane; k < fillv; k += 32) out[outpos + k] = (OutT)stage[k];
-            outpos += fillv;
-            __syncwarp();
-        }
-    }
-}
-
-template <typename OutT>
-int run_coop(const RowArgs &a, int sms, cudaStream_t s) {
-    const size_t per_warp = (size_t)((a.window >> 5) + COOP_STAGE + 4 * a.slot_cap) * 4;
-    const size_t smem = per_warp * COOP_WARPS;
-    allow_max_smem(k_fill_coop<OutT>);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fill_coop<OutT>, COOP_WARPS * 32, smem);
-    if (per_sm < 1) per_sm = 1;
-    const int64_t rows = a.row_end - a.row_begin;
-    const int64_t grid = std::max<int64_t>(
-        1, std::min<int64_t>((int64_t)per_sm * sms, (rows + COOP_WARPS - 1) / COOP_WARPS));
-    k_fill_coop<OutT><<<(unsigned)grid, COOP_WARPS * 32, smem, s>>>(a);
-    return 1;
-}
-
-
-// ---------------------------------------------------------------------------------------
-// Owned partner runs: for every bucket entry (color c, member k) the ascending ids of its
-// owned admitted partners, at a 16-byte aligned offset (TMA bulk copies need it).  Warp per
-// color; 32 bucket positions per step, ballot-compacted, coalesced stores.
-// ---------------------------------------------------------------------------------------
-constexpr int RUN_WARPS = 8;
-
-__global__ void __launch_bounds__(RUN_WARPS * 32) k_write_runs(BucketArgs b, RunArgs r) {
-    const int lane = threadIdx.x & 31;
-    const int64_t gw = blockIdx.x * (int64_t)RUN_WARPS + (threadIdx.x >> 5);
-    const int64_t nw = (int64_t)gridDim.x * RUN_WARPS;
-    for (int64_t c = gw; c < b.P; c += nw) {
-        const int m = b.bstart[c + 1] - b.bstart[c];
-        if (m < 2) continue;
-        const int W = (m + 31) >> 5;
-        const int32_t *mem = b.bmemp + b.bpos[c];
-        const uint32_t *mk = b.masks + b.maskoff[c];
-        for (int k = 0; k < m; ++k) {
-            const int64_t pos = b.bstart[c] + k;
-            int32_t *dst = r.runs + r.runoff[pos];
-            int cnt = 0;
-            for (int w = 0; w < W; ++w) {
-                const uint32_t word = __ldg(mk + (int64_t)k * W + w);  // broadcast
-                if (word == 0u) continue;
-                const int t = 32 * w + lane;
-                const bool keep = (word >> lane) & 1u;
-                const int32_t id = keep ? __ldg(mem + t) : 0;
-                if (keep) dst[cnt + __popc(word & ((1u << lane) - 1u))] = id;
-                cnt += __popc(word);
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------------------
-// Fill from owned runs (warp per row).  Lanes s < L issue one TMA bulk copy each (their
-// run) into the warp's shared staging buffer, completing on an mbarrier; the next row is
-// staged into the other buffer while this one is sorted.  Lanes then walk their run in
-// shared memory and mark partners in the window bitmap; the interleaved harvest emits the
-// row in ascending order (runs are disjoint: no dedupe needed).
-// ---------------------------------------------------------------------------------------
-constexpr int FR_W = 4;  // warps per block
-
-__device__ __forceinline__ void mbar_init(uint32_t mbar) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
-}
-__device__ __forceinline__ void mbar_expect(uint32_t mbar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "W%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "\t@!p bra W%=;\n\t}" ::"r"(mbar),
-        "r"(phase)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-        "l"(src), "r"(bytes), "r"(mbar)
-        : "memory");
-}
-
-struct RowStage {
-    int off, len;     // this lane's run inside the buffer (ids)
-    int deg;          // row total (warp-uniform)
-};
-
-// Issue the TMA copies of row i into buffer `buf_s` (shared byte address).  Returns the
-// lane's run geometry.  deg == -1 marks a row too long for the buffer.
-__device__ __forceinline__ RowStage stage_row(const RowArgs &a, const RunArgs &r, int64_t i,
-                                              uint32_t buf_s, uint32_t mbar, int lane) {
-    RowStage g{0, 0, 0};
-    const int64_t lo = a.loff ? a.loff[i] : i * a.L;
-    const int Li = (int)((a.loff ? a.loff[i + 1] : lo + a.L) - lo);
-    int64_t src = 0;
-    int len = 0;
-    if (lane < Li) {
-        const int c = a.lrel[lo + lane];
-        const int64_t pos = a.bstart[c] + a.posof[lo + lane];
-        len = r.runlen[pos];
-        src = r.runoff[pos];
-    }
-    const int padded = (len + 3) & ~3;
-    int total;
-    int x = padded;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    total = __shfl_sync(0xffffffffu, x, 31);
-    const int off = x - padded;
-    g.off = off;
-    g.len = len;
-    g.deg = total > r.cap ? -1 : total;
-    if (g.deg > 0) {
-        if (lane == 0) mbar_expect(mbar, (uint32_t)total * 4u);
-        __syncwarp();
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (padded > 0) tma_load(buf_s + (uint32_t)off * 4u, r.runs + src, (uint32_t)padded * 4u, mbar);
-    }
-    return g;
-}
-
-template <typename OutT>
-__global__ void __launch_bounds__(FR_W * 32) k_fill_runs(RowArgs a, RunArgs r) {
-    extern __shared__ __align__(16) uint32_t fsm[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int WW = a.window >> 5;
-    const size_t per_warp = (size_t)2 * r.cap + WW + 32 + COOP_STAGE + 4;
-    uint32_t *base = fsm + (size_t)warp * per_warp;
-    int32_t *buf0 = reinterpret_cast<int32_t *>(base);
-    uint32_t *bm = base + 2 * r.cap;
-    int32_t *stage = reinterpret_cast<int32_t *>(bm + WW + 32);
-    uint64_t *mb = reinterpret_cast<uint64_t *>(stage + COOP_STAGE);
-    const uint32_t bufs_s = (uint32_t)__cvta_generic_to_shared(buf0);
-    const uint32_t bm_s = (uint32_t)__cvta_generic_to_shared(bm);
-    const uint32_t dummy_s = bm_s + (uint32_t)(WW + lane) * 4u;
-    const uint32_t mb_s = (uint32_t)__cvta_generic_to_shared(mb);
-    for (int k = lane; k < WW; k += 32) bm[k] = 0u;
-    if (lane == 0) {
-        mbar_init(mb_s);
-        mbar_init(mb_s + 8);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncwarp();
-    OutT *out = reinterpret_cast<OutT *>(a.out);
-    const int64_t stride = (int64_t)gridDim.x * FR_W;
-    int64_t ri = a.row_begin + (int64_t)blockIdx.x * FR_W + warp;
-    uint32_t phase[2] = {0u, 0u};
-    int b = 0;
-    RowStage cur{0, 0, 0};
-    if (ri < a.row_end) cur = stage_row(a, r, ri, bufs_s, mb_s, lane);
-    for (; ri < a.row_end; ri += stride) {
-        const int64_t i = ri;
-        // prefetch the next row into the other buffer
-        RowStage nxt{0, 0, 0};
-        const int64_t rn = ri + stride;
-        if (rn < a.row_end)
-            nxt = stage_row(a, r, rn, bufs_s + (uint32_t)((b ^ 1) * r.cap) * 4u, mb_s + 8 * (b ^ 1), lane);
-        if (cur.deg < 0) {  // too long for the staging buffer: bitmap fallback pass
-            if (lane == 0) r.heavy[atomicAdd(r.nheavy, 1)] = (int32_t)i;
-        } else if (cur.deg > 0) {
-            mbar_wait(mb_s + 8 * b, phase[b]);
-            phase[b] ^= 1u;
-            const int32_t *buf = buf0 + b * r.cap;
-            int t = 0;
-            int64_t outpos = a.rowoff[i] - a.out_base;
-            for (int32_t w0 = 0; w0 < a.n; w0 += a.window) {
-                const int32_t w1 = (int32_t)min((int64_t)a.n, (int64_t)w0 + a.window);
-                bool go = t < cur.len;
-                while (__any_sync(0xffffffffu, go)) {
-                    uint32_t addr[UNR_F], bit[UNR_F];
-                    int k = 0;
-#pragma unroll
-                    for (int u = 0; u < UNR_F; ++u) {
-                        const int32_t v = (go && t + u < cur.len) ? buf[cur.off + t + u] : INT_MAX;
-                        const bool in = v < w1;
-                        k += in ? 1 : 0;
-                        const uint32_t off = (uint32_t)(v - w0);
-                        addr[u] = in ? bm_s + ((off >> 5) << 2) : dummy_s;
-                        bit[u] = in ? (1u << (off & 31)) : 0u;
-                    }
-                    t += k;
-                    go = go && k == UNR_F && t < cur.len;
-                    // mark (plain RMW + verify; atomics only for lost bits)
-                    uint32_t old[UNR_F];
-#pragma unroll
-                    for (int u = 0; u < UNR_F; ++u) old[u] = bit[u] ? c_lds(addr[u]) : 0u;
-#pragma unroll
-                    for (int u = 0; u < UNR_F; ++u)
-                        if (bit[u]) c_sts(addr[u], old[u] | bit[u]);
-                    __syncwarp();
-                    uint32_t lost = 0u;
-#pragma unroll
-                    for (int u = 0; u < UNR_F; ++u) {
-                        old[u] = bit[u] ? (bit[u] & ~c_lds(addr[u])) : 0u;
-                        lost |= old[u];
-                    }
-                    if (__any_sync(0xffffffffu, lost != 0u)) {
-#pragma unroll
-                        for (int u = 0; u < UNR_F; ++u)
-                            if (old[u])
-                                atomicOr(reinterpret_cast<uint32_t *>(__cvta_shared_to_generic(addr[u])), old[u]);
-                    }
-                    __syncwarp();
-                }
-                // harvest: interleaved chunks, staged, coalesced stores
-                const int rows = WW >> 7;
-                int fillv = 0;
-                for (int it = 0; it < rows; ++it) {
-                    const int cc = it * 32 + lane;
-                    const uint32_t ad = bm_s + (uint32_t)cc * 16u;
-                    const uint4 q4 = c_lds4(ad);
-                    const int nb = __popc(q4.x) + __popc(q4.y) + __popc(q4.z) + __popc(q4.w);
-                    int total;
-                    const int bse = c_scan(nb, lane, total);
-                    if (total == 0) continue;
-                    const bool direct = total > COOP_STAGE;
-                    if (fillv > 0 && (direct || fillv + total > COOP_STAGE)) {
-                        __syncwarp();
-                        for (int q = lane; q < fillv; q += 32) out[outpos + q] = (OutT)stage[q];
-                        outpos += fillv;
-                        fillv = 0;
-                        __syncwarp();
-                    }
-                    if (nb) {
-                        c_sts4(ad, make_uint4(0u, 0u, 0u, 0u));
-                        int64_t pos = direct ? outpos + bse : fillv + bse;
-                        const uint32_t wv[4] = {q4.x, q4.y, q4.z, q4.w};
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            uint32_t wd = wv[u];
-                            const int32_t jb = w0 + cc * 128 + 32 * u;
-                            while (wd) {
-                                const int bb = __ffs(wd) - 1;
-                                wd &= wd - 1u;
-                                const int32_t j = jb + bb;
-                                const int32_t val = a.compact ? a.compact[j] : j;
-                                if (direct) out[pos++] = (OutT)val;
-                                else stage[pos++] = val;
-                            }
-                        }
-                    }
-                    if (direct) outpos += total;
-                    else fillv += total;
-                }
-                __syncwarp();
-                for (int q = lane; q < fillv; q += 32) out[outpos + q] = (OutT)stage[q];
-                outpos += fillv;
-                __syncwarp();
-                if (!__any_sync(0xffffffffu, t < cur.len)) break;  // row done before n
-            }
-        }
-        __syncwarp();
-        cur = nxt;
-        b ^= 1;
-    }
-}
-
-template <typename OutT>
-int run_fill_runs(const RowArgs &a, const RunArgs &r, int sms, cudaStream_t s) {
-    const size_t per_warp = ((size_t)2 * r.cap + (a.window >> 5) + 32 + COOP_STAGE + 4) * 4;
-    const size_t smem = per_warp * FR_W;
-    allow_max_smem(k_fill_runs<OutT>);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fill_runs<OutT>, FR_W * 32, smem);
-    if (per_sm < 1) per_sm = 1;
-    const int64_t rows = a.row_end - a.row_begin;
-    const int64_t grid = std::max<int64_t>(
-        1, std::min<int64_t>((int64_t)per_sm * sms, (rows + FR_W - 1) / FR_W));
-    k_fill_runs<OutT><<<(unsigned)grid, FR_W * 32, smem, s>>>(a, r);
-    return 1;
-}
-
 size_t owned_smem(const OwnArgs &o, int kw) {
     return (size_t)(o.hash_slots + o.hash_slots / 2 + 2 * OWN_COLL + o.m_cap + (size_t)o.m_cap * kw) * 4;
 }
@@ -1116,20 +531,6 @@ int run_owned_fr(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s)
     if (per_sm < 1) per_sm = 1;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * sms * 4, b.P));
     k_owned_fr<KW><<<(unsigned)grid, OWN_THREADS, smem, s>>>(b, o);
-    return 1;
-}
-
-template <typename OutT>
-int run_merge(const RowArgs &a, const MergeArgs &g, int sms, cudaStream_t s) {
-    const size_t smem = (size_t)MERGE_WARPS * (2 * g.cap + 68) * 4;
-    allow_max_smem(k_fill_merge<OutT>);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fill_merge<OutT>, MERGE_WARPS * 32, smem);
-    if (per_sm < 1) per_sm = 1;
-    const int64_t rows = a.row_end - a.row_begin;
-    const int64_t grid = std::max<int64_t>(
-        1, std::min<int64_t>((int64_t)per_sm * sms, (rows + MERGE_WARPS - 1) / MERGE_WARPS));
-    k_fill_merge<OutT><<<(unsigned)grid, MERGE_WARPS * 32, smem, s>>>(a, g);
     return 1;
 }
 
@@ -1167,30 +568,6 @@ int launch_count_owned(const RowArgs &a, int sms, cudaStream_t s) {
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, (int64_t)sms * 16));
     k_count_owned<<<(unsigned)grid, 256, 0, s>>>(a);
     return 1;
-}
-
-int launch_fill_merge(const RowArgs &a, const MergeArgs &g, bool out64, int sms, cudaStream_t s) {
-    if (a.row_end <= a.row_begin) return 0;
-    return out64 ? run_merge<int64_t>(a, g, sms, s) : run_merge<int32_t>(a, g, sms, s);
-}
-
-int merge_smem_bytes(int cap) { return MERGE_WARPS * (2 * cap + 68) * 4; }
-
-int launch_write_runs(const BucketArgs &b, const RunArgs &r, int sms, cudaStream_t s) {
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((b.P + RUN_WARPS - 1) / RUN_WARPS,
-                                                                (int64_t)sms * 8));
-    k_write_runs<<<(unsigned)grid, RUN_WARPS * 32, 0, s>>>(b, r);
-    return 1;
-}
-
-int launch_fill_runs(const RowArgs &a, const RunArgs &r, bool out64, int sms, cudaStream_t s) {
-    if (a.row_end <= a.row_begin) return 0;
-    return out64 ? run_fill_runs<int64_t>(a, r, sms, s) : run_fill_runs<int32_t>(a, r, sms, s);
-}
-
-int launch_fill_coop(const RowArgs &a, bool out64, int sms, cudaStream_t s) {
-    if (a.row_end <= a.row_begin) return 0;
-    return out64 ? run_coop<int64_t>(a, sms, s) : run_coop<int32_t>(a, sms, s);
 }
 
 }  // namespace pcg

@@ -105,15 +105,6 @@ struct OwnArgs {
                              // (a sharded build's own rows; other rows are left unwritten)
 };
 
-struct RunArgs {
-    const int32_t *runlen;    // owned partners per sorted position (bucket entry)
-    const int64_t *runoff;    // 4-aligned offset of each entry's run in `runs`
-    int32_t *runs;            // out of k_write_runs: ascending partner ids per entry
-    int32_t cap;              // fill: ids per staging buffer (per warp, x2)
-    int32_t *heavy;           // fill: rows whose runs do not fit the staging buffer
-    int32_t *nheavy;
-};
-
 struct SegArgs {
     int32_t wb;            // window bits per warp bitmap (1024 * S)
     int32_t nwin;          // windows per row
@@ -145,12 +136,6 @@ struct BinArgs {
     int32_t lcap;          // color slots (>= longest list)
 };
 
-struct MergeArgs {
-    int32_t cap;           // ids per warp buffer; longer rows go to the bitmap fill
-    int32_t *heavy;        // out: rows longer than cap
-    int32_t *nheavy;       // out: their count
-};
-
 struct BucketArgs {
     int64_t P;
     const int32_t *bstart;    // (P+1) bucket bounds in the sorted entry array
@@ -162,7 +147,6 @@ struct BucketArgs {
     int32_t *bmem;            // out: unpadded members (direct mode), may be null
     int32_t *posof;           // out: position of each entry in its bucket
     uint32_t *masks;          // out: commute masks
-    int32_t *runlen;          // out (owned mode): popcount of every mask row, by sorted position
     const uint32_t *A;
     const uint32_t *B;
     int32_t kw;
@@ -175,8 +159,8 @@ int launch_encode(const uint64_t *words, int32_t nwords, const int64_t *active, 
 int launch_lists(const int64_t *lists, const int64_t *loff, int64_t n, int32_t L,
                  int64_t entries, int64_t base, int64_t P, int32_t *lrel, int32_t *row_of,
                  int32_t *bad, cudaStream_t s);
-int launch_bucket_bounds(const int32_t *sorted_colors, int64_t entries, int64_t P,
-                         int32_t *bstart, cudaStream_t s);
+int launch_bucket_bounds(const int32_t *sorted_colors, const int32_t *eidx, const int32_t *row_of,
+                         int64_t entries, int64_t P, int32_t *bstart, int32_t *bad, cudaStream_t s);
 int launch_commute_direct(const uint32_t *A, const uint32_t *B, int32_t kw, int64_t npad,
                           int64_t tile0, int64_t tile1, unsigned long long *anti, int sms,
                           cudaStream_t s);
@@ -202,13 +186,8 @@ int launch_bucket_masks(const BucketArgs &b, int sms, cudaStream_t s);
 size_t owned_masks_smem(const OwnArgs &o, int kw);
 int launch_owned_masks(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s);
 int launch_count_owned(const RowArgs &a, int sms, cudaStream_t s);
-int launch_fill_merge(const RowArgs &a, const MergeArgs &g, bool out64, int sms, cudaStream_t s);
-int merge_smem_bytes(int cap);
 int launch_assign_lists(const int64_t *active, int64_t n, uint64_t base_key, int64_t P, int L,
                         int64_t palette_base, int64_t *out, cudaStream_t s);
-int launch_write_runs(const BucketArgs &b, const RunArgs &r, int sms, cudaStream_t s);
-int launch_fill_runs(const RowArgs &a, const RunArgs &r, bool out64, int sms, cudaStream_t s);
-int launch_fill_coop(const RowArgs &a, bool out64, int sms, cudaStream_t s);
 void seg_geometry(int64_t n, int64_t max_bits, int32_t *wb, int32_t *nwin, int32_t *seg);
 int launch_window_bounds(const int32_t *bstart, const int32_t *bpos, const int32_t *bmemp,
                          int64_t P, int nwin, int32_t wb, int32_t *bnd, cudaStream_t s);
@@ -258,17 +237,16 @@ struct pcg_ctx {
     bool h_wide = false;  // the staged H offsets are in the wide kernel's format
     int window = 0;     // K2 window bits (0 auto)
     int fr_ichunk = 0;  // four-Russians i-chunk (0 auto)
-    int merge_cap = 0;  // fill-merge buffer cap (0 auto; testing knob)
     int fill_algo = 0;  // owned masks: 0 auto (block fill up to 128K ids, else the bins fill
                         // when the longest row fits its list (16K ids), else segmented), 7 bins fill
                         // (counting sort per row), 5 block fill (CTA per row), 6 segmented fill (warp-decoded words,
-                        // lane-segment harvest), 3 lane-per-bucket bitmap fill,
-                        // 1 cooperative bitmap, 2 merge, 4 TMA-staged owned runs
+                        // lane-segment harvest), 3 lane-per-bucket bitmap fill (also the fill of
+                        // lists longer than 64 colors and of the non-owned mask modes)
     int seg_bits = 0;   // segmented fill: max window bits per warp (0 auto)
     int seg_warps = 0;  // segmented fill: warps per block (0 auto)
     int own_algo = 0;   // owned masks: 0 four-Russians tables (when kw allows), 1 per-pair
     int own_direct = 1; // ownership: 1 direct-mapped color table when P is small, 0 hash
-    int k2_mode = 0;    // 0 auto, 1 partner gathers, 2 bucket masks + bitmap dedupe, 3 owned masks + merge
+    int k2_mode = 0;    // 0 auto, 1 partner gathers, 2 bucket masks + bitmap dedupe, 3 owned masks
 
     // state of the last count
     bool counted = false;
@@ -284,11 +262,10 @@ struct pcg_ctx {
     // device buffers
     pcg::DevBuf words, active, lists64, loff, A, B, H, lrel, rowof, keys2, vals2, bstart,
         cubtmp, deg, degu, compact, rowoff, scal, bad, members_o, offsets_o, nbr_o, gdeg, items,
-        eidx, bpos, bmemp, posof, maskoff, masks, heavy, runlen, runoff, runs;
+        eidx, bpos, bmemp, posof, maskoff, masks;
     int prep_launches = 0;
     bool masked = false;  // K2 uses bucket masks (K2a/K2b) instead of partner gathers
     bool owned = false;   // masks keep each pair only in its smallest shared color
-    bool runs_ready = false;  // owned partner runs materialised (TMA-staged fill)
     int32_t maxdeg = 0;
     int32_t m_max = 0;        // largest color bucket of the staged build
     size_t free_mem = 0;      // device free memory, queried once per context

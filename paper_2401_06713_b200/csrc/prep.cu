@@ -83,7 +83,7 @@ __global__ void k_lists(const int64_t *__restrict__ lists, const int64_t *__rest
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= entries) return;
     const int64_t rel = lists[e] - base;
-    if (rel < 0 || rel >= P) atomicExch(bad, 2);
+    if (rel < 0 || rel >= P) atomicOr(bad, 2);
     lrel[e] = static_cast<int32_t>(rel < 0 || rel >= P ? 0 : rel);
     int64_t r;
     if (loff == nullptr) {
@@ -99,17 +99,20 @@ __global__ void k_lists(const int64_t *__restrict__ lists, const int64_t *__rest
     row_of[e] = static_cast<int32_t>(r);
 }
 
-// bstart[c] = first position of color c in the sorted color array (lower bound), c in [0,P].
-__global__ void k_bucket_bounds(const int32_t *__restrict__ sorted, int64_t entries, int64_t P,
-                                int32_t *__restrict__ bstart) {
-    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c > P) return;
-    int64_t lo = 0, hi = entries;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (sorted[mid] < c) lo = mid + 1; else hi = mid;
-    }
-    bstart[c] = static_cast<int32_t>(lo);
+// bstart[c] = first position of color c in the sorted color array (lower bound), c in [0,P]:
+// one thread per sorted entry writes the starts of the colors between its predecessor's color
+// and its own (coalesced; no search).  A color listed twice in one row shows up as two
+// adjacent entries of one bucket with the same row (the sort is stable in entry order): flag 4.
+__global__ void k_bucket_bounds(const int32_t *__restrict__ sorted, const int32_t *__restrict__ eidx,
+                                const int32_t *__restrict__ row_of, int64_t entries, int64_t P,
+                                int32_t *__restrict__ bstart, int32_t *__restrict__ bad) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e > entries) return;
+    const int64_t prev = e > 0 ? sorted[e - 1] : -1;
+    const int64_t cur = e < entries ? sorted[e] : P + 1;
+    for (int64_t c = prev + 1; c <= cur && c <= P; ++c) bstart[c] = static_cast<int32_t>(e);
+    if (e > 0 && e < entries && prev == cur && row_of[eidx[e]] == row_of[eidx[e - 1]])
+        atomicOr(bad, 4);
 }
 
 }  // namespace
@@ -134,11 +137,11 @@ int launch_lists(const int64_t *lists, const int64_t *loff, int64_t n, int32_t L
     return 1;
 }
 
-int launch_bucket_bounds(const int32_t *sorted_colors, int64_t entries, int64_t P,
-                         int32_t *bstart, cudaStream_t s) {
+int launch_bucket_bounds(const int32_t *sorted_colors, const int32_t *eidx, const int32_t *row_of,
+                         int64_t entries, int64_t P, int32_t *bstart, int32_t *bad, cudaStream_t s) {
     const int tb = 256;
-    k_bucket_bounds<<<(unsigned)((P + 1 + tb - 1) / tb), tb, 0, s>>>(sorted_colors, entries, P,
-                                                                     bstart);
+    k_bucket_bounds<<<(unsigned)((entries + 1 + tb - 1) / tb), tb, 0, s>>>(sorted_colors, eidx, row_of,
+                                                                         entries, P, bstart, bad);
     return 1;
 }
 

@@ -64,25 +64,8 @@ def test_owned_mask_kernels(golden_cases, golden_ref, own_algo, own_direct):
         ctx.option("k2_mode", 0)
 
 
-@pytest.mark.parametrize("cap", [32, 96, 1024])
-def test_merge_heavy_rows_fallback(golden_cases, cap):
-    """Rows longer than the merge buffer take the bitmap fill; results must not change."""
-    ctx = _native.context()
-    ctx.option("k2_mode", 3)
-    ctx.option("fill_algo", 2)
-    ctx.option("merge_cap", cap)
-    try:
-        for case in golden_cases:
-            case.check(b200.build(case.view, case.lists))
-    finally:
-        ctx.option("merge_cap", 0)
-        ctx.option("fill_algo", 0)
-        ctx.option("k2_mode", 0)
-
-
-@pytest.mark.parametrize("fill_algo", [0, 1, 2, 3, 4, 5, 6, 7],
-                         ids=["auto", "coop", "merge", "lane-bitmap", "runs-tma", "block", "segmented",
-                              "bins"])
+@pytest.mark.parametrize("fill_algo", [0, 3, 5, 6, 7],
+                         ids=["auto", "lane-bitmap", "block", "segmented", "bins"])
 def test_owned_fill_variants(golden_cases, fill_algo):
     ctx = _native.context()
     ctx.option("k2_mode", 3)
@@ -93,23 +76,6 @@ def test_owned_fill_variants(golden_cases, fill_algo):
     finally:
         ctx.option("fill_algo", 0)
         ctx.option("k2_mode", 0)
-
-
-@pytest.mark.parametrize("cap", [32, 256])
-def test_runs_fill_heavy_rows(golden_cases, golden_ref, cap):
-    """Rows whose runs exceed the TMA staging buffer take the bitmap pass."""
-    ctx = _native.context()
-    ctx.option("merge_cap", cap)
-    ctx.option("fill_algo", 4)
-    try:
-        for case in golden_cases:
-            case.check(b200.build(case.view, case.lists))
-        g = golden_ref["builds_hashed"]["q32_n10000"]
-        v = pauli_view(10000, 32, 0)
-        assert sha(b200.build(v, random_lists(v, seed=0)).graph.neighbors) == g["neighbors_sha"]
-    finally:
-        ctx.option("merge_cap", 0)
-        ctx.option("fill_algo", 0)
 
 
 @pytest.mark.parametrize("bits,warps", [(1024, 1), (3072, 2), (12288, 2), (20480, 4),
@@ -183,23 +149,6 @@ def test_bins_fill_geometry(golden_cases, golden_ref, threads, dcap):
     finally:
         for k in ("fill_algo", "bins_threads", "blk_dcap"):
             ctx.option(k, 0)
-
-
-@pytest.mark.parametrize("window", [4096, 8192])
-def test_cooperative_fill_windows(golden_ref, window):
-    g = golden_ref["builds_hashed"]["q32_n20000"]
-    ctx = _native.context()
-    ctx.option("k2_mode", 3)
-    ctx.option("fill_algo", 1)
-    ctx.option("window", window)
-    try:
-        v = pauli_view(20000, 32, 0)
-        gc = b200.build(v, random_lists(v, seed=0))
-    finally:
-        ctx.option("window", 0)
-        ctx.option("fill_algo", 0)
-        ctx.option("k2_mode", 0)
-    assert sha(gc.graph.neighbors) == g["neighbors_sha"]
 
 
 @pytest.mark.parametrize("n", [5000, 10000, 20000])
@@ -604,3 +553,28 @@ def test_delta_copy_out_matches_widened_copy(n, pct, alpha):
         for k, d in (("d2h_mode", 0), ("d2h_gap16", 0), ("d2h_pipe", 1), ("d2h_pieces", 0), ("d2h_chunk", 0),
                      ("d2h_dma", -1)):
             ctx.option(k, d)
+
+
+@pytest.mark.parametrize("ragged", [False, True])
+def test_duplicate_colors_in_a_row(ragged):
+    """A list naming one color twice (the reference ORs it into the palette mask once,
+    driver.py:152-172): the device flags it in the bucket pass, the rows are deduped and the
+    build matches the oracle (which builds the same set masks)."""
+    n = 3000
+    v = pauli_view(n, 24, 21)
+    lists = random_lists(v, seed=8)
+    arr = lists.array.copy()
+    rs = np.random.default_rng(4)
+    rows = rs.choice(n, size=40, replace=False)
+    arr[rows, 1] = arr[rows, 0]  # duplicate the first color of 40 rows
+    if ragged:
+        rl = [arr[i, : 3 + (i % 5)].copy() for i in range(n)]
+        lists = b200.ColorLists(v.active, rl, lists.palette_base, lists.palette_size)
+    else:
+        lists = b200.ColorLists.from_array(v.active, arr, lists.palette_base, lists.palette_size)
+    gc = b200.build(v, lists)
+    want = oracle_builder(v, lists)
+    assert np.array_equal(gc.members, want.members)
+    assert np.array_equal(gc.graph.offsets, want.graph.offsets)
+    assert np.array_equal(gc.graph.neighbors, want.graph.neighbors)
+    assert gc.view_edges_scanned == want.view_edges_scanned

@@ -57,7 +57,9 @@ def test_beyond_reference_cap():
     ps = b200.PauliSet.from_strings(b200.random_pauli_strings(30000, 32, seed=5))
     view = b200.pauli_view(ps)
     res = b200.run(view, b200.PaletteParams(12.5, 2.0, seed=0))
-    rep = validation.validate(view, res)
+    with pytest.raises(b200.errors.TooLargeForExactError):
+        validation.validate(view, res)  # the reference's cap is the default
+    rep = validation.validate(view, res, uncapped=True)
     assert rep.proper and rep.violation_count == 0
     assert rep.oracle_edges == res.oracle_edges
     # give vertex v the color of a commuting partner u < v: exactly the violations of v
@@ -68,6 +70,6 @@ def test_beyond_reference_cap():
     same = np.flatnonzero((bad == bad[v]) & (np.arange(bad.size) != v))
     commuting = same[view.pair_mask(same, np.full(same.size, v))]
     res.color = bad
-    rep = validation.validate(view, res)
+    rep = validation.validate(view, res, uncapped=True)
     assert rep.violation_count == commuting.size >= 1
     assert rep.violations[: len(commuting)] == sorted((int(a), v) for a in commuting)

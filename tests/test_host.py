@@ -214,3 +214,16 @@ def test_hostpool_never_hands_out_a_live_buffer():
     assert not np.shares_memory(small, d)
     hp.release()
     assert hp.cached_bytes() == 0
+
+
+def test_dedupe_rows_keeps_each_rows_distinct_colors():
+    """The host side of the duplicate-color path (_native.dedupe_rows): every row keeps its
+    distinct colors (ascending), uniform and ragged inputs."""
+    from paper_2401_06713_b200._native import dedupe_rows
+
+    arr = np.array([[5, 3, 5], [1, 2, 3], [7, 7, 7]], dtype=np.int64)
+    d, off, L = dedupe_rows(arr.reshape(-1), None, 3, 3)
+    assert L == 0 and off.tolist() == [0, 2, 5, 6]
+    assert d.tolist() == [3, 5, 1, 2, 3, 7]
+    d, off, _ = dedupe_rows(np.array([4, 4, 9, 1], dtype=np.int64), np.array([0, 2, 4]), 0, 2)
+    assert off.tolist() == [0, 1, 3] and d.tolist() == [4, 1, 9]

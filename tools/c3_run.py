@@ -26,6 +26,6 @@ for r in res.iterations:
 from paper_2401_06713_b200.validation import validate
 
 t0 = time.time()
-rep = validate(view, res, "exhaustive")
+rep = validate(view, res, "exhaustive", uncapped=True)
 print(f"validate (exhaustive, GPU): proper={rep.proper} violations={rep.violation_count} "
       f"colors={rep.colors_used} |E|={rep.oracle_edges} in {time.time() - t0:.2f} s", flush=True)
