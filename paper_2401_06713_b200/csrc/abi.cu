@@ -1680,9 +1680,11 @@ static int fill_rows_device(pcg_ctx *ctx, int64_t r0, int64_t r1, const int32_t 
         PCG_CHECK_LAUNCH(ctx);
         return PCG_OK;
     }
-    // the bins fill (counting sort per row) is the default beyond the block fill's range
-    // when the longest row fits its list (1M ids: 23.7 ms vs the segmented fill's 52.8)
-    const bool bins_auto = ctx->fill_algo == 0 && ctx->n > 131072;
+    // the bins fill (counting sort per row, bins sorted by bitonic networks) is the default
+    // from 40K ids when the longest row fits its list.  Measured (block fill vs bins): 20K ids
+    // 0.204 vs 0.230 ms, 50K 0.611 vs 0.587, 100K (config 2) 1.368 vs 1.256, 140K 2.33 vs
+    // 2.02; 1M (config 3) 20.7 ms vs the segmented fill's 52.8
+    const bool bins_auto = ctx->fill_algo == 0 && ctx->n >= 40000;
     // measured (500k ids): rows up to 16K ids still win with the bins fill (P' = 20%,
     // alpha = 4.5, mean row 8.5k: 36.9 ms with 384 threads vs the segmented fill's 52.9)
     const int32_t bins_maxdeg = ctx->bins_maxdeg > 0 ? ctx->bins_maxdeg : 16384;
@@ -1708,7 +1710,7 @@ static int fill_rows_device(pcg_ctx *ctx, int64_t r0, int64_t r1, const int32_t 
     }
     // measured (c2, 100k ids): block fill 1.37-1.40 ms vs segmented 1.68 ms; at 1M ids the
     // segmented fill's narrower windows win, so the block fill is the default up to 128K ids
-    const bool blk_auto = ctx->fill_algo == 0 && ctx->n <= 131072;
+    const bool blk_auto = ctx->fill_algo == 0 && ctx->n <= 131072;  // (and bins did not fit)
     if ((ctx->fill_algo == 5 || blk_auto) && ctx->mask_words < (1LL << 32)) {
         // block fill: one CTA per row, bitmap over the whole id range (or wide windows)
         BlkArgs g{};

@@ -611,13 +611,16 @@ size_t bins_smem_bytes(const BinArgs &g) {
            (size_t)g.lcap * 12 + 33 * 4;
 }
 
-// bins of 2^shift ids with ~4 admitted ids per bin on average: shift = floor(log2(4n / mean
-// row)).  Measured at 1M ids (~3.1k per row): 192 threads with ~4 ids per bin 23.7 ms; ~1 id
-// per bin 28.0 ms (more bins: more shared memory, fewer CTAs); 128 threads 27.8-34.5 ms;
-// 256 threads 26.3 ms; the segmented fill 52.8 ms.
+// bins of 2^shift ids with 2-4 admitted ids per bin on average: shift = floor(log2(4n / mean
+// row)).  Measured at 1M ids (~3.1k per row, before the bitonic bin sort): ~4 ids per bin
+// 23.7 ms, ~1 id per bin 28.0 ms (more bins: more shared memory, fewer CTAs); with the bin
+// sort, double-width bins 22.8 ms and half-width 24.9 vs 20.7 ms.
 void bins_geometry(int64_t n, double mean_deg, int threads, BinArgs *g) {
-    // longer rows want more threads per row (mean 8.5k ids: 384 threads 36.9 ms, 192: 57.7)
-    g->threads = threads > 0 ? threads : (mean_deg > 6000.0 ? 384 : 192);
+    // ~16 of the row's ids per thread, 64-384 threads.  Measured: 100K ids (2.1k per row) 128
+    // threads 1.256 ms, 192 1.37; 1M (3.1k per row) 192 20.7 ms, 128 22.9, 256 23.1; 500k with
+    // 8.5k per row 384 36.9 ms, 192 57.7
+    const int nt = (int)((mean_deg / 16.0 + 16.0) / 32.0) * 32;
+    g->threads = threads > 0 ? threads : std::max(64, std::min(384, nt));
     int sh = 0;
     const double want = mean_deg > 1.0 ? 4.0 * (double)n / mean_deg : (double)n;
     while (sh < 30 && (double)(1LL << (sh + 1)) <= want) ++sh;

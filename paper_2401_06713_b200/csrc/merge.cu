@@ -193,27 +193,29 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_masks(BucketArgs b, OwnAr
 // instead of one AND/POPC chain per pair.  Ownership inserts run warp-per-member with the
 // lanes over the member's (sorted) list, colors below c only.
 // ---------------------------------------------------------------------------------------
-template <int KW>
-__global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs o) {
+template <int KW, bool DB>
+__global__ void __launch_bounds__(OWN_THREADS, (KW <= 4 ? 4 : 3)) k_owned_fr(BucketArgs b, OwnArgs o) {
     constexpr int NIB = 8 * KW;
     extern __shared__ __align__(16) uint32_t osm[];
     const int HS = o.hash_slots;
     // ownership state: hash (large palettes) or a direct-mapped table over the colors
     uint32_t *table = osm;                                        // HS: (c'+1)<<12 | first k
-    unsigned short *head = reinterpret_cast<unsigned short *>(osm + HS);  // HS: last coll + 1
-    uint32_t *coll = osm + HS + HS / 2;                           // OWN_COLL: slot<<12 | k
-    int32_t *link = reinterpret_cast<int32_t *>(coll + OWN_COLL); // OWN_COLL: previous in slot
+    uint32_t *coll = osm + HS;                                    // OWN_COLL: slot<<12 | k
     unsigned short *dtab = reinterpret_cast<unsigned short *>(osm);  // direct: P member tags
     uint32_t *lA = osm + o.dtab_words;                            // direct: losers (c'<<12|k)
     const int lcap = o.lcap > 0 ? o.lcap : OWN_LCAP;
     uint32_t *lB = lA + lcap;
     int32_t *sid = reinterpret_cast<int32_t *>(osm + (o.direct ? o.dtab_words + 2 * lcap
-                                                               : HS + HS / 2 + 2 * OWN_COLL));
-    uint32_t *T = reinterpret_cast<uint32_t *>(sid + ((o.m_cap + 3) & ~3));  // NIB*16 table
-    uint32_t *BT = T + NIB * 16;                                  // 32*KW transposed bits
-    uint32_t *sB = BT + 32 * KW;                                  // members' partner vectors
+                                                               : HS + OWN_COLL));
+    constexpr int NB = DB ? 2 : 1;  // table buffers
+    uint32_t *T = reinterpret_cast<uint32_t *>(sid + ((o.m_cap + 3) & ~3));  // NB x NIB*16 tables
+    uint32_t *BT = T + NB * NIB * 16;                             // NB x 32*KW transposed bits
+    uint32_t *sB = BT + NB * 32 * KW;                             // partner vectors, stride KW+1
+    // row stride: odd (conflict-free transposition loads) from KW = 4; at KW = 2 the 2-way
+    // conflict is cheaper than the padding (which would cost a CTA per SM at config 2)
+    constexpr int SBS = KW >= 4 ? KW + 1 : KW;
     // members' color lists (rectangular lists): u16 when the palette allows, else u32
-    void *sLv = sB + o.m_cap * KW;
+    void *sLv = sB + ((o.m_cap * SBS + 3) & ~3);
     unsigned short *sL16 = reinterpret_cast<unsigned short *>(sLv);
     int32_t *sL32 = reinterpret_cast<int32_t *>(sLv);
     const bool stage_lists = o.stage_lists != 0;
@@ -224,7 +226,7 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
     if (o.direct) {
         for (int x = tid; x < o.dtab_words; x += OWN_THREADS) osm[x] = 0u;
     } else {
-        for (int x = tid; x < HS + HS / 2; x += OWN_THREADS) osm[x] = 0u;
+        for (int x = tid; x < HS; x += OWN_THREADS) osm[x] = 0u;
     }
     for (int64_t c = blockIdx.x; c < b.P; c += gridDim.x) {
         const int m = b.bstart[c + 1] - b.bstart[c];
@@ -261,7 +263,7 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
         // stage the members' partner vectors and color lists once (all loads in flight
         // together; every later pass reads shared memory)
         for (int x = tid; x < m * KW; x += OWN_THREADS)
-            sB[x] = __ldg(b.B + (int64_t)sid[x / KW] * KW + x % KW);
+            sB[(x / KW) * SBS + x % KW] = __ldg(b.B + (int64_t)sid[x / KW] * KW + x % KW);
         if (stage_lists) {
             const uint32_t items = (uint32_t)m * (uint32_t)o.L;
             for (uint32_t e = tid; e < items; e += OWN_THREADS) {
@@ -283,18 +285,31 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
                 for (int g = 0; g < NIB; ++g)
                     naddr[g] = T_s + (uint32_t)(g * 16 + ((av[g >> 3] >> (4 * (g & 7))) & 15u)) * 4u;
             }
+            // per 32-partner word w: transpose (BT), tabulate (T), look up.  Double buffered
+            // (DB), one word's lookups overlap the next word's transposition (two barriers per
+            // word); single buffered (when the second buffer would cost a CTA per SM), three
             for (int w = 0; w < W; ++w) {
-                // transposed partner bits: warp j takes bit positions [j*4*KW, (j+1)*4*KW)
+                const int bw = DB ? (w & 1) : 0;
+                uint32_t *BTw = BT + bw * 32 * KW;
+                uint32_t *Tw = T + bw * NIB * 16;
+                // transposed partner bits: warp j takes bit positions [j*PER, (j+1)*PER), all in
+                // one 32-bit word of the partner vectors; lane pp keeps ballot pp
                 {
                     const int t = 32 * w + lane;
                     constexpr int PER = 4 * KW;  // bits per warp (32*KW / 8 warps)
+                    const int p0 = warp * PER;
+                    // (PER = 24 at KW = 6: a warp's bits may span two words)
+                    const uint32_t wlo = t < m ? sB[t * SBS + (p0 >> 5)] : 0u;
+                    const uint32_t whi = (32 % PER == 0) ? wlo : t < m ? sB[t * SBS + ((p0 + PER - 1) >> 5)] : 0u;
+                    uint32_t mine = 0u;
 #pragma unroll
                     for (int pp = 0; pp < PER; ++pp) {
-                        const int p = warp * PER + pp;
-                        const uint32_t word = t < m ? sB[t * KW + (p >> 5)] : 0u;
+                        const int p = p0 + pp;
+                        const uint32_t word = ((p >> 5) == (p0 >> 5)) ? wlo : whi;
                         const uint32_t bal = __ballot_sync(0xffffffffu, (word >> (p & 31)) & 1u);
-                        if (lane == 0) BT[p] = bal;
+                        if (lane == pp) mine = bal;
                     }
+                    if (lane < PER) BTw[p0 + lane] = mine;
                 }
                 __syncthreads();
                 for (int x = tid; x < NIB * 16; x += OWN_THREADS) {
@@ -302,16 +317,17 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
                     uint32_t e = 0u;
 #pragma unroll
                     for (int q = 0; q < 4; ++q)
-                        if ((v >> q) & 1) e ^= BT[4 * g + q];
-                    T[x] = e;
+                        if ((v >> q) & 1) e ^= BTw[4 * g + q];
+                    Tw[x] = e;
                 }
                 __syncthreads();
                 if (k < m) {
+                    const uint32_t toff = (uint32_t)(bw * NIB * 16 * 4);
                     uint32_t acc = 0u;
 #pragma unroll
                     for (int g = 0; g < NIB; ++g) {
                         uint32_t e;
-                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(naddr[g]));
+                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(naddr[g] + toff));
                         acc ^= e;
                     }
                     const int tend = min(32, m - 32 * w);
@@ -319,8 +335,9 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
                     if (k >> 5 == w) bits &= ~(1u << (k & 31));  // no self pair
                     out[(int64_t)k * W + w] = bits;
                 }
-                __syncthreads();
+                if (!DB) __syncthreads();
             }
+            if (DB) __syncthreads();  // (the next row block reuses the buffers from word 0)
         }
         // ---- ownership: (c', k) for every color c' < c of every member's list.  Rectangular
         // lists: one thread per (member, slot) item, consecutive threads on consecutive slots
@@ -337,20 +354,8 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
                 if (prev == 0u) return;
                 if ((prev >> 12) == cp) {
                     const int q = atomicAdd(&ncoll, 1);
-                    if (q < OWN_COLL) {
-                        coll[q] = (slot << 12) | (uint32_t)k;
-                        uint32_t *hw = reinterpret_cast<uint32_t *>(head) + (slot >> 1);
-                        const int sh = (slot & 1) * 16;
-                        uint32_t old = *hw, assumed;
-                        do {
-                            assumed = old;
-                            const uint32_t nv = (assumed & ~(0xffffu << sh)) | ((uint32_t)(q + 1) << sh);
-                            old = atomicCAS(hw, assumed, nv);
-                        } while (old != assumed);
-                        link[q] = (int)((old >> sh) & 0xffffu) - 1;
-                    } else {
-                        overflow = 1;
-                    }
+                    if (q < OWN_COLL) coll[q] = (slot << 12) | (uint32_t)k;
+                    else overflow = 1;
                     return;
                 }
                 slot = (slot + 1) & (HS - 1);
@@ -417,12 +422,25 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
                 dst = t;
             }
         } else if (!o.loff) {
+            // the list loads of OWN_BATCH items are issued together (the inserts' atomics
+            // would otherwise serialise each load behind the previous item's insert)
+            constexpr int OWN_BATCH = 8;
             const uint32_t items = (uint32_t)m * (uint32_t)o.L;
-            for (uint32_t e = tid; e < items; e += OWN_THREADS) {
-                const int k = (int)__umulhi(e, o.l_magic);  // e / L (exact for e < 2^20)
-                const int32_t cx = !stage_lists ? o.lrel[(int64_t)sid[k] * o.L + (e - (uint32_t)k * (uint32_t)o.L)]
-                                 : o.l16 ? (int32_t)sL16[e] : sL32[e];
-                if (cx < c) insert((uint32_t)cx + 1u, k);
+            for (uint32_t e0 = tid; e0 < items; e0 += OWN_BATCH * OWN_THREADS) {
+                int32_t cx[OWN_BATCH];
+                int kk[OWN_BATCH];
+#pragma unroll
+                for (int u = 0; u < OWN_BATCH; ++u) {
+                    const uint32_t e = e0 + (uint32_t)(u * OWN_THREADS);
+                    const int k = (int)__umulhi(e, o.l_magic);  // e / L (exact for e < 2^20)
+                    kk[u] = k;
+                    cx[u] = e >= items ? INT_MAX
+                          : !stage_lists ? __ldg(o.lrel + (int64_t)sid[k] * o.L + (e - (uint32_t)k * (uint32_t)o.L))
+                          : o.l16 ? (int32_t)sL16[e] : sL32[e];
+                }
+#pragma unroll
+                for (int u = 0; u < OWN_BATCH; ++u)
+                    if (cx[u] < c) insert((uint32_t)cx[u] + 1u, kk[u]);
             }
         } else {
             for (int k = warp; k < m; k += NWARPS) {
@@ -436,26 +454,33 @@ __global__ void __launch_bounds__(OWN_THREADS) k_owned_fr(BucketArgs b, OwnArgs 
         __syncthreads();
         const int nc = o.direct ? 0 : min(ncoll, OWN_COLL);
         if (overflow && tid == 0) atomicMax(o.overflow, overflow);
+        // every collision entry (a later holder k2 of a color c' < c) pairs with the first
+        // holder (the table slot) and with the earlier collision entries of the same slot, so
+        // each pair of a group sharing c' is cleared exactly once (groups are almost always
+        // pairs: ~(L-1)^2/P of a bucket's pairs share a second color)
         for (int q = tid; q < nc; q += OWN_THREADS) {
-            const uint32_t slot = coll[q] >> 12;
-            const int k2 = (int)(coll[q] & 0xfffu);
-            int k1 = (int)(table[slot] & 0xfffu);
-            for (int p = link[q];; p = link[p]) {
-                if (k1 != k2) {
-                    atomicAnd(&out[(int64_t)k1 * W + (k2 >> 5)], ~(1u << (k2 & 31)));
-                    atomicAnd(&out[(int64_t)k2 * W + (k1 >> 5)], ~(1u << (k1 & 31)));
+            const uint32_t cq = coll[q];
+            const uint32_t slot = cq >> 12;
+            const int k2 = (int)(cq & 0xfffu);
+            const int k1 = (int)(table[slot] & 0xfffu);
+            if (k1 != k2) {
+                atomicAnd(&out[(int64_t)k1 * W + (k2 >> 5)], ~(1u << (k2 & 31)));
+                atomicAnd(&out[(int64_t)k2 * W + (k1 >> 5)], ~(1u << (k1 & 31)));
+            }
+            for (int p = 0; p < q; ++p) {
+                const uint32_t cp = coll[p];
+                const int k0 = (int)(cp & 0xfffu);
+                if ((cp >> 12) == slot && k0 != k2) {
+                    atomicAnd(&out[(int64_t)k0 * W + (k2 >> 5)], ~(1u << (k2 & 31)));
+                    atomicAnd(&out[(int64_t)k2 * W + (k0 >> 5)], ~(1u << (k0 & 31)));
                 }
-                if (p < 0) break;
-                k1 = (int)(coll[p] & 0xfffu);
             }
         }
         __syncthreads();
-        // reset the hash table and the chain heads this color touched (direct tags carry the
-        // color: nothing to reset)
+        // reset the hash table (direct tags carry the color: nothing to reset)
         if (!o.direct) {
             for (int x = 4 * tid; x < HS; x += 4 * OWN_THREADS)
                 *reinterpret_cast<uint4 *>(table + x) = make_uint4(0u, 0u, 0u, 0u);
-            for (int q = tid; q < nc; q += OWN_THREADS) head[coll[q] >> 12] = 0;  // (16-bit store)
         }
         __syncthreads();
     }
@@ -514,23 +539,30 @@ int run_owned(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s) {
     return 1;
 }
 
-size_t owned_fr_smem(const OwnArgs &o, int kw) {
+size_t owned_fr_smem(const OwnArgs &o, int kw, bool db = false) {
     const size_t state = o.direct ? (size_t)o.dtab_words + 2 * (size_t)(o.lcap > 0 ? o.lcap : OWN_LCAP)
-                                  : (size_t)o.hash_slots + o.hash_slots / 2 + 2 * OWN_COLL;
+                                  : (size_t)o.hash_slots + OWN_COLL;
     const size_t lists = o.stage_lists ? (size_t)o.m_cap * o.L * (o.l16 ? 2 : 4) : 0;
-    return (state + ((o.m_cap + 3) & ~3) + 8 * (size_t)kw * 16 + 32 * (size_t)kw + (size_t)o.m_cap * kw) * 4 +
+    const size_t nb = db ? 2 : 1;
+    return (state + ((o.m_cap + 3) & ~3) + nb * 8 * (size_t)kw * 16 + nb * 32 * (size_t)kw +
+            (((size_t)o.m_cap * (kw >= 4 ? kw + 1 : kw) + 3) & ~(size_t)3)) * 4 +
            ((lists + 15) & ~(size_t)15);
 }
 
+// double-buffered tables unless the second buffer costs a CTA per SM
 template <int KW>
 int run_owned_fr(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s) {
-    int per_sm = 0;
-    const size_t smem = owned_fr_smem(o, KW);
-    allow_max_smem(k_owned_fr<KW>);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_owned_fr<KW>, OWN_THREADS, smem);
-    if (per_sm < 1) per_sm = 1;
+    int per1 = 0, per2 = 0;
+    const size_t smem1 = owned_fr_smem(o, KW, false), smem2 = owned_fr_smem(o, KW, true);
+    allow_max_smem(k_owned_fr<KW, false>);
+    allow_max_smem(k_owned_fr<KW, true>);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k_owned_fr<KW, false>, OWN_THREADS, smem1);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_owned_fr<KW, true>, OWN_THREADS, smem2);
+    const bool db = per2 >= per1 && per2 >= 1;
+    const int per_sm = std::max(1, db ? per2 : per1);
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * sms * 4, b.P));
-    k_owned_fr<KW><<<(unsigned)grid, OWN_THREADS, smem, s>>>(b, o);
+    if (db) k_owned_fr<KW, true><<<(unsigned)grid, OWN_THREADS, smem2, s>>>(b, o);
+    else k_owned_fr<KW, false><<<(unsigned)grid, OWN_THREADS, smem1, s>>>(b, o);
     return 1;
 }
 

@@ -129,14 +129,17 @@ def test_block_fill_geometry(golden_cases, golden_ref, threads, groups, dcap, ec
             ctx.option(k, 0)
 
 
-@pytest.mark.parametrize("threads,dcap", [(32, 0), (128, 8), (256, 0), (1024, 24)])
-def test_bins_fill_geometry(golden_cases, golden_ref, threads, dcap):
-    """Bins fill (counting sort per row): CTA size and descriptor chunking must not change a
-    single entry."""
+@pytest.mark.parametrize("threads,dcap,shift", [(32, 0, 0), (128, 8, 0), (256, 0, 0), (1024, 24, 0),
+                                               (128, 0, 1), (192, 0, 3), (192, 16, 5), (128, 0, -1)])
+def test_bins_fill_geometry(golden_cases, golden_ref, threads, dcap, shift):
+    """Bins fill (counting sort per row): CTA size, descriptor chunking and bin width must not
+    change a single entry.  Wider bins (shift > 0) exercise the spill list (bins of 10-16 ids)
+    and the per-row fallback (bins of more than 16 ids: list, scatter, sort from the list)."""
     ctx = _native.context()
     ctx.option("fill_algo", 7)
     ctx.option("bins_threads", threads)
     ctx.option("blk_dcap", dcap)
+    ctx.option("bins_shift", shift)
     try:
         for case in golden_cases:
             case.check(b200.build(case.view, case.lists))
@@ -147,7 +150,7 @@ def test_bins_fill_geometry(golden_cases, golden_ref, threads, dcap):
             assert (sha(gc.graph.offsets), sha(gc.graph.neighbors)) == (
                 g["offsets_sha"], g["neighbors_sha"])
     finally:
-        for k in ("fill_algo", "bins_threads", "blk_dcap"):
+        for k in ("fill_algo", "bins_threads", "blk_dcap", "bins_shift"):
             ctx.option(k, 0)
 
 

@@ -227,3 +227,19 @@ def test_dedupe_rows_keeps_each_rows_distinct_colors():
     assert d.tolist() == [3, 5, 1, 2, 3, 7]
     d, off, _ = dedupe_rows(np.array([4, 4, 9, 1], dtype=np.int64), np.array([0, 2, 4]), 0, 2)
     assert off.tolist() == [0, 1, 3] and d.tolist() == [4, 1, 9]
+
+
+def test_build_reference_and_lists_intersect_match_goldens(golden_cases):
+    """The host equivalence oracle kept for API parity (conflict.py:28-39, 170-205) gives the
+    reference's CSR on the small golden builds (the GPU build never calls it)."""
+    from paper_2401_06713_b200.conflict import build_reference, lists_intersect
+
+    assert lists_intersect([1, 4, 9], [2, 4]) and not lists_intersect([1, 3], [2, 4, 6])
+    assert not lists_intersect([], [1])
+    done = 0
+    for case in golden_cases:
+        if case.view.n_active > 400 or case.view.mode != "implicit-complement":
+            continue
+        case.check(build_reference(case.view, case.lists))
+        done += 1
+    assert done >= 5

@@ -15,7 +15,7 @@ import sys
 import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-LIB = os.path.join(ROOT, "paper_2401_06713_b200", "libpicasso_b200.so")
+LIB = os.environ.get("PCG_LIB", os.path.join(ROOT, "paper_2401_06713_b200", "libpicasso_b200.so"))
 
 
 def line_table(stem, mangled_hint):
@@ -58,9 +58,11 @@ def main():
     # the function whose SASS matches the report's instruction text best
     sass = [(int(r[ia], 16) - base, r[1].strip()) for r in rows]
 
+    norm = lambda x: re.sub(r"0x[0-9a-f]+|`\(\.L_x_\d+\)", "", x).split()
+
     def score(f):
         t = funcs[f]
-        return sum(1 for off, s in sass[:400] if off in t and t[off][1].split()[0] == s.split()[0])
+        return sum(1 for off, s in sass if off in t and norm(t[off][1]) == norm(s))
 
     best = max(funcs, key=score)
     table = funcs[best]
