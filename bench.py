@@ -280,11 +280,11 @@ def smem_peak(sm_mhz: float) -> tuple:
 
 
 def k1_table_bytes_per_pair(q: int) -> float:
-    """Shared-memory bytes one pair costs in K1 (k_commute_fr6: one 128-byte table row per
-    6-bit slice per 1024 partners = 8 B per slice per 64 partners; k_commute_fr: one 4-byte
-    entry per 4-bit slice per 32 partners)."""
+    """Shared-memory bytes one pair costs in K1 (k_commute_fr8, K = 64*ceil(q/32) bits <= 256:
+    one EB-byte table entry per 8-bit slice per 8*EB partners = K/64 bytes; k_commute_fr: one
+    4-byte entry per 4-bit slice per 32 partners)."""
     K = 64 * ((q + 31) // 32)
-    return 8.0 * ((K + 5) // 6) / 64.0 if K <= 128 else 4.0 * (K // 4) / 32.0
+    return K / 64.0 if K <= 256 else 4.0 * (K // 4) / 32.0
 
 
 def device_steps(ctx, stream, steps: int, warmup: int, flush, clocks=None):
@@ -365,7 +365,7 @@ def measure_workload(name, args, local, clocks_on: bool):
     # K1 against the shared-memory bound of its table lookups
     k1_ms = float(kt[0])
     bpp = k1_table_bytes_per_pair(q)
-    k1_kernel = "k_commute_fr6" if q <= 64 else "k_commute_fr"
+    k1_kernel = "k_commute_fr8" if q <= 128 else "k_commute_fr"
     speak, speak_src, bpc = smem_peak(sm_mhz)
     k1_ach = pairs * bpp / (k1_ms * 1e-3) / 1e9
     k1_traffic = measured_traffic(k1_kernel) or (None, None)
@@ -374,8 +374,9 @@ def measure_workload(name, args, local, clocks_on: bool):
                "traffic": k1_traffic[0], "traffic_source": k1_traffic[1],
                "bytes_per_launch": int(pairs * bpp), "launch_ms": k1_ms,
                "note": f"algorithmic bytes = shared-memory table bytes: {bpp} B per pair (one "
-                       "128-byte table row per 6-bit slice per 1024 partners, read as LDS.128 by "
-                       "quarter-warps) x n(n-1)/2 pairs; K1 reads "
+                       "32-byte table entry per 8-bit slice per 256 partners, read as LDS.128 by "
+                       "lane pairs, 4 rows per quarter-warp on distinct bank groups) x n(n-1)/2 "
+                       "pairs; K1 reads "
                        "~0 HBM (traffic), its bound is the shared-memory pipe. peak = "
                        f"{bpc:.1f} B/clk/SM x 148 x {sm_mhz:.0f} MHz ({speak_src})"}
     # the conflict-row fill against HBM (algorithmic bytes: CSR ids written + rows read)
@@ -383,7 +384,7 @@ def measure_workload(name, args, local, clocks_on: bool):
     words_b = n * view.backing.words.shape[1] * 8
     fill_bytes = (2 * edges) * 4 + (members + 1) * 8 + members * 8 + n * plan.list_size * 4 + words_b
     fill_ach = fill_bytes / (fill_ms * 1e-3) / 1e9
-    fill_kernel = "k_fill_blk" if n <= 131072 else "k_fill_bins"
+    fill_kernel = "k_fill_bins" if n >= 40000 else "k_fill_blk"  # the auto choice (abi.cu)
     fill_traffic = measured_traffic(fill_kernel) or (None, None)
     roof_fill = {"bound": "hbm", "kernel": f"conflict-row fill ({fill_kernel})", "achieved": fill_ach,
                  "peak": hbm, "unit": "GB/s", "frac": fill_ach / hbm, "traffic": fill_traffic[0],

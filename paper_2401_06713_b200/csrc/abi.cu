@@ -342,8 +342,10 @@ static bool fr6_supported(int32_t kw) { return kw == 2 || kw == 4; }
 
 static int fr_offsets(pcg_ctx *ctx, cudaStream_t s) {
     if (!fr_supported(ctx->kw)) return PCG_OK;
-    // the 6-bit kernel (the default for kw 2/4) reads the bit planes directly
-    if (fr6_supported(ctx->kw) && (ctx->k1_algo == 0 || ctx->k1_algo == 4)) return PCG_OK;
+    // the 8-bit kernel (the default for kw 2/4/6/8) and the 6-bit one read the bit planes
+    // directly
+    if (fr8_supported(ctx->kw) && (ctx->k1_algo == 0 || ctx->k1_algo == 5)) return PCG_OK;
+    if (fr6_supported(ctx->kw) && ctx->k1_algo == 4) return PCG_OK;
     PCG_ALLOC(ctx, ctx->H, (size_t)ctx->npad * ctx->kw * 4 * 4);
     ctx->h_wide = fr_jb(ctx->kw, ctx->k1_wide) == K1_FR_JB2;
     if (ctx->h_wide) launch_fr_prep2(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
@@ -700,16 +702,22 @@ extern "C" int pcg_set_inputs(pcg_ctx *ctx, const uint64_t *words, int64_t n_tot
 // --------------------------------------------------------------------------------------
 // count pass
 // --------------------------------------------------------------------------------------
-// 1 direct tiles, 2 four-Russians 4-bit slices, 4 6-bit slices (the default where
-// supported: kw 2/4; k1_algo 3, 5-bit slices, was measured slower and removed)
+// 1 direct tiles, 2 four-Russians 4-bit slices, 4 6-bit slices, 5 8-bit slices (the default
+// where supported: kw 2/4/6/8; k1_algo 3, 5-bit slices, was measured slower and removed)
 static int k1_algo(const pcg_ctx *ctx) {
     if (ctx->k1_algo == 1) return 1;
     if (ctx->k1_algo == 2 && fr_supported(ctx->kw)) return 2;
+    if (ctx->k1_algo == 4 && fr6_supported(ctx->kw)) return 4;
+    if (fr8_supported(ctx->kw)) return 5;
     if (fr6_supported(ctx->kw)) return 4;
     return fr_supported(ctx->kw) ? 2 : 1;
 }
 
-static int64_t fr_ichunk(const pcg_ctx *ctx) { return ctx->fr_ichunk > 0 ? ctx->fr_ichunk : 2048; }
+// rows per K1 work item: 8192 for the 8-bit kernel (measured at 1M x 64q: 2048 32.2 ms,
+// 4096 31.1, 8192 30.1), 2048 for the others
+static int64_t fr_ichunk(const pcg_ctx *ctx, bool fr8) {
+    return ctx->fr_ichunk > 0 ? ctx->fr_ichunk : fr8 ? 8192 : 2048;
+}
 
 // pairs (i<j, both < n) inside four-Russians item (jb, rows [i0,i1))
 static int64_t fr_item_pairs(int64_t n, int64_t jb, int64_t i0, int64_t i1, int64_t JB) {
@@ -746,24 +754,30 @@ static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, 
                   cudaStream_t s, unsigned long long *anti) {
     const int64_t n = ctx->n;
     if (k1_algo(ctx) >= 2) {
-        const bool fr6 = k1_algo(ctx) == 4;
-        const int64_t JB = (ctx->h_wide && !fr6) ? K1_FR_JB2 : K1_FR_JB;
-        const int64_t njb = ctx->npad / JB, ic = fr_ichunk(ctx);
+        const bool fr6 = k1_algo(ctx) == 4, fr8 = k1_algo(ctx) == 5;
+        const int64_t JB = fr8 ? fr8_jb(ctx->kw) : (ctx->h_wide && !fr6) ? K1_FR_JB2 : K1_FR_JB;
+        const int64_t njb = ctx->npad / JB, ic = fr_ichunk(ctx, fr8);
+        // item_start runs over the blocks in visit order; the 8-bit kernel folds the triangle
+        // (blocks 0, njb-1, 1, njb-2, ...) so that every CTA's item range spans about the
+        // same number of table rebuilds (a short early block is paired with a long late one)
+        auto jb_of = [&](int64_t v) { return fr8 ? fr8_fold(v, njb) : v; };
         std::vector<int64_t> start(njb + 1, 0);
-        for (int64_t jb = 0; jb < njb; ++jb) {
-            const int64_t jlast = std::min(n, (jb + 1) * JB);
-            start[jb + 1] = start[jb] + (jlast + ic - 1) / ic;
+        for (int64_t v = 0; v < njb; ++v) {
+            // (a padding block past the last row has no pairs and no items)
+            const int64_t jlast = jb_of(v) * JB < n ? std::min(n, (jb_of(v) + 1) * JB) : 0;
+            start[v + 1] = start[v] + (jlast + ic - 1) / ic;
         }
         const int64_t items = start[njb];
         const int64_t i0 = items * shard / nshards, i1 = items * (shard + 1) / nshards;
         if (nshards == 1) {
             *pairs = n * (n - 1) / 2;
         } else {
-            int64_t p = 0, jb = 0;
+            int64_t p = 0, v = 0;
             for (int64_t it = i0; it < i1; ++it) {
-                while (start[jb + 1] <= it) ++jb;
+                while (start[v + 1] <= it) ++v;
+                const int64_t jb = jb_of(v);
                 const int64_t jlast = std::min(n, (jb + 1) * JB);
-                const int64_t r0 = (it - start[jb]) * ic, r1 = std::min(r0 + ic, jlast);
+                const int64_t r0 = (it - start[v]) * ic, r1 = std::min(r0 + ic, jlast);
                 p += fr_item_pairs(n, jb, r0, r1, JB);
             }
             *pairs = p;
@@ -772,7 +786,11 @@ static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, 
         PCG_ALLOC(ctx, ctx->items, (size_t)(njb + 1) * 8);
         PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->items.p, start.data(), (size_t)(njb + 1) * 8,
                                           cudaMemcpyHostToDevice, s));
-        if (fr6)
+        if (fr8)
+            *launches += launch_commute_fr8_items(ctx->A.as<uint32_t>(), ctx->B.as<uint32_t>(),
+                                                  ctx->kw, n, ctx->items.as<int64_t>(), njb,
+                                                  (int32_t)ic, i0, i1, anti, ctx->sms, s);
+        else if (fr6)
             *launches += launch_commute_fr6_items(ctx->A.as<uint32_t>(), ctx->B.as<uint32_t>(),
                                                   ctx->kw, n, ctx->items.as<int64_t>(), njb,
                                                   (int32_t)ic, i0, i1, anti, ctx->sms,

@@ -176,6 +176,16 @@ int launch_commute_fr6_items(const uint32_t *A, const uint32_t *B, int32_t kw, i
                              int64_t item0, int64_t item1, unsigned long long *anti, int sms,
                              int wide_loads, cudaStream_t s);
 int launch_fr_prep2(const uint32_t *A, int32_t kw, int64_t npad, uint32_t *H, cudaStream_t s);
+bool fr8_supported(int32_t kw);
+// visit order of the 8-bit K1's partner blocks: 0, njb-1, 1, njb-2, ... (a permutation)
+__host__ __device__ inline int64_t fr8_fold(int64_t v, int64_t njb) {
+    return (v & 1) ? njb - 1 - (v >> 1) : (v >> 1);
+}
+int fr8_jb(int32_t kw);
+int launch_commute_fr8_items(const uint32_t *A, const uint32_t *B, int32_t kw, int64_t n,
+                             const int64_t *item_start, int64_t njb, int32_t ichunk,
+                             int64_t item0, int64_t item1, unsigned long long *anti, int sms,
+                             cudaStream_t s);
 int launch_commute_fr2_items(const uint32_t *B, const uint32_t *H, int32_t kw, int64_t n,
                              const int64_t *item_start, int64_t njb, int32_t ichunk,
                              int64_t item0, int64_t item1, unsigned long long *anti, int sms,

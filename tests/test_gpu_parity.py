@@ -16,8 +16,9 @@ from conftest import oracle_builder, pauli_view, random_lists, sha
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=[(1, 0), (2, 0), (2, 1), (4, 0)],
-                ids=["k1-direct", "k1-fourrussians", "k1-fourrussians-wide", "k1-fourrussians-6bit"])
+@pytest.fixture(params=[(1, 0), (2, 0), (2, 1), (4, 0), (5, 0)],
+                ids=["k1-direct", "k1-fourrussians", "k1-fourrussians-wide", "k1-fourrussians-6bit",
+                     "k1-fourrussians-8bit"])
 def k1_algo(request):
     ctx = _native.context()
     ctx.option("k1_algo", request.param[0])

@@ -20,7 +20,7 @@ for W in c3 c2; do
      python bench.py --workload $W --secondary '' --steps 2 --warmup 3 --no-cpu-baseline --no-clocks --no-run \
      > $OUT/ncu_bench_$W.log 2>&1
 done
-for spec in c3:k_commute_fr6 c3:k_fill_bins c3:k_owned_fr c2:k_fill_blk c2:k_owned_fr c2:k_commute_fr6; do
+for spec in c3:k_commute_fr8 c3:k_fill_bins c3:k_owned_fr c2:k_fill_bins c2:k_owned_fr c2:k_commute_fr8; do
   W=${spec%%:*}; k=${spec#*:}
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
      -o $OUT/full_${W}_$k python bench.py --workload $W --secondary '' --steps 1 --warmup 3 \

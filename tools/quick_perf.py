@@ -36,6 +36,7 @@ ap.add_argument("--async", dest="k1_async", type=int, default=0)
 ap.add_argument("--early", type=int, default=1)
 ap.add_argument("--check", action="store_true", help="compare the CSR with the default fill")
 ap.add_argument("--pct", type=float, default=12.5)
+ap.add_argument("--ichunk", type=int, default=0)
 ap.add_argument("--alpha", type=float, default=2.0)
 a = ap.parse_args()
 
@@ -63,6 +64,7 @@ ctx.option("bins_shift", a.bins_shift)
 ctx.option("bins_maxdeg", a.bins_maxdeg)
 ctx.option("k1_async", a.k1_async)
 ctx.option("k1_early", a.early)
+ctx.option("fr_ichunk", a.ichunk)
 ctx.profiling(True)
 stage(v, lists, ctx)
 print("prep ms", ctx.kernel_times()[4])
