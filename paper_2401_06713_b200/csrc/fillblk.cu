@@ -132,7 +132,7 @@ struct BlkLayout {
 
 // descriptors [cb, cb+nd) of the row's flattened (slot, word) list, padded with empty words
 __device__ __forceinline__ void blk_build_desc(const BlkLayout &L, const uint32_t *masks, int cb,
-                                               int nd, int T, int Li) {
+                                               int nd, int T, int Li, uint64_t pol) {
     for (int d = threadIdx.x; d < nd; d += blockDim.x) {
         const int dd = cb + d;
         int2 v = make_int2(0, 0);
@@ -143,7 +143,7 @@ __device__ __forceinline__ void blk_build_desc(const BlkLayout &L, const uint32_
                 if (L.sC[mid] <= dd) lo_s = mid; else hi_s = mid - 1;
             }
             const int q = dd - L.sC[lo_s];
-            v = make_int2(L.sB[lo_s] + 32 * q, (int)__ldg(masks + L.sR[lo_s] + (uint32_t)q));
+            v = make_int2(L.sB[lo_s] + 32 * q, (int)ldg_pol(masks + L.sR[lo_s] + (uint32_t)q, pol));
         }
         L.desc[d] = v;
     }
@@ -188,6 +188,7 @@ __global__ void __launch_bounds__(1024) k_fill_blk(RowArgs a, BlkArgs g) {
     asm("mov.b64 %0, %1;" : "=l"(bmem_l) : "l"(a.bmemp + lane));
     const uint32_t *masks = a.masks;
     const int32_t *compact = a.compact;
+    const uint64_t pol_masks = l2_policy_stream();
     const uint32_t lt = (1u << lane) - 1u;
     const bool own_groups = tid * G < nga;  // this thread's groups exist
     __syncthreads();
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(1024) k_fill_blk(RowArgs a, BlkArgs g) {
             // ---- B: mark (and collect the admitted ids in the row's list while they fit)
             for (int cb = 0; cb < Tp; cb += g.dcap) {
                 const int nd = min(Tp - cb, g.dcap);
-                blk_build_desc(L, masks, cb, nd, T, Li);
+                blk_build_desc(L, masks, cb, nd, T, Li, pol_masks);
                 __syncthreads();
                 for (int d0 = warp * 8; d0 < nd; d0 += NW * 8) {
                     int32_t x[8];
@@ -314,7 +315,7 @@ __global__ void __launch_bounds__(1024) k_fill_blk(RowArgs a, BlkArgs g) {
                 for (int cb = 0; cb < Tp; cb += g.dcap) {
                     const int nd = min(Tp - cb, g.dcap);
                     if (!once) {
-                        blk_build_desc(L, masks, cb, nd, T, Li);
+                        blk_build_desc(L, masks, cb, nd, T, Li, pol_masks);
                         __syncthreads();
                     }
                     for (int d0 = warp * 8; d0 < nd; d0 += NW * 8) {
@@ -394,7 +395,7 @@ int run_blk_t(const RowArgs &a, const BlkArgs &g, int sms, cudaStream_t s) {
 // (padded with INT_MAX), fully unrolled (compile-time indices)
 template <int N, typename OutT, bool COMPACT>
 __device__ __forceinline__ void bins_sort_out(const int32_t *src, int k, OutT *dst,
-                                              const int32_t *compact) {
+                                              const int32_t *compact, uint64_t pol) {
     int32_t v[N];
 #pragma unroll
     for (int t = 0; t < N; ++t) v[t] = t < k ? src[t] : INT_MAX;
@@ -414,7 +415,7 @@ __device__ __forceinline__ void bins_sort_out(const int32_t *src, int k, OutT *d
     }
 #pragma unroll
     for (int t = 0; t < N; ++t)
-        if (t < k) dst[t] = (OutT)(COMPACT ? __ldg(compact + v[t]) : v[t]);
+        if (t < k) stg_pol(dst + t, COMPACT ? __ldg(compact + v[t]) : v[t], pol);
 }
 
 template <typename OutT, bool COMPACT>
@@ -442,6 +443,7 @@ __global__ void __launch_bounds__(1024) k_fill_bins(RowArgs a, BinArgs g) {
     const uint32_t lt = (1u << lane) - 1u;
     const int sh = g.shift;
     const int per = (g.nbins + NT - 1) / NT;  // bins per thread in the scan
+    const uint64_t pol_keep = l2_policy_keep(), pol_out = l2_policy_stream(), pol_masks = pol_out;
     __syncthreads();
 
     for (int64_t ri = a.row_begin + blockIdx.x; ri < a.row_end; ri += gridDim.x) {
@@ -474,7 +476,7 @@ __global__ void __launch_bounds__(1024) k_fill_bins(RowArgs a, BinArgs g) {
         // ---- collect the admitted ids and count them per bin
         for (int cb = 0; cb < Tp; cb += g.dcap) {
             const int nd = min(Tp - cb, g.dcap);
-            blk_build_desc(L, masks, cb, nd, T, Li);
+            blk_build_desc(L, masks, cb, nd, T, Li, pol_masks);
             __syncthreads();
             for (int d0 = warp * 8; d0 < nd; d0 += NW * 8) {
                 int32_t x[8];
@@ -482,7 +484,7 @@ __global__ void __launch_bounds__(1024) k_fill_bins(RowArgs a, BinArgs g) {
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const int2 dv = L.desc[d0 + u];
-                    x[u] = __ldg(bmem_l + (uint32_t)dv.x);
+                    x[u] = ldg_pol(bmem_l + (uint32_t)dv.x, pol_keep);
                     mw[u] = (uint32_t)dv.y;
                 }
                 int cnt = 0;
@@ -535,15 +537,15 @@ __global__ void __launch_bounds__(1024) k_fill_bins(RowArgs a, BinArgs g) {
             const int bl = b > 0 ? bins[b - 1] : 0, bh = bins[b], k = bh - bl;
             if (k == 0) continue;
             if (k <= 8) {
-                bins_sort_out<8, OutT, COMPACT>(buf + bl, k, orow + bl, compact);
+                bins_sort_out<8, OutT, COMPACT>(buf + bl, k, orow + bl, compact, pol_out);
             } else if (k <= 16) {
-                bins_sort_out<16, OutT, COMPACT>(buf + bl, k, orow + bl, compact);
+                bins_sort_out<16, OutT, COMPACT>(buf + bl, k, orow + bl, compact, pol_out);
             } else {
                 for (int p = bl; p < bh; ++p) {
                     const int32_t x = buf[p];
                     int r = bl;
                     for (int q = bl; q < bh; ++q) r += buf[q] < x;
-                    orow[r] = (OutT)(COMPACT ? __ldg(compact + x) : x);
+                    stg_pol(orow + r, COMPACT ? __ldg(compact + x) : x, pol_out);
                 }
             }
         }

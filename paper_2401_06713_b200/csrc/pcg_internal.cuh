@@ -18,6 +18,37 @@ namespace pcg {
 // threads launching the same kernel with different sizes (one thread's smaller cap lands just
 // before the other's launch: invalid argument).  The cap is not an allocation; occupancy
 // follows each launch's actual request.
+// L2 eviction priorities for the fills (PTX createpolicy + .L2::cache_hint): the bucket
+// member gathers are kept (evict_last) while the streaming owned-mask reads and the CSR
+// writes go first, so the 130 MB member array at config 3 stays mostly L2-resident.
+__device__ __forceinline__ uint64_t l2_policy_keep() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_stream() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ int32_t ldg_pol(const int32_t *ptr, uint64_t pol) {
+    int32_t v;
+    asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(ptr), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint32_t ldg_pol(const uint32_t *ptr, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(ptr), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void stg_pol(int32_t *ptr, int32_t v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.s32 [%0], %1, %2;" ::"l"(ptr), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void stg_pol(int64_t *ptr, int32_t v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.s64 [%0], %1, %2;" ::"l"(ptr), "l"((int64_t)v), "l"(pol)
+                 : "memory");
+}
+
 template <typename F>
 inline void allow_max_smem(F kern) {
     static const int optin = [] {
