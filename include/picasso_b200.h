@@ -149,7 +149,9 @@ int pcg_kernel_times(pcg_ctx *ctx, float *ms, int32_t n);
  *                          "d2h_pipe" 1 (default) fill in pieces overlapping the copy-out,
  *                          "d2h_pieces", "d2h_chunk" (ids), "d2h_threads", "d2h_gap16"
  *                          (1 16-bit, 2 8-bit gaps), "d2h_dma" (% of chunks as int64 DMA)
- *   sharded:               "rows_out32" 1: pcg_fill_rows_device writes int32 ids */
+ *   sharded:               "rows_out32" 1: pcg_fill_rows_device writes int32 ids;
+ *                          "rows_out_abs" 1: ... at the rows' global CSR offsets (the
+ *                          pointer is the whole CSR's base: the root's exchange buffer) */
 int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value);
 
 /*
@@ -198,6 +200,20 @@ int pcg_validate(pcg_ctx *ctx, const uint64_t *words, int64_t n_total, int32_t n
  * registers its reused host output buffer once (hostpool.py).
  */
 int pcg_host_register(void *ptr, uint64_t bytes, int32_t on);
+
+/*
+ * Multi-GPU exchange through peer memory (replaces the slice gather of a sharded build,
+ * SURVEY.md §8(e); the reference has no multi-GPU path — its single build is conflict.py:
+ * 89-167).  The root calls pcg_exchange_buffer for a device buffer of `bytes` (reused while
+ * large enough) and its 64-byte CUDA IPC handle; every rank maps it with pcg_exchange_map
+ * (cached per handle) and passes the mapped pointer to pcg_fill_rows_device with
+ * "rows_out32" = 1 and "rows_out_abs" = 1, so its fill stores its rows straight into the
+ * root's HBM over NVLink, at their global offsets.  After a barrier the root copies the int32 ids to its int64 host
+ * output with pcg_ids_to_host.
+ */
+int pcg_exchange_buffer(pcg_ctx *ctx, uint64_t bytes, void **dptr, uint8_t *handle);
+int pcg_exchange_map(pcg_ctx *ctx, const uint8_t *handle, void **dptr);
+int pcg_ids_to_host(pcg_ctx *ctx, const int32_t *src_dev, int64_t count, int64_t *dst);
 
 /*
  * With the option "k1_async" set, pcg_count launches the commuting-pair sweep (K1) on a side

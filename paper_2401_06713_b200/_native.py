@@ -111,6 +111,12 @@ def library():
         lib.pcg_launch_total.restype = ctypes.c_int64
         lib.pcg_stream.argtypes = [_VP]
         lib.pcg_stream.restype = _VP
+        lib.pcg_exchange_buffer.argtypes = [_VP, ctypes.c_uint64, ctypes.POINTER(_VP), _VP]
+        lib.pcg_exchange_buffer.restype = ctypes.c_int
+        lib.pcg_exchange_map.argtypes = [_VP, _VP, ctypes.POINTER(_VP)]
+        lib.pcg_exchange_map.restype = ctypes.c_int
+        lib.pcg_ids_to_host.argtypes = [_VP, _VP, _I64, _VP]
+        lib.pcg_ids_to_host.restype = ctypes.c_int
         for name in ("pcg_create", "pcg_destroy", "pcg_set_inputs", "pcg_count",
                      "pcg_copy_degrees", "pcg_fill", "pcg_fill_rows", "pcg_count_device",
                      "pcg_fill_device", "pcg_build_device", "pcg_set_profiling",
@@ -127,7 +133,8 @@ EXPORTED = (
     "pcg_build_device", "pcg_set_profiling", "pcg_kernel_times", "pcg_set_option", "pcg_stream",
     "pcg_degrees_device", "pcg_fill_rows_device", "pcg_prep_device", "pcg_color_dynamic",
     "pcg_assign_lists", "pcg_validate", "pcg_host_register", "pcg_last_copy_bytes",
-    "pcg_k1_result", "pcg_color_dynamic_mt", "pcg_launch_total",
+    "pcg_k1_result", "pcg_color_dynamic_mt", "pcg_launch_total", "pcg_exchange_buffer",
+    "pcg_exchange_map", "pcg_ids_to_host",
 )
 
 
@@ -143,8 +150,9 @@ class Context:
         h = _VP()
         rc = self.lib.pcg_create(int(device), ctypes.byref(h))
         if rc != PCG_OK:
+            why = self.lib.pcg_last_error(None).decode(errors="replace")
             raise DeviceError(f"pcg_create(device={device}) failed with code {rc}: "
-                              "no usable CUDA device")
+                              f"no usable CUDA device ({why})")
         self.h = h
         self.device = device
 
@@ -255,6 +263,26 @@ class Context:
                                                   ctypes.byref(lo), ctypes.byref(hi)),
                     "pcg_fill_rows_device")
         return int(lo.value), int(hi.value)
+
+    def exchange_buffer(self, nbytes: int) -> tuple:
+        """(device pointer, 64-byte IPC handle) of this context's exported exchange buffer."""
+        p, h = _VP(), ctypes.create_string_buffer(64)
+        self._check(self.lib.pcg_exchange_buffer(self.h, ctypes.c_uint64(max(int(nbytes), 16)),
+                                                 ctypes.byref(p), h), "pcg_exchange_buffer")
+        return int(p.value), bytes(h.raw)
+
+    def exchange_map(self, handle: bytes) -> int:
+        """A peer's exchange buffer mapped into this device's address space (cached)."""
+        p = _VP()
+        hb = ctypes.create_string_buffer(bytes(handle), 64)
+        self._check(self.lib.pcg_exchange_map(self.h, hb, ctypes.byref(p)), "pcg_exchange_map")
+        return int(p.value)
+
+    def ids_to_host(self, src_ptr: int, out: np.ndarray) -> None:
+        """int32 ids at a device pointer -> the int64 host array ``out`` (widened)."""
+        assert out.dtype == np.int64 and out.flags.c_contiguous
+        self._check(self.lib.pcg_ids_to_host(self.h, _VP(src_ptr), int(out.size), _ptr(out)),
+                    "pcg_ids_to_host")
 
     def assign_lists(self, active: np.ndarray, base_key: int, P: int, L: int, base: int) -> np.ndarray:
         active = np.ascontiguousarray(active, dtype=np.int64)

@@ -127,18 +127,28 @@ extern "C" {
 
 int pcg_version(void) { return 1; }
 
+// why the last pcg_create failed (pcg_last_error(NULL)), per host thread
+static thread_local std::string g_create_err = "null context";
+
 int pcg_create(int device, pcg_ctx **out) {
     if (!out) return PCG_E_ARG;
     *out = nullptr;
     int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || device < 0 || device >= ndev) {
+        g_create_err = e != cudaSuccess ? std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e)
+                                        : "device " + std::to_string(device) + " of " +
+                                              std::to_string(ndev);
         cudaGetLastError();
         return PCG_E_CUDA;
     }
     pcg_ctx *ctx = new pcg_ctx();
     ctx->device = device;
-    if (cudaSetDevice(device) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        g_create_err = std::string("device ") + std::to_string(device) + ": " + cudaGetErrorString(e);
+        cudaGetLastError();
         delete ctx;
         return PCG_E_CUDA;
     }
@@ -161,6 +171,8 @@ int pcg_destroy(pcg_ctx *ctx) {
                       &ctx->vkeys2, &ctx->vvals, &ctx->vvals2, &ctx->vcnt, &ctx->voff,
                       &ctx->vpairs};
     for (DevBuf *b : bufs) release(*b);
+    for (auto &m : ctx->xmaps) cudaIpcCloseMemHandle(m.second);
+    release(ctx->xbuf);
     for (void *p : ctx->ring)
         if (p) cudaFreeHost(p);
     for (auto &e : ctx->ring_ev) cudaEventDestroy(e);
@@ -194,7 +206,7 @@ int pcg_destroy(pcg_ctx *ctx) {
     return PCG_OK;
 }
 
-const char *pcg_last_error(const pcg_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+const char *pcg_last_error(const pcg_ctx *ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
 
 int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     if (!ctx || !key) return PCG_E_ARG;
@@ -227,6 +239,7 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "bins_shift")) ctx->bins_shift = (int)value;
     else if (!strcmp(key, "bins_maxdeg")) ctx->bins_maxdeg = (int)value;
     else if (!strcmp(key, "rows_out32")) ctx->rows_out32 = (int)value;
+    else if (!strcmp(key, "rows_out_abs")) ctx->rows_out_abs = (int)value;
     else if (!strcmp(key, "seg_warps")) ctx->seg_warps = (int)value;
     else return fail(ctx, PCG_E_ARG, std::string("unknown option ") + key);
     return PCG_OK;
@@ -2007,10 +2020,12 @@ extern "C" int pcg_fill_rows_device(pcg_ctx *ctx, const int32_t *global_deg_dev,
     *slice_end = lohi[1];
     if (!neighbors_dev || lohi[1] == lohi[0]) return PCG_OK;
     int l = 0;
+    // option "rows_out_abs": neighbors_dev is the whole CSR's base (the rows land at their
+    // global offsets: the root's exchange buffer), not the slice's.
     // option "rows_out32": the slice is written as int32 (a sharded build all-gathers half
     // the bytes and widens after the exchange)
     rc = fill_rows_device(ctx, r0, r1, ctx->gdeg.as<int32_t>(), maxdeg, nm == n, neighbors_dev,
-                          lohi[0], &l, /*out64=*/ctx->rows_out32 == 0);
+                          ctx->rows_out_abs ? 0 : lohi[0], &l, /*out64=*/ctx->rows_out32 == 0);
     ctx->launch_total += l + 3;  // + the prefix scans and compaction
     if (rc) return rc;
     PCG_TRY_CUDA(ctx, cudaStreamSynchronize(s));
@@ -2185,3 +2200,62 @@ extern "C" int pcg_host_register(void *ptr, uint64_t bytes, int32_t on) {
 // Bytes the last pcg_fill copied device -> host (members, offsets and the encoded neighbor
 // ids), for the benchmark's e2e accounting.
 extern "C" int64_t pcg_last_copy_bytes(const pcg_ctx *ctx) { return ctx ? ctx->copy_bytes : 0; }
+
+// --------------------------------------------------------------------------------------
+// Multi-GPU exchange through peer memory (distributed.py, exchange="p2p").  The root rank
+// exports one device buffer (the canonical CSR's int32 ids); every rank maps it and its fill
+// (pcg_fill_rows_device with rows_out32) stores its rows straight into the root's HBM over
+// NVLink as they are produced — the slice transfer overlaps the fill row by row, with no
+// separate gather.  Handles are CUDA IPC handles (64 bytes), exchanged by the caller's
+// process group; a buffer is reused (and its handle stays valid) while it is large enough.
+// --------------------------------------------------------------------------------------
+extern "C" int pcg_exchange_buffer(pcg_ctx *ctx, uint64_t bytes, void **dptr, uint8_t *handle) {
+    if (!ctx || !dptr || !handle) return PCG_E_ARG;
+    PCG_TRY_CUDA(ctx, cudaSetDevice(ctx->device));
+    PCG_ALLOC(ctx, ctx->xbuf, (size_t)bytes);
+    if (ctx->xhandle_of != ctx->xbuf.p) {
+        PCG_TRY_CUDA(ctx, cudaIpcGetMemHandle(&ctx->xhandle, ctx->xbuf.p));
+        ctx->xhandle_of = ctx->xbuf.p;
+    }
+    *dptr = ctx->xbuf.p;
+    memcpy(handle, &ctx->xhandle, sizeof(cudaIpcMemHandle_t));
+    return PCG_OK;
+}
+
+extern "C" int pcg_exchange_map(pcg_ctx *ctx, const uint8_t *handle, void **dptr) {
+    if (!ctx || !dptr || !handle) return PCG_E_ARG;
+    PCG_TRY_CUDA(ctx, cudaSetDevice(ctx->device));
+    const std::string key(reinterpret_cast<const char *>(handle), sizeof(cudaIpcMemHandle_t));
+    for (auto &m : ctx->xmaps)
+        if (m.first == key) {
+            *dptr = m.second;
+            return PCG_OK;
+        }
+    // a new buffer from this peer (it grew): drop the old mappings
+    for (auto &m : ctx->xmaps) cudaIpcCloseMemHandle(m.second);
+    ctx->xmaps.clear();
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void *p = nullptr;
+    PCG_TRY_CUDA(ctx, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    ctx->xmaps.emplace_back(key, p);
+    *dptr = p;
+    return PCG_OK;
+}
+
+// int32 ids in device memory -> the int64 host array (pinned or pageable), widened on the
+// way (the root's copy-out of the exchanged CSR)
+extern "C" int pcg_ids_to_host(pcg_ctx *ctx, const int32_t *src_dev, int64_t count, int64_t *dst) {
+    if (!ctx || count < 0 || (count > 0 && (!src_dev || !dst))) return PCG_E_ARG;
+    if (count == 0) return PCG_OK;
+    PCG_TRY_CUDA(ctx, cudaSetDevice(ctx->device));
+    cudaPointerAttributes at{};
+    const bool pinned = cudaPointerGetAttributes(&at, dst) == cudaSuccess &&
+                        at.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    const int rc = pinned ? d2h_widen_direct(ctx, dst, src_dev, (size_t)count)
+                          : d2h_widen(ctx, dst, src_dev, (size_t)count);
+    if (rc) return rc;
+    PCG_TRY_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return PCG_OK;
+}

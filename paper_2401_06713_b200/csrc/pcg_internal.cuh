@@ -315,6 +315,12 @@ struct pcg_ctx {
     int64_t mask_words = 0;   // owned/bucket mask words of the staged build
     pcg::DevBuf bnd;          // segmented fill window bounds
     pcg::DevBuf vcolor, vkeys, vkeys2, vvals, vvals2, vcnt, voff, vpairs;  // validator
+    // multi-GPU exchange through peer memory: this rank's exported buffer (the root's CSR
+    // ids, written by every rank's fill) and the peers' buffers mapped here
+    pcg::DevBuf xbuf;
+    cudaIpcMemHandle_t xhandle{};
+    void *xhandle_of = nullptr;  // the allocation xhandle was taken from
+    std::vector<std::pair<std::string, void *>> xmaps;  // handle bytes -> mapped pointer
     // pipelined D2H of the neighbor ids: ring of pinned staging chunks
     int d2h_chunk = 0;        // ids per chunk (0 auto)
     int d2h_threads = 0;      // host widening threads (0 auto)
@@ -341,6 +347,7 @@ struct pcg_ctx {
     unsigned char *hs = nullptr;  // pinned scratch for the small per-build readbacks (512 B)
     int64_t launch_total = 0;     // kernels launched by this context (pcg_launch_total)
     int rows_out32 = 0;           // pcg_fill_rows_device writes int32 ids (sharded exchange)
+    int rows_out_abs = 0;         // ... at the rows' global CSR offsets (peer exchange buffer)
     int k1_early = 1;             // with k1_async: launch K1 from the prep (k1_launch_early)
     bool k1_early_valid = false;  // an early K1 of the staged build is in flight (scal[7])
     int k1_slot = 0;              // scal word pcg_k1_result reads (0, or 7 for the early K1)

@@ -67,20 +67,33 @@ class NativeEngine:
     def degrees(self, rows):
         return self.ctx.degrees(rows)
 
-    def fill_rows_device(self, global_deg, out_ptr, out32: bool = False):
-        """The rank's CSR slice into a device buffer, int64 or int32 (None: bounds only)."""
+    def fill_rows_device(self, global_deg, out_ptr, out32: bool = False, absolute: bool = False):
+        """The rank's CSR slice into a device buffer, int64 or int32 (None: bounds only);
+        ``absolute``: out_ptr is the whole CSR's base (the rows go to their global offsets)."""
         import torch
 
         g = torch.from_numpy(np.ascontiguousarray(global_deg, dtype=np.int32)).cuda()
         mx = int(global_deg.max()) if global_deg.size else 0
         torch.cuda.synchronize()  # the upload (torch's stream) before the context's stream reads it
         self.ctx.option("rows_out32", 1 if out32 else 0)
+        self.ctx.option("rows_out_abs", 1 if absolute else 0)
         try:
             lohi = self.ctx.fill_rows_device(g.data_ptr(), mx, out_ptr)
         finally:
             self.ctx.option("rows_out32", 0)
+            self.ctx.option("rows_out_abs", 0)
         torch.cuda.synchronize()
         return lohi
+
+    # peer-memory exchange (exchange="p2p"): the root's exported buffer, mapped by every rank
+    def exchange_buffer(self, nbytes: int):
+        return self.ctx.exchange_buffer(nbytes)
+
+    def exchange_map(self, handle: bytes) -> int:
+        return self.ctx.exchange_map(handle)
+
+    def ids_to_host(self, ptr: int, out: np.ndarray) -> None:
+        self.ctx.ids_to_host(ptr, out)
 
     def fill_rows(self, global_deg, want_values: bool):
         lo, hi = self.ctx.fill_rows(global_deg, None)
@@ -114,9 +127,25 @@ def _all_gather_rows(dist, local: np.ndarray, ranges, dev) -> np.ndarray:
     return np.concatenate([o[: sizes[r]].cpu().numpy() for r, o in enumerate(out)]) if world else local
 
 
+def _share_handle(dist, handle: Optional[bytes], root: int, dev) -> bytes:
+    """The root's 64-byte IPC handle on every rank (a broadcast over the process group)."""
+    import torch
+
+    t = torch.zeros(64, dtype=torch.uint8)
+    if handle is not None:
+        t[:] = torch.frombuffer(bytearray(handle), dtype=torch.uint8)
+    t = t.to(dev)
+    dist.broadcast(t, src=root)
+    return bytes(t.cpu().numpy().tobytes())
+
+
+def p2p_available(engine) -> bool:
+    return hasattr(engine, "exchange_buffer") and hasattr(engine, "fill_rows_device")
+
+
 def build_sharded(view, lists, *, edge_budget: Optional[int] = None, threads: int = 1,
                   block_pairs: int = 1 << 20, two_phase: bool = True, engine=None,
-                  gather: str = "root", root: int = 0):
+                  gather: str = "root", root: int = 0, exchange: str = "auto"):
     """The conflict build of ``conflict.build``, sharded over the default process group.
 
     ``gather="root"``: the root rank returns the canonical ConflictGraph (bit-identical to
@@ -124,12 +153,20 @@ def build_sharded(view, lists, *, edge_budget: Optional[int] = None, threads: in
     same members, offsets, edge_count and view_edges_scanned, with an empty neighbor array.
     ``gather="all"``: every rank returns the whole graph.  Budget errors are raised on every
     rank, with the caller's exception class (conflict._error_types).
+
+    ``exchange`` (gather="root"): "p2p" — the root exports one device buffer for the CSR's
+    int32 ids (a CUDA IPC handle, broadcast over the process group) and every rank's fill
+    stores its rows straight into it over NVLink while it produces them; "collective" — each
+    rank fills a local slice and the process group gathers the slices to the root; "auto"
+    (default) — p2p when the engine is the native (GPU) one.
     """
     import torch
     import torch.distributed as dist
 
     if gather not in ("root", "all"):
         raise ValueError("gather must be 'root' or 'all'")
+    if exchange not in ("auto", "p2p", "collective"):
+        raise ValueError("exchange must be 'auto', 'p2p' or 'collective'")
     rank, world = dist.get_rank(), dist.get_world_size()
     dev = _coll_device(dist)
     engine = engine or NativeEngine()
@@ -164,6 +201,25 @@ def build_sharded(view, lists, *, edge_budget: Optional[int] = None, threads: in
     # every slice's length follows from the gathered degrees
     starts = np.concatenate([[0], np.cumsum(gdeg.astype(np.int64))])
     lens_np = [int(starts[b] - starts[a]) for a, b in ranges]
+    p2p = gather == "root" and (exchange == "p2p" or (exchange == "auto" and p2p_available(engine)))
+    if p2p:
+        if not p2p_available(engine):
+            raise ValueError("exchange='p2p' needs the native (GPU) engine")
+        # the root's CSR buffer in its HBM; every rank's fill writes its rows into it
+        ptr, handle = engine.exchange_buffer(4 * max(2 * total, 1)) if rank == root else (0, None)
+        handle = _share_handle(dist, handle, root, dev)
+        base = ptr if rank == root else engine.exchange_map(handle)
+        if lens_np[rank]:
+            engine.fill_rows_device(gdeg, base, out32=True, absolute=True)
+        dist.barrier()  # every rank's fill has completed (its stream synchronized)
+        if rank == root:
+            nbr = hostpool.empty_int64(2 * total)
+            engine.ids_to_host(ptr, nbr)
+        else:
+            nbr = np.zeros(0, dtype=np.int64)
+        return CG(members=members_ids, graph=EG(n=int(members_ids.size), offsets=offsets,
+                                                  neighbors=nbr),
+                  edge_count=total, view_edges_scanned=pairs - anti)
     width = max(max(lens_np, default=0), 1)
     device_fill = dev.type == "cuda" and hasattr(engine, "fill_rows_device")
     t = torch.zeros(width, dtype=torch.int32 if device_fill else torch.int64, device=dev)
@@ -204,7 +260,7 @@ def build_sharded(view, lists, *, edge_budget: Optional[int] = None, threads: in
 
 
 def run_sharded(view, params, *, strategy: str = "dynamic", edge_budget: Optional[int] = None,
-                block_pairs: int = 1 << 20, engine=None, root: int = 0):
+                block_pairs: int = 1 << 20, engine=None, root: int = 0, exchange: str = "auto"):
     """The whole Picasso run (driver.run) with every conflict build sharded over the default
     process group.  The root rank colors each conflict graph (list_coloring, the reference's
     draw order) and broadcasts the outcome; every rank returns the identical ColoringResult."""
@@ -217,7 +273,8 @@ def run_sharded(view, params, *, strategy: str = "dynamic", edge_budget: Optiona
 
     def builder(v, lists, **kw):
         kw.pop("threads", None)
-        return build_sharded(v, lists, engine=engine, gather="root", root=root, **kw)
+        return build_sharded(v, lists, engine=engine, gather="root", root=root,
+                             exchange=exchange, **kw)
 
     def coloring(gc, lists, strategy, seed, iteration):
         box = [None]
@@ -266,6 +323,21 @@ def bench_sharded(args) -> None:
     ctx.option("rows_out32", 1)  # the timed step exchanges int32 slices
     deg_local = torch.zeros(width, dtype=torch.int32, device=dev)
     gdeg_parts = torch.zeros(world * width, dtype=torch.int32, device=dev)
+    # exchange: "p2p" (default) — every rank's fill stores its rows into the root's CSR
+    # buffer over NVLink (CUDA IPC mapping, set up once: the buffer is reused every step);
+    # "collective" (PICASSO_EXCHANGE=collective) — int32 slices gathered by NCCL
+    exchange = os.environ.get("PICASSO_EXCHANGE", "p2p")
+    xbase = [0]
+    if exchange == "p2p":
+        ctx.option("rows_out_abs", 1)
+        ctx.prep_device()
+        ctx.count(rank, world, r0, r1)
+        ctx.degrees_device(deg_local.data_ptr())
+        dist.all_gather_into_tensor(gdeg_parts, deg_local)
+        total_ids = int(gdeg_parts.to(torch.int64).sum().item())
+        ptr, handle = ctx.exchange_buffer(4 * max(total_ids, 1)) if rank == 0 else (0, None)
+        handle = _share_handle(dist, handle, 0, dev)
+        xbase[0] = ptr if rank == 0 else ctx.exchange_map(handle)
 
     def step():
         # input prep (buckets replicated, owned masks of this rank's rows) + count of its shard
@@ -276,6 +348,10 @@ def bench_sharded(args) -> None:
         gdeg = torch.cat([gdeg_parts[k * width: k * width + (ranges[k][1] - ranges[k][0])]
                           for k in range(world)])
         mx = int(gdeg.max().item()) if n else 0
+        if exchange == "p2p":  # the rows go straight into the root's HBM
+            ctx.fill_rows_device(gdeg.data_ptr(), mx, xbase[0])
+            dist.barrier()
+            return c
         lo, hi = ctx.fill_rows_device(gdeg.data_ptr(), mx, None)
         lens = torch.tensor([hi - lo], dtype=torch.int64, device=dev)
         all_lens = torch.zeros(world, dtype=torch.int64, device=dev)
@@ -311,6 +387,7 @@ def bench_sharded(args) -> None:
     ms = float(t.item())
 
     ctx.option("rows_out32", 0)
+    ctx.option("rows_out_abs", 0)
     ctx.option("own_rows_lo", 0)
     ctx.option("own_rows_hi", -1)
     # ---- end to end through the public sharded build (host inputs in, the canonical int64
@@ -340,7 +417,10 @@ def bench_sharded(args) -> None:
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic", "config": bench_mod.config_for(args.workload, world),
             "sharding": "K1 work items and K2 row ranges by rank, owned masks of the rank's "
-                        "rows, NCCL degree all-gather + int32 CSR slice gather to rank 0",
+                        "rows, NCCL degree all-gather; " + (
+                            "each rank's fill stores its int32 CSR rows straight into rank 0's "
+                            "buffer over NVLink (CUDA IPC peer memory)" if exchange == "p2p" else
+                            "int32 CSR slices gathered to rank 0 by NCCL"),
             "e2e": {"value": pairs / e2e_s, "unit": "pairs/s",
                     # root rank: its inputs and the gathered degrees up; down: the degrees and
                     # the canonical int64 CSR (members and offsets are derived on the host

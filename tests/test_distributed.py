@@ -66,7 +66,8 @@ class OracleEngine:
         return lo, hi, (self.csr.neighbors[lo:hi].copy() if want else None)
 
 
-def _worker(rank, world, port, name, budget, two_phase, q, native=False, gather="root"):
+def _worker(rank, world, port, name, budget, two_phase, q, native=False, gather="root",
+            exchange="auto"):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -93,7 +94,7 @@ def _worker(rank, world, port, name, budget, two_phase, q, native=False, gather=
             eng._r0 = dmod.row_ranges(case.view.n_active, world)[rank][0]
         try:
             gc = dmod.build_sharded(case.view, case.lists, engine=eng, edge_budget=budget,
-                                    two_phase=two_phase, gather=gather)
+                                    two_phase=two_phase, gather=gather, exchange=exchange)
             if gather == "all" or rank == 0:
                 case.check(gc)
             else:  # the header: everything but the neighbor ids
@@ -114,13 +115,13 @@ def _worker(rank, world, port, name, budget, two_phase, q, native=False, gather=
 
 
 def _run(world, name, budget=None, two_phase=True, native=False, gather="root", target=None,
-         args=None):
+         args=None, exchange="auto"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     target = target or _worker
     args = args if args is not None else (name, budget, two_phase)
-    extra = (native, gather) if target is _worker else (native,)
+    extra = (native, gather, exchange) if target is _worker else (native, exchange)
     procs = [ctx.Process(target=target, args=(r, world, port, *args, q, *extra))
              for r in range(world)]
     for p in procs:
@@ -141,7 +142,7 @@ def test_sharded_build_matches_golden(world, name, gather):
     assert [r[1] for r in res] == ["ok"] * world, res
 
 
-def _run_worker(rank, world, port, name, q, native=False):
+def _run_worker(rank, world, port, name, q, native=False, exchange="auto"):
     """A whole sharded Picasso run (distributed.run_sharded) on one rank."""
     import sys
 
@@ -164,7 +165,7 @@ def _run_worker(rank, world, port, name, q, native=False):
         v = pauli_view(r["n"], r["q"], r["gen_seed"])
         eng = dmod.NativeEngine(0) if native else OracleEngine()
         res = dmod.run_sharded(v, b200.PaletteParams(r["palette_pct"], r["alpha"], seed=r["seed"]),
-                               strategy=r["strategy"], engine=eng)
+                               strategy=r["strategy"], engine=eng, exchange=exchange)
         ok = (sha(res.color) == r["color_sha"] and res.total_colors == r["colors"]
               and len(res.iterations) == r["iterations"] and res.oracle_edges == r["oracle_edges"]
               and res.peak_conflict_edges == r["peak_conflict_edges"])
@@ -202,20 +203,69 @@ def test_row_ranges_cover_rows():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,name,gather", [(2, "c1_iter1", "root"), (3, "induced_subset", "all"),
-                                               (2, "ragged_lists", "root")])
-def test_sharded_native_engine_on_one_gpu(world, name, gather):
+@pytest.mark.parametrize("world,name,gather,exchange",
+                         [(2, "c1_iter1", "root", "p2p"), (2, "c1_iter1", "root", "collective"),
+                          (3, "induced_subset", "all", "auto"), (2, "ragged_lists", "root", "p2p"),
+                          (3, "tc_all_modes_pauli", "root", "p2p"), (3, "two_vertices", "root", "p2p")])
+def test_sharded_native_engine_on_one_gpu(world, name, gather, exchange):
     """Each rank runs the CUDA K1 work-item shard + the owned masks of its rows + K2 row shard
-    + sharded fill (all ranks share cuda:0); the gathered CSR must equal the reference."""
-    res = _run(world, name, native=True, gather=gather)
+    + sharded fill (all ranks share cuda:0); the root's CSR must equal the reference.  With
+    exchange="p2p" every rank's fill stores its rows into the root's exported buffer (CUDA
+    IPC between the rank processes, here on one device); "collective" gathers slices."""
+    res = _run(world, name, native=True, gather=gather, exchange=exchange)
     assert [r[1] for r in res] == ["ok"] * world, res
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,name", [(2, "c1"), (3, "tout_k4")])
-def test_sharded_whole_run_native_on_one_gpu(world, name):
-    res = _run(world, name, native=True, target=_run_worker, args=(name,))
+@pytest.mark.parametrize("world,name,exchange", [(2, "c1", "p2p"), (3, "tout_k4", "p2p"),
+                                                 (2, "c1", "collective")])
+def test_sharded_whole_run_native_on_one_gpu(world, name, exchange):
+    res = _run(world, name, native=True, target=_run_worker, args=(name,), exchange=exchange)
     assert [r[1] for r in res] == ["ok"] * world, res
+
+
+@pytest.mark.gpu
+def test_sharded_p2p_exchange_q32_20k_golden(golden_ref):
+    """Three ranks on one GPU, peer-memory exchange: the root's CSR of the reference's
+    20k-vertex q=32 build (hashes from the reference run) and the 4-byte id stores of three
+    processes into one exported buffer."""
+    res = _run(3, "q32_n20000", native=True, target=_p2p_worker, args=("q32_n20000",))
+    assert [r[1] for r in res] == ["ok"] * 3, res
+
+
+def _p2p_worker(rank, world, port, name, q, native=True, exchange="p2p"):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import json
+
+        from conftest import pauli_view, random_lists, sha
+        from paper_2401_06713_b200 import distributed as dmod
+
+        with open(os.path.join(ROOT, "tests", "golden", "reference.json")) as f:
+            g = json.load(f)["builds_hashed"][name]
+        v = pauli_view(20000, 32, 0)
+        for _ in range(2):  # the second build reuses the exported buffer and the mappings
+            gc = dmod.build_sharded(v, random_lists(v, seed=0), engine=dmod.NativeEngine(0),
+                                    exchange=exchange)
+            ok = sha(gc.graph.offsets) == g["offsets_sha"]
+            if rank == 0:
+                ok = ok and sha(gc.graph.neighbors) == g["neighbors_sha"]
+            if not ok:
+                break
+        q.put((rank, "ok" if ok else "mismatch", None))
+    except Exception:  # report, don't hang the other ranks
+        import traceback
+
+        q.put((rank, "error", traceback.format_exc()[-1500:]))
+    finally:
+        dist.destroy_process_group()
 
 
 @pytest.mark.gpu
