@@ -161,13 +161,14 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(busy), "sm_max_mhz": mx, "reasons": reasons}
 
 
-def measured_traffic(kernel: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`, from the committed
-    ncu --set full capture of this bench command (profiles/roofline_traffic.json, written by
-    tools/profile_summary.py); None when no capture is committed."""
+def measured_traffic(kernel: str, workload: str = ""):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` on `workload`, from
+    the committed ncu --set full capture of this bench command (profiles/roofline_traffic.json,
+    written by tools/profile_summary.py); None when no capture is committed."""
     try:
         with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
-            rec = json.load(f).get(kernel)
+            recs = json.load(f)
+        rec = recs.get(f"{workload}:{kernel}")
         return None if rec is None else (float(rec["dram_bytes_per_launch"]), "profiles/" + rec["source"])
     except (OSError, ValueError, KeyError):
         return None
@@ -368,7 +369,7 @@ def measure_workload(name, args, local, clocks_on: bool):
     k1_kernel = "k_commute_fr8" if q <= 128 else "k_commute_fr"
     speak, speak_src, bpc = smem_peak(sm_mhz)
     k1_ach = pairs * bpp / (k1_ms * 1e-3) / 1e9
-    k1_traffic = measured_traffic(k1_kernel) or (None, None)
+    k1_traffic = measured_traffic(k1_kernel, name) or (None, None)
     roof_k1 = {"bound": "smem", "kernel": f"commuting-pair sweep K1 ({k1_kernel})",
                "achieved": k1_ach, "peak": speak, "unit": "GB/s", "frac": k1_ach / speak,
                "traffic": k1_traffic[0], "traffic_source": k1_traffic[1],
@@ -385,7 +386,7 @@ def measure_workload(name, args, local, clocks_on: bool):
     fill_bytes = (2 * edges) * 4 + (members + 1) * 8 + members * 8 + n * plan.list_size * 4 + words_b
     fill_ach = fill_bytes / (fill_ms * 1e-3) / 1e9
     fill_kernel = "k_fill_bins" if n >= 40000 else "k_fill_blk"  # the auto choice (abi.cu)
-    fill_traffic = measured_traffic(fill_kernel) or (None, None)
+    fill_traffic = measured_traffic(fill_kernel, name) or (None, None)
     roof_fill = {"bound": "hbm", "kernel": f"conflict-row fill ({fill_kernel})", "achieved": fill_ach,
                  "peak": hbm, "unit": "GB/s", "frac": fill_ach / hbm, "traffic": fill_traffic[0],
                  "traffic_source": fill_traffic[1], "bytes_per_launch": int(fill_bytes),

@@ -133,11 +133,9 @@ void *pcg_stream(pcg_ctx *ctx);
 int pcg_kernel_times(pcg_ctx *ctx, float *ms, int32_t n);
 /* Kernel configuration knobs (testing/tuning; 0 = auto unless noted).  Every setting gives
  * the same CSR; the defaults are the measured fastest.
- *   K1 (commuting pairs):  "k1_algo" 1 direct LOP3/POPC tiles, 2 four-Russians 4-bit slices,
- *                          4 four-Russians 6-bit slices (default for q <= 64); "k1_wide" 1
- *                          (default) 64-bit 4-bit-slice table
- *                          entries; "fr_ichunk" rows per work item; "k1_async" 1 runs K1 on a
- *                          side stream (pcg_k1_result collects it)
+ *   K1 (commuting pairs):  "k1_algo" 1 direct LOP3/POPC tiles, 5 four-Russians 8-bit slices
+ *                          (default for q <= 128); "fr_ichunk" rows per work item; "k1_async"
+ *                          1 runs K1 on a side stream (pcg_k1_result collects it)
  *   K2 (conflict rows):    "k2_mode" 1 partner gather, 2 bucket masks, 3 owned masks;
  *                          "own_algo" 0 four-Russians / 1 per-pair masks; "own_direct" 0 forces
  *                          the hash ownership table; "window" row-pass bitmap (ids)

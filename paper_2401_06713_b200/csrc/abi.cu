@@ -163,7 +163,7 @@ int pcg_destroy(pcg_ctx *ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     DevBuf *bufs[] = {&ctx->words, &ctx->active, &ctx->lists64, &ctx->loff, &ctx->A, &ctx->B,
-                      &ctx->H, &ctx->lrel, &ctx->rowof, &ctx->keys2, &ctx->vals2, &ctx->bstart,
+                      &ctx->lrel, &ctx->rowof, &ctx->keys2, &ctx->vals2, &ctx->bstart,
                       &ctx->cubtmp, &ctx->deg, &ctx->degu, &ctx->compact, &ctx->rowoff,
                       &ctx->scal, &ctx->bad, &ctx->members_o, &ctx->offsets_o, &ctx->nbr_o,
                       &ctx->gdeg, &ctx->items, &ctx->eidx, &ctx->bpos, &ctx->bmemp,
@@ -222,8 +222,6 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "d2h_threads")) ctx->d2h_threads = (int)value;
     else if (!strcmp(key, "d2h_mode")) ctx->d2h_mode = (int)value;
     else if (!strcmp(key, "k1_async")) ctx->k1_async = (int)value;
-    else if (!strcmp(key, "k1_wide")) ctx->k1_wide = (int)value;
-    else if (!strcmp(key, "k1_lds")) ctx->k1_lds = (int)value;
     else if (!strcmp(key, "own_rows_lo")) ctx->own_lo = value;
     else if (!strcmp(key, "own_rows_hi")) ctx->own_hi = value;
     else if (!strcmp(key, "k1_early")) ctx->k1_early = (int)value;
@@ -350,23 +348,6 @@ static BucketArgs bucket_args(const pcg_ctx *ctx) {
 static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, int *launches,
                   cudaStream_t s, unsigned long long *anti);
 
-// four-Russians row offsets of the bit planes (the layout of the selected K1 kernel)
-static bool fr6_supported(int32_t kw) { return kw == 2 || kw == 4; }
-
-static int fr_offsets(pcg_ctx *ctx, cudaStream_t s) {
-    if (!fr_supported(ctx->kw)) return PCG_OK;
-    // the 8-bit kernel (the default for kw 2/4/6/8) and the 6-bit one read the bit planes
-    // directly
-    if (fr8_supported(ctx->kw) && (ctx->k1_algo == 0 || ctx->k1_algo == 5)) return PCG_OK;
-    if (fr6_supported(ctx->kw) && ctx->k1_algo == 4) return PCG_OK;
-    PCG_ALLOC(ctx, ctx->H, (size_t)ctx->npad * ctx->kw * 4 * 4);
-    ctx->h_wide = fr_jb(ctx->kw, ctx->k1_wide) == K1_FR_JB2;
-    if (ctx->h_wide) launch_fr_prep2(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
-    else launch_fr_prep(ctx->A.as<uint32_t>(), ctx->kw, ctx->npad, ctx->H.as<uint32_t>(), s);
-    PCG_CHECK_LAUNCH(ctx);
-    return PCG_OK;
-}
-
 // K1 launched from the input prep, right after the bit planes exist (option "k1_early", with
 // "k1_async"): the commuting-pair sweep then overlaps the bucket sort and the owned masks as
 // well as the count and fill passes.  It accumulates into its own counter (scal[7]); the count
@@ -439,8 +420,6 @@ static int prep_device(pcg_ctx *ctx) {
     PrepTrace tr(s);
     tr.mark("start");
     int rc = encode_vectors(ctx, false);
-    if (rc) return rc;
-    rc = fr_offsets(ctx, s);
     if (rc) return rc;
     rc = k1_launch_early(ctx, s);
     if (rc) return rc;
@@ -524,8 +503,6 @@ static int prep_device(pcg_ctx *ctx) {
             ctx->k1_early_valid = false;
         }
         rc = encode_vectors(ctx, true);
-        if (rc) return rc;
-        rc = fr_offsets(ctx, s);
         if (rc) return rc;
     }
     // bucket masks when they fit comfortably (dense corners with huge buckets use the
@@ -626,7 +603,7 @@ static int prep_device(pcg_ctx *ctx) {
     tr.mark("(end)");
     PCG_ALLOC(ctx, ctx->deg, (size_t)n_active * 4);
     PCG_ALLOC(ctx, ctx->degu, (size_t)n_active * 4);
-    ctx->prep_launches = 6 + (bad[0] ? 1 : 0) + (ctx->masked ? 1 : 0) + (fr_supported(ctx->kw) ? 1 : 0) +
+    ctx->prep_launches = 6 + (bad[0] ? 1 : 0) + (ctx->masked ? 1 : 0) +
                          (ctx->k1_early_valid ? 1 : 0);  // + the early K1 sweep
     if (ctx->prof) {
         cudaEventRecord(ctx->ev[11], s);
@@ -667,7 +644,7 @@ extern "C" int pcg_set_inputs(pcg_ctx *ctx, const uint64_t *words, int64_t n_tot
     ctx->P = std::max<int64_t>(1, (palette_size + 63) / 64) * 64;
     palette_size = ctx->P;
     ctx->ragged = list_off != nullptr;
-    ctx->npad = round_up(n_active, K1_FR_JB2);
+    ctx->npad = round_up(n_active, K1_NPAD);
     int64_t entries = 0;
     int32_t lmax = list_len;
     if (ctx->ragged) {
@@ -715,22 +692,15 @@ extern "C" int pcg_set_inputs(pcg_ctx *ctx, const uint64_t *words, int64_t n_tot
 // --------------------------------------------------------------------------------------
 // count pass
 // --------------------------------------------------------------------------------------
-// 1 direct tiles, 2 four-Russians 4-bit slices, 4 6-bit slices, 5 8-bit slices (the default
-// where supported: kw 2/4/6/8; k1_algo 3, 5-bit slices, was measured slower and removed)
+// 1 direct tiles, 5 four-Russians 8-bit slices (the default where supported: kw 2/4/6/8,
+// q <= 128; the 4-, 5- and 6-bit four-Russians kernels were measured slower and removed)
 static int k1_algo(const pcg_ctx *ctx) {
     if (ctx->k1_algo == 1) return 1;
-    if (ctx->k1_algo == 2 && fr_supported(ctx->kw)) return 2;
-    if (ctx->k1_algo == 4 && fr6_supported(ctx->kw)) return 4;
-    if (fr8_supported(ctx->kw)) return 5;
-    if (fr6_supported(ctx->kw)) return 4;
-    return fr_supported(ctx->kw) ? 2 : 1;
+    return fr8_supported(ctx->kw) ? 5 : 1;
 }
 
-// rows per K1 work item: 8192 for the 8-bit kernel (measured at 1M x 64q: 2048 32.2 ms,
-// 4096 31.1, 8192 30.1), 2048 for the others
-static int64_t fr_ichunk(const pcg_ctx *ctx, bool fr8) {
-    return ctx->fr_ichunk > 0 ? ctx->fr_ichunk : fr8 ? 8192 : 2048;
-}
+// rows per K1 work item (measured at 1M x 64q: 2048 32.2 ms, 4096 31.1, 8192 30.1)
+static int64_t fr_ichunk(const pcg_ctx *ctx) { return ctx->fr_ichunk > 0 ? ctx->fr_ichunk : 8192; }
 
 // pairs (i<j, both < n) inside four-Russians item (jb, rows [i0,i1))
 static int64_t fr_item_pairs(int64_t n, int64_t jb, int64_t i0, int64_t i1, int64_t JB) {
@@ -766,14 +736,13 @@ static int64_t direct_pairs(int64_t n, int64_t T, int64_t t0, int64_t t1) {
 static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, int *launches,
                   cudaStream_t s, unsigned long long *anti) {
     const int64_t n = ctx->n;
-    if (k1_algo(ctx) >= 2) {
-        const bool fr6 = k1_algo(ctx) == 4, fr8 = k1_algo(ctx) == 5;
-        const int64_t JB = fr8 ? fr8_jb(ctx->kw) : (ctx->h_wide && !fr6) ? K1_FR_JB2 : K1_FR_JB;
-        const int64_t njb = ctx->npad / JB, ic = fr_ichunk(ctx, fr8);
-        // item_start runs over the blocks in visit order; the 8-bit kernel folds the triangle
+    if (k1_algo(ctx) == 5) {
+        const int64_t JB = fr8_jb(ctx->kw);
+        const int64_t njb = ctx->npad / JB, ic = fr_ichunk(ctx);
+        // item_start runs over the blocks in visit order; the kernel folds the triangle
         // (blocks 0, njb-1, 1, njb-2, ...) so that every CTA's item range spans about the
         // same number of table rebuilds (a short early block is paired with a long late one)
-        auto jb_of = [&](int64_t v) { return fr8 ? fr8_fold(v, njb) : v; };
+        auto jb_of = [&](int64_t v) { return fr8_fold(v, njb); };
         std::vector<int64_t> start(njb + 1, 0);
         for (int64_t v = 0; v < njb; ++v) {
             // (a padding block past the last row has no pairs and no items)
@@ -799,23 +768,9 @@ static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, 
         PCG_ALLOC(ctx, ctx->items, (size_t)(njb + 1) * 8);
         PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->items.p, start.data(), (size_t)(njb + 1) * 8,
                                           cudaMemcpyHostToDevice, s));
-        if (fr8)
-            *launches += launch_commute_fr8_items(ctx->A.as<uint32_t>(), ctx->B.as<uint32_t>(),
-                                                  ctx->kw, n, ctx->items.as<int64_t>(), njb,
-                                                  (int32_t)ic, i0, i1, anti, ctx->sms, s);
-        else if (fr6)
-            *launches += launch_commute_fr6_items(ctx->A.as<uint32_t>(), ctx->B.as<uint32_t>(),
-                                                  ctx->kw, n, ctx->items.as<int64_t>(), njb,
-                                                  (int32_t)ic, i0, i1, anti, ctx->sms,
-                                                  ctx->k1_lds == 128 ? 1 : 0, s);
-        else if (ctx->h_wide)
-            *launches += launch_commute_fr2_items(ctx->B.as<uint32_t>(), ctx->H.as<uint32_t>(),
-                                                  ctx->kw, n, ctx->items.as<int64_t>(), njb,
-                                                  (int32_t)ic, i0, i1, anti, ctx->sms, s);
-        else
-            *launches += launch_commute_fr_items(ctx->B.as<uint32_t>(), ctx->H.as<uint32_t>(),
-                                                 ctx->kw, n, ctx->items.as<int64_t>(), njb,
-                                                 (int32_t)ic, i0, i1, anti, ctx->sms, s);
+        *launches += launch_commute_fr8_items(ctx->A.as<uint32_t>(), ctx->B.as<uint32_t>(),
+                                              ctx->kw, n, ctx->items.as<int64_t>(), njb,
+                                              (int32_t)ic, i0, i1, anti, ctx->sms, s);
     } else {
         const int64_t T = ctx->npad / K1_TILE, NT = tri_tiles(T);
         const int64_t t0 = NT * shard / nshards, t1 = NT * (shard + 1) / nshards;
@@ -2103,7 +2058,7 @@ extern "C" int pcg_validate(pcg_ctx *ctx, const uint64_t *words, int64_t n_total
     ctx->n = n_active;
     ctx->nwords = nwords;
     ctx->q = num_qubits;
-    ctx->npad = round_up(n_active, K1_FR_JB2);
+    ctx->npad = round_up(n_active, K1_NPAD);
     PCG_ALLOC(ctx, ctx->bad, 16);
     PCG_ALLOC(ctx, ctx->scal, 64);
     PCG_ALLOC(ctx, ctx->words, (size_t)n_total * nwords * 8);
@@ -2126,8 +2081,6 @@ extern "C" int pcg_validate(pcg_ctx *ctx, const uint64_t *words, int64_t n_total
         if (rc) return rc;
     }
     // |E|: the commuting-pair sweep (K1)
-    rc = fr_offsets(ctx, s);
-    if (rc) return rc;
     PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->scal.p, 0, 64, s));
     int64_t pairs = 0;
     int launches = 0;

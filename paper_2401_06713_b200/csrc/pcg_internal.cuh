@@ -84,8 +84,7 @@ void release(DevBuf &b);
 // Geometry of the commuting-pair sweep (K1).
 // ---------------------------------------------------------------------------
 constexpr int K1_TILE = 128;  // rows == cols of one upper-triangle tile (direct kernel)
-constexpr int K1_FR_JB = 1024;  // j-block of the four-Russians kernel (32 lanes x 32 bits)
-constexpr int K1_FR_JB2 = 2048; // j-block of the wide four-Russians kernel (32 lanes x 64 bits)
+constexpr int K1_NPAD = 2048;   // rows of the bit planes are padded to a multiple of this
 
 // ---------------------------------------------------------------------------
 // Arguments of the conflict-row kernels (K2).
@@ -195,18 +194,6 @@ int launch_bucket_bounds(const int32_t *sorted_colors, const int32_t *eidx, cons
 int launch_commute_direct(const uint32_t *A, const uint32_t *B, int32_t kw, int64_t npad,
                           int64_t tile0, int64_t tile1, unsigned long long *anti, int sms,
                           cudaStream_t s);
-bool fr_supported(int32_t kw);
-int launch_commute_fr_items(const uint32_t *B, const uint32_t *H, int32_t kw, int64_t n,
-                            const int64_t *item_start, int64_t njb, int32_t ichunk,
-                            int64_t item0, int64_t item1, unsigned long long *anti, int sms,
-                            cudaStream_t s);
-int launch_fr_prep(const uint32_t *A, int32_t kw, int64_t npad, uint32_t *H, cudaStream_t s);
-int fr_jb(int32_t kw, int wide);
-int launch_commute_fr6_items(const uint32_t *A, const uint32_t *B, int32_t kw, int64_t n,
-                             const int64_t *item_start, int64_t njb, int32_t ichunk,
-                             int64_t item0, int64_t item1, unsigned long long *anti, int sms,
-                             int wide_loads, cudaStream_t s);
-int launch_fr_prep2(const uint32_t *A, int32_t kw, int64_t npad, uint32_t *H, cudaStream_t s);
 bool fr8_supported(int32_t kw);
 // visit order of the 8-bit K1's partner blocks: 0, njb-1, 1, njb-2, ... (a permutation)
 __host__ __device__ inline int64_t fr8_fold(int64_t v, int64_t njb) {
@@ -214,10 +201,6 @@ __host__ __device__ inline int64_t fr8_fold(int64_t v, int64_t njb) {
 }
 int fr8_jb(int32_t kw);
 int launch_commute_fr8_items(const uint32_t *A, const uint32_t *B, int32_t kw, int64_t n,
-                             const int64_t *item_start, int64_t njb, int32_t ichunk,
-                             int64_t item0, int64_t item1, unsigned long long *anti, int sms,
-                             cudaStream_t s);
-int launch_commute_fr2_items(const uint32_t *B, const uint32_t *H, int32_t kw, int64_t n,
                              const int64_t *item_start, int64_t njb, int32_t ichunk,
                              int64_t item0, int64_t item1, unsigned long long *anti, int sms,
                              cudaStream_t s);
@@ -273,9 +256,6 @@ struct pcg_ctx {
     int64_t own_lo = 0, own_hi = -1;  // options own_rows_lo/hi: rows whose owned-mask rows
                                       // the prep computes (-1: all; sharded builds)
     int64_t prep_lo = 0, prep_hi = 0; // the range the current masks hold
-    int k1_lds = 128;   // 6-bit K1 lookup width: 128 (LDS.128, quarter-warp rows) or 64
-    int k1_wide = 1;    // four-Russians with 64-bit entries (2048-partner blocks) when kw <= 4
-    bool h_wide = false;  // the staged H offsets are in the wide kernel's format
     int window = 0;     // K2 window bits (0 auto)
     int fr_ichunk = 0;  // four-Russians i-chunk (0 auto)
     int fill_algo = 0;  // owned masks: 0 auto (block fill up to 128K ids, else the bins fill
@@ -301,7 +281,7 @@ struct pcg_ctx {
     void *stage[2] = {nullptr, nullptr};  // pinned D2H staging (32 MiB each)
 
     // device buffers
-    pcg::DevBuf words, active, lists64, loff, A, B, H, lrel, rowof, keys2, vals2, bstart,
+    pcg::DevBuf words, active, lists64, loff, A, B, lrel, rowof, keys2, vals2, bstart,
         cubtmp, deg, degu, compact, rowoff, scal, bad, members_o, offsets_o, nbr_o, gdeg, items,
         eidx, bpos, bmemp, posof, maskoff, masks;
     int prep_launches = 0;

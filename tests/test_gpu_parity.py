@@ -16,16 +16,12 @@ from conftest import oracle_builder, pauli_view, random_lists, sha
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=[(1, 0), (2, 0), (2, 1), (4, 0), (5, 0)],
-                ids=["k1-direct", "k1-fourrussians", "k1-fourrussians-wide", "k1-fourrussians-6bit",
-                     "k1-fourrussians-8bit"])
+@pytest.fixture(params=[1, 5], ids=["k1-direct", "k1-fourrussians-8bit"])
 def k1_algo(request):
     ctx = _native.context()
-    ctx.option("k1_algo", request.param[0])
-    ctx.option("k1_wide", request.param[1])
+    ctx.option("k1_algo", request.param)
     yield request.param
     ctx.option("k1_algo", 0)
-    ctx.option("k1_wide", 1)
 
 
 @pytest.fixture(params=[1, 2, 3], ids=["k2-gather", "k2-bucketmasks", "k2-owned"])

@@ -15,6 +15,10 @@ fi
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+# the sharded (torchrun) path with one rank: peer-memory exchange into its own buffer
+PICASSO_FORCE_SHARDED=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 \
+   --master-addr 127.0.0.1 --master-port 29555 bench.py --steps 5 --warmup 3 \
+   > $OUT/bench_sharded1.json 2> $OUT/bench_sharded1.err
 for W in c3 c2; do
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $OUT/launches_$W.csv \
      python bench.py --workload $W --secondary '' --steps 2 --warmup 3 --no-cpu-baseline --no-clocks --no-run \

@@ -23,7 +23,7 @@ RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "l1tex__data_pipe_lsu_wa
 STALLS = "smsp__pcsamp_warps_issue_stalled_"
 traffic = {}
 out = ["# ncu --set full summaries (" + os.path.basename(src.rstrip('/')) + ")", "",
-       "One capture per kernel of `bench.py --steps 1 --warmup 3` (config 2), "
+       "One capture per kernel of `bench.py --workload W --steps 1 --warmup 3`, "
        "`--clock-control none`. Times under ncu are serialised and cold-cache; compare shares, "
        "not absolutes.", ""]
 for f in sorted(os.listdir(src)):
@@ -58,11 +58,13 @@ for f in sorted(os.listdir(src)):
         scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         nbytes = sum(float(rawv[k]) * scale[units[k]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         short = kname.split("::")[-1].split("(")[0].split("<")[0].strip()
-        traffic[short] = {"dram_bytes_per_launch": nbytes, "kernel": kname,
-                          "source": os.path.basename(prefix) + "_ncu_summary.md"}
+        wl = f.split("_")[1] if f.startswith("full_") else ""  # full_<workload>_<kernel>
+        traffic[f"{wl}:{short}" if wl else short] = {
+            "dram_bytes_per_launch": nbytes, "kernel": kname, "workload": wl,
+            "source": os.path.basename(prefix) + "_ncu_summary.md"}
     except (ValueError, KeyError):
         pass
-    out.append(f"## `{kname[:110]}`")
+    out.append(f"## `{kname[:110]}`" + (f" — {f.split('_')[1]}" if f.startswith("full_") else ""))
     out.append("")
     out.append("| metric | value |")
     out.append("|---|---|")

@@ -23,8 +23,6 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--seg-bits", type=int, default=0)
 ap.add_argument("--seg-warps", type=int, default=0)
 ap.add_argument("--own", type=int, default=0)
-ap.add_argument("--wide", type=int, default=1)
-ap.add_argument("--k1-lds", type=int, default=128)
 ap.add_argument("--own-direct", type=int, default=1)
 ap.add_argument("--blk-threads", type=int, default=0)
 ap.add_argument("--blk-groups", type=int, default=0)
@@ -53,8 +51,6 @@ ctx.option("fill_algo", a.fill)
 ctx.option("seg_bits", a.seg_bits)
 ctx.option("seg_warps", a.seg_warps)
 ctx.option("own_algo", a.own)
-ctx.option("k1_wide", a.wide)
-ctx.option("k1_lds", a.k1_lds)
 ctx.option("own_direct", a.own_direct)
 ctx.option("blk_threads", a.blk_threads)
 ctx.option("blk_groups", a.blk_groups)

@@ -9,7 +9,7 @@ import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2401_06713_b200", "libpicasso_b200.so")
-DEFAULT = ["k_commute_fr6", "k_owned_fr", "k_count_owned", "k_fill_blk", "k_fill_bins", "k_delta",
+DEFAULT = ["k_commute_fr8", "k_commute_direct", "k_owned_fr", "k_count_owned", "k_fill_blk", "k_fill_bins", "k_delta",
            "k_encode", "k_lists", "k_bucket_bounds", "k_compact"]
 SHOW = 12
 KEY = {"LDS", "STS", "POPC", "PRMT", "ATOMS", "REDS", "RED", "LDG", "STG", "BAR", "SHFL", "FLO"}
