@@ -173,6 +173,7 @@ int pcg_destroy(pcg_ctx *ctx) {
     for (DevBuf *b : bufs) release(*b);
     for (auto &m : ctx->xmaps) cudaIpcCloseMemHandle(m.second);
     release(ctx->xbuf);
+    release(ctx->workctr);
     for (void *p : ctx->ring)
         if (p) cudaFreeHost(p);
     for (auto &e : ctx->ring_ev) cudaEventDestroy(e);
@@ -238,6 +239,8 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "bins_maxdeg")) ctx->bins_maxdeg = (int)value;
     else if (!strcmp(key, "rows_out32")) ctx->rows_out32 = (int)value;
     else if (!strcmp(key, "rows_out_abs")) ctx->rows_out_abs = (int)value;
+    else if (!strcmp(key, "dyn_work")) ctx->dyn_work = (int)value;
+    else if (!strcmp(key, "k1_warps")) ctx->k1_warps = (int)value;
     else if (!strcmp(key, "seg_warps")) ctx->seg_warps = (int)value;
     else return fail(ctx, PCG_E_ARG, std::string("unknown option ") + key);
     return PCG_OK;
@@ -348,9 +351,10 @@ static BucketArgs bucket_args(const pcg_ctx *ctx) {
 static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, int *launches,
                   cudaStream_t s, unsigned long long *anti);
 
-// K1 launched from the input prep, right after the bit planes exist (option "k1_early", with
-// "k1_async"): the commuting-pair sweep then overlaps the bucket sort and the owned masks as
-// well as the count and fill passes.  It accumulates into its own counter (scal[7]); the count
+// K1 launched from the input prep, once the color buckets are sorted (option "k1_early", with
+// "k1_async"): the commuting-pair sweep (8 warps per SM) then overlaps the owned masks, the
+// count and the fill passes, which take their work from atomic counters (dyn_work) so that
+// their CTAs resident next to K1 do the work.  It accumulates into its own counter (scal[7]); the count
 // pass of the same build (one shard) takes it over instead of launching K1 again.
 static int k1_launch_early(pcg_ctx *ctx, cudaStream_t s) {
     ctx->k1_early_valid = false;
@@ -420,8 +424,6 @@ static int prep_device(pcg_ctx *ctx) {
     PrepTrace tr(s);
     tr.mark("start");
     int rc = encode_vectors(ctx, false);
-    if (rc) return rc;
-    rc = k1_launch_early(ctx, s);
     if (rc) return rc;
     PCG_ALLOC(ctx, ctx->lrel, (size_t)entries * 4);
     PCG_ALLOC(ctx, ctx->rowof, (size_t)entries * 4);
@@ -497,14 +499,13 @@ static int prep_device(pcg_ctx *ctx) {
     if (bad[1] & 2) return fail(ctx, PCG_E_COLOR, "a list color lies outside the palette");
     if (bad[1] & 4) return fail(ctx, PCG_E_DUPLICATE, "a color list names the same color twice");
     if (bad[0]) {  // invalid 3-bit codes: exact raw-word predicate
-        if (ctx->k1_early_valid) {  // the early K1 read the wrong planes: drop it
-            PCG_TRY_CUDA(ctx, cudaEventSynchronize(ctx->k1_done));
-            ctx->k1_pending = false;
-            ctx->k1_early_valid = false;
-        }
         rc = encode_vectors(ctx, true);
         if (rc) return rc;
     }
+    // K1 starts here, after the bucket sort (CUB's onesweep sort cannot share an SM with it)
+    // and before the owned masks, the count and the fill, whose CTAs fill the SMs next to it
+    rc = k1_launch_early(ctx, s);
+    if (rc) return rc;
     // bucket masks when they fit comfortably (dense corners with huge buckets use the
     // partner-gather row kernel instead; both are exact).  Free memory is queried once per
     // context (and again only when a decision is close), not on every build.
@@ -586,6 +587,11 @@ static int prep_device(pcg_ctx *ctx) {
         if (ctx->owned) {
             OwnArgs &o = own;
             PCG_TRY_CUDA(ctx, cudaMemsetAsync(o.overflow, 0, 4, s));
+            if (ctx->dyn_work) {  // colors from an atomic counter (see work_first)
+                PCG_ALLOC(ctx, ctx->workctr, 64);
+                PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->workctr.p, 0, 8, s));
+                o.work = ctx->workctr.as<unsigned long long>();
+            }
             launch_owned_masks(b, o, ctx->sms, s);
             PCG_CHECK_LAUNCH(ctx);
             // the per-pair mask kernel (own_algo 1) always writes every row
@@ -768,9 +774,12 @@ static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, 
         PCG_ALLOC(ctx, ctx->items, (size_t)(njb + 1) * 8);
         PCG_TRY_CUDA(ctx, cudaMemcpyAsync(ctx->items.p, start.data(), (size_t)(njb + 1) * 8,
                                           cudaMemcpyHostToDevice, s));
+        // 8 warps when K1 shares the SMs with the row passes (its side stream), else 16
+        const int warps = ctx->k1_warps > 0 ? ctx->k1_warps
+                                            : (ctx->k1_stream && s == ctx->k1_stream) ? 8 : 16;
         *launches += launch_commute_fr8_items(ctx->A.as<uint32_t>(), ctx->B.as<uint32_t>(),
                                               ctx->kw, n, ctx->items.as<int64_t>(), njb,
-                                              (int32_t)ic, i0, i1, anti, ctx->sms, s);
+                                              (int32_t)ic, i0, i1, anti, ctx->sms, warps, s);
     } else {
         const int64_t T = ctx->npad / K1_TILE, NT = tri_tiles(T);
         const int64_t t0 = NT * shard / nshards, t1 = NT * (shard + 1) / nshards;
@@ -1689,7 +1698,13 @@ static int fill_rows_device(pcg_ctx *ctx, int64_t r0, int64_t r1, const int32_t 
         if (ctx->blk_dcap > 0) g.dcap = (ctx->blk_dcap + 7) & ~7;
         g.ecap = (std::max(maxdeg, 1) + 31) & ~31;
         if (bins_smem_bytes(g) <= 227u * 1024u && g.nbins <= (1 << 16)) {
-            *launches += launch_fill_bins(a, g, out64, ctx->sms, s);
+            RowArgs ab = a;
+            if (ctx->dyn_work) {  // rows from an atomic counter (see work_first)
+                PCG_ALLOC(ctx, ctx->workctr, 64);
+                PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->workctr.as<unsigned long long>() + 1, 0, 8, s));
+                ab.work = ctx->workctr.as<unsigned long long>() + 1;
+            }
+            *launches += launch_fill_bins(ab, g, out64, ctx->sms, s);
             PCG_CHECK_LAUNCH(ctx);
             return PCG_OK;
         }

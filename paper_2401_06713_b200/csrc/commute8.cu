@@ -30,7 +30,6 @@ namespace pcg {
 
 namespace {
 
-constexpr int FR8_WARPS = 16;
 
 __host__ __device__ constexpr int ctz_c(int k) { return (k & 1) ? 0 : 1 + ctz_c(k >> 1); }
 
@@ -57,13 +56,13 @@ __device__ __forceinline__ void lds128(uint32_t addr, uint32_t &a, uint32_t &b, 
                  : "r"(addr));
 }
 
-template <int KW>
+template <int KW, int FR8_WARPS>
 __global__ void __launch_bounds__(FR8_WARPS * 32, 1) k_commute_fr8(
     const uint32_t *__restrict__ A, const uint32_t *__restrict__ B, int64_t n,
     const int64_t *__restrict__ item_start, int64_t njb, int32_t ichunk, int64_t item0,
     int64_t item1, unsigned long long *__restrict__ anti) {
     using G = Fr8Geom<KW>;
-    constexpr int K = G::K, S = G::S, EB = G::EB, JB = G::JB, LPR = G::LPR, RPQ = G::RPQ,
+    constexpr int S = G::S, EB = G::EB, JB = G::JB, LPR = G::LPR, RPQ = G::RPQ,
                   RPW = G::RPW, STRIDE = G::STRIDE, BTW = G::BTW, BTS = G::BTS;
     constexpr int NT = FR8_WARPS * 32;
     extern __shared__ __align__(128) uint32_t smem[];
@@ -245,19 +244,31 @@ __global__ void __launch_bounds__(FR8_WARPS * 32, 1) k_commute_fr8(
     }
 }
 
+template <int KW, int NW>
+int run_fr8_w(const uint32_t *A, const uint32_t *B, int64_t n, const int64_t *item_start,
+              int64_t njb, int32_t ichunk, int64_t item0, int64_t item1,
+              unsigned long long *anti, int sms, cudaStream_t s) {
+    const size_t smem = Fr8Geom<KW>::SMEM;
+    allow_max_smem(k_commute_fr8<KW, NW>);
+    prefer_max_shared(k_commute_fr8<KW, NW>);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_commute_fr8<KW, NW>, NW * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * sms, item1 - item0));
+    k_commute_fr8<KW, NW><<<(unsigned)grid, NW * 32, smem, s>>>(A, B, n, item_start, njb, ichunk,
+                                                               item0, item1, anti);
+    return 1;
+}
+
+// 16 warps (the whole register file) when K1 runs alone; 8 when it shares the SMs with the
+// row passes (k1_async): half the registers stay free for their CTAs
 template <int KW>
 int run_fr8(const uint32_t *A, const uint32_t *B, int64_t n, const int64_t *item_start,
             int64_t njb, int32_t ichunk, int64_t item0, int64_t item1,
-            unsigned long long *anti, int sms, cudaStream_t s) {
-    const size_t smem = Fr8Geom<KW>::SMEM;
-    allow_max_smem(k_commute_fr8<KW>);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_commute_fr8<KW>, FR8_WARPS * 32, smem);
-    if (per_sm < 1) per_sm = 1;
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * sms, item1 - item0));
-    k_commute_fr8<KW><<<(unsigned)grid, FR8_WARPS * 32, smem, s>>>(A, B, n, item_start, njb, ichunk,
-                                                                   item0, item1, anti);
-    return 1;
+            unsigned long long *anti, int sms, int warps, cudaStream_t s) {
+    if (warps == 8)
+        return run_fr8_w<KW, 8>(A, B, n, item_start, njb, ichunk, item0, item1, anti, sms, s);
+    return run_fr8_w<KW, 16>(A, B, n, item_start, njb, ichunk, item0, item1, anti, sms, s);
 }
 
 }  // namespace
@@ -277,13 +288,13 @@ int fr8_jb(int32_t kw) {
 int launch_commute_fr8_items(const uint32_t *A, const uint32_t *B, int32_t kw, int64_t n,
                              const int64_t *item_start, int64_t njb, int32_t ichunk,
                              int64_t item0, int64_t item1, unsigned long long *anti, int sms,
-                             cudaStream_t s) {
+                             int warps, cudaStream_t s) {
     if (item1 <= item0) return 0;
     switch (kw) {
-        case 2: return run_fr8<2>(A, B, n, item_start, njb, ichunk, item0, item1, anti, sms, s);
-        case 4: return run_fr8<4>(A, B, n, item_start, njb, ichunk, item0, item1, anti, sms, s);
-        case 6: return run_fr8<6>(A, B, n, item_start, njb, ichunk, item0, item1, anti, sms, s);
-        case 8: return run_fr8<8>(A, B, n, item_start, njb, ichunk, item0, item1, anti, sms, s);
+        case 2: return run_fr8<2>(A, B, n, item_start, njb, ichunk, item0, item1, anti, sms, warps, s);
+        case 4: return run_fr8<4>(A, B, n, item_start, njb, ichunk, item0, item1, anti, sms, warps, s);
+        case 6: return run_fr8<6>(A, B, n, item_start, njb, ichunk, item0, item1, anti, sms, warps, s);
+        case 8: return run_fr8<8>(A, B, n, item_start, njb, ichunk, item0, item1, anti, sms, warps, s);
         default: return 0;
     }
 }

@@ -446,7 +446,9 @@ __global__ void __launch_bounds__(1024) k_fill_bins(RowArgs a, BinArgs g) {
     const uint64_t pol_keep = l2_policy_keep(), pol_out = l2_policy_stream(), pol_masks = pol_out;
     __syncthreads();
 
-    for (int64_t ri = a.row_begin + blockIdx.x; ri < a.row_end; ri += gridDim.x) {
+    __shared__ long long witem;
+    for (int64_t ri = a.row_begin + work_first(a.work, &witem); ri < a.row_end;
+         ri = a.row_begin + work_next(a.work, &witem, ri - a.row_begin)) {
         const int64_t i = a.rows_list ? (int64_t)a.rows_list[ri] : ri;
         if (a.deg[i] == 0) continue;
         const int64_t lo = a.loff ? a.loff[i] : i * a.L;
@@ -560,6 +562,7 @@ int run_bins(const RowArgs &a, const BinArgs &g, int sms, cudaStream_t s) {
     const size_t smem = bins_smem_bytes(g);
     auto kern = k_fill_bins<OutT, COMPACT>;
     allow_max_smem(kern);
+    prefer_max_shared(kern);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, g.threads, smem);
     if (per_sm < 1) per_sm = 1;

@@ -228,7 +228,8 @@ __global__ void __launch_bounds__(OWN_THREADS, (KW <= 4 ? 4 : 3)) k_owned_fr(Buc
     } else {
         for (int x = tid; x < HS; x += OWN_THREADS) osm[x] = 0u;
     }
-    for (int64_t c = blockIdx.x; c < b.P; c += gridDim.x) {
+    __shared__ long long witem;
+    for (int64_t c = work_first(o.work, &witem); c < b.P; c = work_next(o.work, &witem, c)) {
         const int m = b.bstart[c + 1] - b.bstart[c];
         if (m < 2) {
             if (m == 1 && tid == 0) b.masks[b.maskoff[c]] = 0u;
@@ -556,6 +557,8 @@ int run_owned_fr(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s)
     const size_t smem1 = owned_fr_smem(o, KW, false), smem2 = owned_fr_smem(o, KW, true);
     allow_max_smem(k_owned_fr<KW, false>);
     allow_max_smem(k_owned_fr<KW, true>);
+    prefer_max_shared(k_owned_fr<KW, false>);
+    prefer_max_shared(k_owned_fr<KW, true>);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k_owned_fr<KW, false>, OWN_THREADS, smem1);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_owned_fr<KW, true>, OWN_THREADS, smem2);
     const bool db = per2 >= per1 && per2 >= 1;

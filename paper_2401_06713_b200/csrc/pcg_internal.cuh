@@ -67,6 +67,17 @@ inline void allow_max_smem(F kern) {
         cudaGetLastError();  // the launch itself reports a request above the cap
 }
 
+// The SM's L1/shared split is set when a CTA lands on an idle SM, from the kernel's preferred
+// carveout.  K1 (136 KB of tables) would otherwise get the smallest split that fits it and
+// leave no shared memory for the owned-mask and fill CTAs meant to run next to it: the
+// kernels that share SMs ask for the whole carveout.
+template <typename F>
+inline void prefer_max_shared(F kern) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             (int)cudaSharedmemCarveoutMaxShared) != cudaSuccess)
+        cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // Device memory: grow-only buffers owned by one context.
 // ---------------------------------------------------------------------------
@@ -115,6 +126,7 @@ struct RowArgs {
     const int64_t *maskoff; // (P+1) word offset of each color's commute-mask matrix
     const uint32_t *masks;  // per color: m rows of ceil(m/32) words, bit t = commute(k, t)
     const int32_t *rows_list; // if set: process rows rows_list[row_begin..row_end) instead
+    unsigned long long *work; // if set (zeroed): rows handed out by an atomic counter
 };
 
 struct OwnArgs {
@@ -133,7 +145,27 @@ struct OwnArgs {
     int32_t lcap;          // direct mode: losers per level (0: 1024)
     int32_t row_lo, row_hi;  // four-Russians kernel: mask rows only for members in [lo, hi)
                              // (a sharded build's own rows; other rows are left unwritten)
+    unsigned long long *work;  // if set (zeroed): colors handed out by an atomic counter
 };
+
+// Work distribution of the persistent row/color loops.  Static (item += gridDim.x) when
+// `work` is null; otherwise every CTA takes the next item from an atomic counter, so the
+// CTAs that are resident take all the work — the ones that only fit once the concurrently
+// running K1 has drained find the counter exhausted.  Block-uniform; `slot` is __shared__.
+__device__ __forceinline__ int64_t work_first(unsigned long long *work, long long *slot) {
+    if (!work) return blockIdx.x;
+    if (threadIdx.x == 0) *slot = (long long)atomicAdd(work, 1ull);
+    __syncthreads();
+    return *slot;
+}
+__device__ __forceinline__ int64_t work_next(unsigned long long *work, long long *slot,
+                                             int64_t cur) {
+    if (!work) return cur + gridDim.x;
+    __syncthreads();  // every thread has read the current item
+    if (threadIdx.x == 0) *slot = (long long)atomicAdd(work, 1ull);
+    __syncthreads();
+    return *slot;
+}
 
 struct SegArgs {
     int32_t wb;            // window bits per warp bitmap (1024 * S)
@@ -203,7 +235,7 @@ int fr8_jb(int32_t kw);
 int launch_commute_fr8_items(const uint32_t *A, const uint32_t *B, int32_t kw, int64_t n,
                              const int64_t *item_start, int64_t njb, int32_t ichunk,
                              int64_t item0, int64_t item1, unsigned long long *anti, int sms,
-                             cudaStream_t s);
+                             int warps, cudaStream_t s);
 int launch_rows(const RowArgs &a, bool fill, bool out64, int sms, cudaStream_t s);
 int launch_bucket_layout(const BucketArgs &b, int64_t entries, cudaStream_t s);
 int launch_bucket_masks(const BucketArgs &b, int sms, cudaStream_t s);
@@ -298,6 +330,9 @@ struct pcg_ctx {
     // multi-GPU exchange through peer memory: this rank's exported buffer (the root's CSR
     // ids, written by every rank's fill) and the peers' buffers mapped here
     pcg::DevBuf xbuf;
+    pcg::DevBuf workctr;  // atomic work counters of the dynamically scheduled kernels
+    int dyn_work = 1;     // K2a and the bins fill take their items from an atomic counter
+    int k1_warps = 0;     // K1 CTA size: 0 auto (8 warps next to the row passes, else 16)
     cudaIpcMemHandle_t xhandle{};
     void *xhandle_of = nullptr;  // the allocation xhandle was taken from
     std::vector<std::pair<std::string, void *>> xmaps;  // handle bytes -> mapped pointer

@@ -35,6 +35,8 @@ ap.add_argument("--early", type=int, default=1)
 ap.add_argument("--check", action="store_true", help="compare the CSR with the default fill")
 ap.add_argument("--pct", type=float, default=12.5)
 ap.add_argument("--ichunk", type=int, default=0)
+ap.add_argument("--k1-warps", type=int, default=0)
+ap.add_argument("--dyn", type=int, default=1)
 ap.add_argument("--alpha", type=float, default=2.0)
 a = ap.parse_args()
 
@@ -61,6 +63,8 @@ ctx.option("bins_maxdeg", a.bins_maxdeg)
 ctx.option("k1_async", a.k1_async)
 ctx.option("k1_early", a.early)
 ctx.option("fr_ichunk", a.ichunk)
+ctx.option("k1_warps", a.k1_warps)
+ctx.option("dyn_work", a.dyn)
 ctx.profiling(True)
 stage(v, lists, ctx)
 print("prep ms", ctx.kernel_times()[4])
