@@ -354,6 +354,13 @@ def measure_workload(name, args, local, clocks_on: bool):
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     with ClockSampler(local if clocks_on else None) as clocks:
         c, times, kt, launches = device_steps(ctx, stream, args.steps, args.warmup, flush)
+    # K1 alone (outside the timed region): one build with K1 on the builder's stream, 16 warps,
+    # nothing beside it — the kernel's own fraction of its bound, next to the in-step one
+    ctx.option("k1_async", 0)
+    l2_flush(flush)
+    ctx.build_device()
+    k1_alone_ms = float(ctx.kernel_times()[0])
+    ctx.option("k1_async", 1)
     del flush
     ctx.profiling(False)  # the public build runs without the per-phase events
     e2e_t, h2d, d2h, out_bytes = e2e_steps(view, lists, args.steps, args.warmup, local)
@@ -374,6 +381,12 @@ def measure_workload(name, args, local, clocks_on: bool):
                "achieved": k1_ach, "peak": speak, "unit": "GB/s", "frac": k1_ach / speak,
                "traffic": k1_traffic[0], "traffic_source": k1_traffic[1],
                "bytes_per_launch": int(pairs * bpp), "launch_ms": k1_ms,
+               "alone": {"launch_ms": k1_alone_ms,
+                         "achieved": pairs * bpp / (k1_alone_ms * 1e-3) / 1e9,
+                         "frac": pairs * bpp / (k1_alone_ms * 1e-3) / 1e9 / speak,
+                         "note": "one build with K1 alone on the builder's stream (16 warps); "
+                                 "in the timed steps K1 (8 warps) shares every SM with the "
+                                 "owned-mask kernel, which finishes inside K1's launch"},
                "note": f"algorithmic bytes = shared-memory table bytes: {bpp} B per pair (one "
                        "32-byte table entry per 8-bit slice per 256 partners, read as LDS.128 by "
                        "lane pairs, 4 rows per quarter-warp on distinct bank groups) x n(n-1)/2 "
