@@ -9,6 +9,7 @@ reference's recorded 50k whole run.  The product side goes through the public AP
 the same way (oracle/scale.py csr_hashes: members/offsets sha + a block hash of the
 neighbors).  Reference: conflict.py:89-167, driver.py:272-385.
 """
+import hashlib
 import json
 import os
 import time
@@ -18,7 +19,7 @@ import pytest
 
 import paper_2401_06713_b200 as b200
 from conftest import GOLDEN
-from oracle.scale import csr_hashes, sha16
+from oracle.scale import BLOCK_ROWS, csr_hashes, sha16
 
 pytestmark = pytest.mark.gpu
 
@@ -91,3 +92,54 @@ def test_whole_run_identical_coloring_full_size(scale_gold, name):
     assert len(res.iterations) == want["iterations"]
     assert res.oracle_edges == want["oracle_edges"]
     assert res.peak_conflict_edges == want["peak_conflict_edges"]
+
+
+def test_c4_iteration1_csr_full_hash(scale_gold):
+    """Config 4 (4M x 128 qubits, two-word bit planes): the whole iteration-1 CSR (7.2e9 edges)
+    against the scale oracle's hashes, without the 115 GB int64 array on the host at once.
+    The build is counted once over all rows (every degree, K1 over the whole triangle); the
+    neighbor ids then come out through the row-range ABI (pcg_count / pcg_fill_rows) in
+    chunks of whole 4096-row hash blocks, each hashed as the oracle hashes it."""
+    if "c4" not in scale_gold["builds"]:
+        pytest.skip("no c4 golden (tools/make_golden_scale.py --builds c4)")
+    from paper_2401_06713_b200 import _native
+    from paper_2401_06713_b200.conflict import stage
+
+    want = scale_gold["builds"]["c4"]
+    view = _view("c4")
+    assert sha16(view.backing.words.view(np.int64)) == want["words_sha"]
+    n = view.n_active
+    plan = b200.plan_iteration(1, n, b200.PaletteParams(12.5, 2.0, seed=0))
+    lists = b200.assign_random_lists(plan, view.active, 0)
+    assert sha16(lists.array) == want["lists_sha"]
+    ctx = _native.context()
+    t = time.perf_counter()
+    stage(view, lists, ctx)
+    c = ctx.count(0, 1, 0, n)
+    print(f"c4: prep + count {time.perf_counter() - t:.2f} s", flush=True)
+    assert int(c.deg_sum) // 2 == want["edge_count"]
+    assert int(c.pairs_in_shard - c.anticommuting) == want["view_edges_scanned"]
+    deg, _ = ctx.degrees(n)
+    has = deg > 0
+    assert int(has.sum()) == want["n_members"]
+    offsets = np.zeros(n + 1, dtype=np.int64) if has.all() else None
+    assert offsets is not None, "c4 iteration 1 has a row without conflicts: compaction"
+    np.cumsum(deg.astype(np.int64), out=offsets[1:])
+    assert sha16(view.active[has]) == want["members_sha"]
+    assert sha16(offsets) == want["offsets_sha"]
+    digests = []
+    chunk = 64 * BLOCK_ROWS
+    for r0 in range(0, n, chunk):
+        r1 = min(n, r0 + chunk)
+        ctx.count(0, 1 << 22, r0, r1)  # this row range (and a negligible K1 shard)
+        lo, hi = ctx.fill_rows(deg, None)
+        assert (lo, hi) == (int(offsets[r0]), int(offsets[r1]))
+        buf = np.empty(hi - lo, dtype=np.int64)
+        ctx.fill_rows(deg, buf)
+        for b0 in range(r0, r1, BLOCK_ROWS):
+            b1 = min(b0 + BLOCK_ROWS, r1)
+            digests.append(hashlib.sha256(buf[offsets[b0] - lo:offsets[b1] - lo].data).digest())
+        del buf
+    got = hashlib.sha256(b"".join(digests)).hexdigest()[:16]
+    print(f"c4: full CSR hashed in {time.perf_counter() - t:.1f} s", flush=True)
+    assert got == want["neighbors_bsha"]
