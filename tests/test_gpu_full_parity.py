@@ -127,19 +127,48 @@ def test_c4_iteration1_csr_full_hash(scale_gold):
     np.cumsum(deg.astype(np.int64), out=offsets[1:])
     assert sha16(view.active[has]) == want["members_sha"]
     assert sha16(offsets) == want["offsets_sha"]
+    from concurrent.futures import ThreadPoolExecutor
+
     digests = []
     chunk = 64 * BLOCK_ROWS
-    for r0 in range(0, n, chunk):
-        r1 = min(n, r0 + chunk)
-        ctx.count(0, 1 << 22, r0, r1)  # this row range (and a negligible K1 shard)
-        lo, hi = ctx.fill_rows(deg, None)
-        assert (lo, hi) == (int(offsets[r0]), int(offsets[r1]))
-        buf = np.empty(hi - lo, dtype=np.int64)
-        ctx.fill_rows(deg, buf)
-        for b0 in range(r0, r1, BLOCK_ROWS):
-            b1 = min(b0 + BLOCK_ROWS, r1)
-            digests.append(hashlib.sha256(buf[offsets[b0] - lo:offsets[b1] - lo].data).digest())
-        del buf
+    with ThreadPoolExecutor(os.cpu_count() or 1) as ex:
+        for r0 in range(0, n, chunk):
+            r1 = min(n, r0 + chunk)
+            ctx.count(0, 1 << 22, r0, r1)  # this row range (and a negligible K1 shard)
+            lo, hi = ctx.fill_rows(deg, None)
+            assert (lo, hi) == (int(offsets[r0]), int(offsets[r1]))
+            buf = np.empty(hi - lo, dtype=np.int64)
+            ctx.fill_rows(deg, buf)
+            blocks = [(b0, min(b0 + BLOCK_ROWS, r1)) for b0 in range(r0, r1, BLOCK_ROWS)]
+            digests += list(ex.map(
+                lambda b: hashlib.sha256(buf[offsets[b[0]] - lo:offsets[b[1]] - lo].data).digest(),
+                blocks))
+            del buf
     got = hashlib.sha256(b"".join(digests)).hexdigest()[:16]
     print(f"c4: full CSR hashed in {time.perf_counter() - t:.1f} s", flush=True)
     assert got == want["neighbors_bsha"]
+
+
+C5 = {"c5_p20_a0.5": (20.0, 0.5), "c5_p5_a2": (5.0, 2.0), "c5_p2.5_a3": (2.5, 3.0)}
+
+
+@pytest.mark.parametrize("name", sorted(C5))
+def test_config5_grid_cell_full_hash(scale_gold, name):
+    """Config 5 (500k x 64q, palette/alpha sweep): whole iteration-1 CSRs of grid cells from
+    sparse (P' = 20%, alpha = 0.5: 7-color lists) to dense (P' = 2.5%, alpha = 3: 39-color
+    lists, ~1.5k members per bucket) against the scale oracle."""
+    if name not in scale_gold["builds"]:
+        pytest.skip(f"no golden for {name}")
+    want = scale_gold["builds"][name]
+    pct, alpha = C5[name]
+    view = b200.pauli_view(b200.PauliSet.from_strings(b200.random_pauli_strings(500_000, 64, seed=0)))
+    plan = b200.plan_iteration(1, view.n_active, b200.PaletteParams(pct, alpha, seed=0))
+    lists = b200.assign_random_lists(plan, view.active, 0)
+    assert sha16(lists.array) == want["lists_sha"]
+    t = time.perf_counter()
+    gc = b200.build(view, lists)
+    print(f"{name}: build {time.perf_counter() - t:.3f} s, |E_c|={gc.edge_count}")
+    got = _hashes(gc)
+    for k in ("members_sha", "offsets_sha", "neighbors_bsha", "n_members", "edge_count",
+              "view_edges_scanned"):
+        assert got[k] == want[k], (k, got[k], want[k])

@@ -35,6 +35,10 @@ CONFIGS = {  # name: (n, q, gen_seed, palette_pct, alpha, seed)
     "c3": (1_000_000, 64, 0, 12.5, 2.0, 0),
     "c4": (4_000_000, 128, 0, 12.5, 2.0, 0),
     "q32_n50000": (50_000, 32, 0, 12.5, 2.0, 0),
+    # config 5 grid cells (500k x 64q, palette P' and alpha varied)
+    "c5_p20_a0.5": (500_000, 64, 0, 20.0, 0.5, 0),
+    "c5_p5_a2": (500_000, 64, 0, 5.0, 2.0, 0),
+    "c5_p2.5_a3": (500_000, 64, 0, 2.5, 3.0, 0),
 }
 
 
