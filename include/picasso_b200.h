@@ -170,13 +170,23 @@ int pcg_assign_lists(pcg_ctx *ctx, const int64_t *active, int64_t n, uint64_t ba
 int pcg_color_dynamic(int64_t nm, const int64_t *offsets, const int64_t *neighbors,
                       const int64_t *list_data, const int64_t *list_off, uint64_t *rng6,
                       int64_t *color_of, int64_t *removal_ops);
-/* Same coloring (same draws, same result) with each step's neighbor scan split across
- * `threads` host threads (0: up to 16) for rows of at least `par_min_deg` entries (-1: 512);
- * the hits are applied in row order by the calling thread.  pcg_color_dynamic = (0, -1). */
+/* Same coloring (same draws, same result).  par_min_deg >= -1 (default -1): each step walks
+ * the picked color's bucket (members listing it, ascending) and tests adjacency by galloping
+ * through the CSR row; par_min_deg < -1: the neighbor-row scan split across `threads` host
+ * threads (0: up to 16) for rows of at least -par_min_deg-2 entries, hits applied in row order
+ * (also taken when the colors do not suit buckets).  pcg_color_dynamic = (0, -1). */
 int pcg_color_dynamic_mt(int64_t nm, const int64_t *offsets, const int64_t *neighbors,
                          const int64_t *list_data, const int64_t *list_off, uint64_t *rng6,
                          int64_t *color_of, int64_t *removal_ops, int32_t threads,
                          int64_t par_min_deg);
+/* Same coloring for the conflict graph of a Pauli view, without the CSR: words = the members'
+ * packed 3-bit code words (nm x nwords, PauliSet.words[members], pauli.py:217); two members of
+ * one color bucket are conflict neighbors iff their strings commute (graph.py:327-336).
+ * Returns 1, having drawn nothing, when the colors do not suit the bucket form (color range
+ * above 2^28, or a list naming a color twice): use pcg_color_dynamic_mt then. */
+int pcg_color_dynamic_words(int64_t nm, const uint64_t *words, int32_t nwords,
+                            const int64_t *list_data, const int64_t *list_off, uint64_t *rng6,
+                            int64_t *color_of, int64_t *removal_ops);
 
 /*
  * Exhaustive properness check of a coloring (validation.py:41-131, exhaustive mode; the

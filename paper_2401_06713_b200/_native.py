@@ -99,6 +99,8 @@ def library():
         lib.pcg_color_dynamic_mt.argtypes = [ctypes.c_int64, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                              _I32, _I64]
         lib.pcg_color_dynamic_mt.restype = ctypes.c_int
+        lib.pcg_color_dynamic_words.argtypes = [ctypes.c_int64, _VP, _I32, _VP, _VP, _VP, _VP, _VP]
+        lib.pcg_color_dynamic_words.restype = ctypes.c_int
         lib.pcg_validate.argtypes = [_VP, _VP, _I64, _I32, _I32, _VP, _I64, _VP, _I32, _VP,
                                      ctypes.POINTER(_I64), ctypes.POINTER(_I64)]
         lib.pcg_validate.restype = ctypes.c_int
@@ -135,7 +137,7 @@ EXPORTED = (
     "pcg_degrees_device", "pcg_fill_rows_device", "pcg_prep_device", "pcg_color_dynamic",
     "pcg_assign_lists", "pcg_validate", "pcg_host_register", "pcg_last_copy_bytes",
     "pcg_k1_result", "pcg_color_dynamic_mt", "pcg_launch_total", "pcg_exchange_buffer",
-    "pcg_exchange_map", "pcg_ids_to_host",
+    "pcg_exchange_map", "pcg_ids_to_host", "pcg_color_dynamic_words",
 )
 
 

@@ -276,11 +276,11 @@ def run_sharded(view, params, *, strategy: str = "dynamic", edge_budget: Optiona
         return build_sharded(v, lists, engine=engine, gather="root", root=root,
                              exchange=exchange, **kw)
 
-    def coloring(gc, lists, strategy, seed, iteration):
+    def coloring(gc, lists, strategy, seed, iteration, view=None):
         box = [None]
         if rank == root:
             o = list_coloring.color_conflict_graph(gc, lists, strategy=strategy, seed=seed,
-                                                   iteration=iteration)
+                                                   iteration=iteration, view=view)
             ids = np.fromiter(o.colored.keys(), dtype=np.int64, count=len(o.colored))
             cols = np.fromiter(o.colored.values(), dtype=np.int64, count=len(o.colored))
             box[0] = (ids, cols, o.uncolored, o.colors_used, o.empties, o.removal_ops)

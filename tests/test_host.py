@@ -145,20 +145,23 @@ def test_native_list_coloring_matches_python(seed):
         gc = oracle_builder(v, lists)
         r1 = np.random.default_rng(np.random.SeedSequence([seed, 1, 0xC01]))
         r2 = np.random.default_rng(np.random.SeedSequence([seed, 1, 0xC01]))
-        a = lc.color_dynamic(gc, lists, r1)
+        r3 = np.random.default_rng(np.random.SeedSequence([seed, 1, 0xC01]))
+        a = lc.color_dynamic(gc, lists, r1)  # color buckets, CSR-row adjacency
         b = lc.color_dynamic_py(gc, lists, r2)
-        assert a.colored == b.colored
-        assert np.array_equal(a.uncolored, b.uncolored)
-        assert a.removal_ops == b.removal_ops
-        assert r1.bit_generator.state == r2.bit_generator.state
+        w = lc.color_dynamic(gc, lists, r3, view=v)  # color buckets, word-predicate adjacency
+        for o in (a, w):
+            assert o.colored == b.colored
+            assert np.array_equal(o.uncolored, b.uncolored)
+            assert o.removal_ops == b.removal_ops
+        assert r1.bit_generator.state == r2.bit_generator.state == r3.bit_generator.state
         assert r1.integers(1 << 30) == r2.integers(1 << 30)
 
 
 @pytest.mark.parametrize("threads,par_min", [(4, 1), (3, 16), (16, 64)])
 def test_native_list_coloring_threaded_scan(threads, par_min):
-    """The threaded neighbor scan (pcg_color_dynamic_mt) gives the sequential scan's coloring,
-    removal count and generator state, on graphs whose rows are far above the threshold, and
-    the sequential scan matches the Python restatement."""
+    """The threaded neighbor scan (pcg_color_dynamic_mt, par_min_deg < -1) gives the color-bucket
+    coloring's result (CSR-row and word adjacency), removal count and generator state, on
+    graphs whose rows are far above the threshold, and both match the Python restatement."""
     from paper_2401_06713_b200 import list_coloring as lc
 
     for n, q, pct, alpha, seed in ((3000, 16, 12.5, 2.0, 0), (2500, 12, 4.0, 3.0, 9)):
@@ -169,14 +172,14 @@ def test_native_list_coloring_threaded_scan(threads, par_min):
         assert np.diff(gc.graph.offsets).max() > 4 * par_min
         out = []
         try:
-            for thr, pm in ((1, -1), (threads, par_min)):
+            for thr, pm, view in ((1, -1, None), (threads, -par_min - 2, None), (1, -1, v)):
                 lc.NATIVE_THREADS, lc.NATIVE_PAR_MIN_DEG = thr, pm
                 r = np.random.default_rng(np.random.SeedSequence([seed, 1, 0xC01]))
-                o = lc.color_dynamic(gc, lists, r)
+                o = lc.color_dynamic(gc, lists, r, view=view)
                 out.append((o.colored, list(o.uncolored), o.removal_ops, r.bit_generator.state))
         finally:
             lc.NATIVE_THREADS, lc.NATIVE_PAR_MIN_DEG = 0, -1
-        assert out[0] == out[1]
+        assert out[0] == out[1] == out[2]
         if n <= 2500:
             r = np.random.default_rng(np.random.SeedSequence([seed, 1, 0xC01]))
             p = lc.color_dynamic_py(gc, lists, r)
