@@ -318,6 +318,7 @@ int color_dynamic_buckets(int64_t nm, Adjacent &&adjacent, const int64_t *list_d
     int64_t left = nm, removals = 0;
     int32_t lowest = 0;
     std::vector<uint8_t> hit;     // batch tests of one bucket walk
+    std::vector<int32_t> live;    // its live entries
     std::vector<int32_t> hits;    // positions of the hits in the walked bucket
     auto finish = [&](int32_t k) {  // processed: none of its remaining colors is live
         for (int64_t x = list_off[k]; x < list_off[k] + ms[k].len; ++x) alive[ent[x]] = 0;
@@ -372,16 +373,25 @@ int color_dynamic_buckets(int64_t nm, Adjacent &&adjacent, const int64_t *list_d
             // every live entry's test first, without branches (its loads overlap), then the
             // hits in order; an apply never changes another entry of the same bucket
             const int64_t b0 = bstart[rc], nb = bstart[rc + 1] - b0;
-            if ((int64_t)hit.size() < nb) hit.resize(nb);
+            if ((int64_t)hit.size() < nb) {
+                hit.resize(nb);
+                live.resize(nb);
+            }
             const uint64_t a1 = trace ? __rdtsc() : 0;
-            constexpr int PF = 16;
+            // the live entries (branch-free compaction), then their tests
+            int32_t nl = 0;
             for (int64_t q = 0; q < nb; ++q) {
-                if (q + PF < nb) adjacent.prefetch(bmem[b0 + q + PF]);
-                hit[q] = alive[b0 + q] & (uint8_t)adjacent.test(bmem[b0 + q]);
+                live[nl] = (int32_t)q;
+                nl += alive[b0 + q];
+            }
+            constexpr int PF = 16;
+            for (int32_t i = 0; i < nl; ++i) {
+                if (i + PF < nl) adjacent.prefetch(bmem[b0 + live[i + PF]]);
+                hit[i] = (uint8_t)adjacent.test(bmem[b0 + live[i]]);
             }
             hits.clear();
-            for (int64_t q = 0; q < nb; ++q)
-                if (hit[q]) hits.push_back((int32_t)q);
+            for (int32_t i = 0; i < nl; ++i)
+                if (hit[i]) hits.push_back(live[i]);
             const uint64_t a2 = trace ? __rdtsc() : 0;
             // the applies' scattered state is requested a few hits ahead: the member and its
             // list (distance 8), then its slot in its size bucket (distance 4)
@@ -405,7 +415,7 @@ int color_dynamic_buckets(int64_t nm, Adjacent &&adjacent, const int64_t *list_d
                 tc[0] += a1 - a0;
                 tc[1] += a2 - a1;
                 tc[2] += a3 - a2;
-                scanned += nb;
+                scanned += nl;
             }
         } else {
             for (int64_t p = bstart[rc]; p < bstart[rc + 1]; ++p) {
@@ -419,7 +429,7 @@ int color_dynamic_buckets(int64_t nm, Adjacent &&adjacent, const int64_t *list_d
     *removal_ops = removals;
     if (trace)
         fprintf(stderr, "color buckets: pick+finish %.3g, tests %.3g, applies %.3g Gcycles; "
-                "%lld entries tested, %lld removals\n", tc[0] * 1e-9, tc[1] * 1e-9, tc[2] * 1e-9,
+                "%lld live entries tested, %lld removals\n", tc[0] * 1e-9, tc[1] * 1e-9, tc[2] * 1e-9,
                 (long long)scanned, (long long)removals);
     return 0;
 }
