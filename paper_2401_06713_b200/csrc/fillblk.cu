@@ -47,6 +47,16 @@ __device__ __forceinline__ void blk_red_or_if(bool p, uint32_t addr, uint32_t v)
                  "r"(v), "r"((uint32_t)p)
                  : "memory");
 }
+__device__ __forceinline__ void blk_sts_if(bool p, uint32_t addr, uint32_t v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}" ::"r"(addr),
+                 "r"(v), "r"((uint32_t)p)
+                 : "memory");
+}
+__device__ __forceinline__ void blk_red_add_if(bool p, uint32_t addr, uint32_t v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q red.shared.add.u32 [%0], %1;\n\t}" ::"r"(addr),
+                 "r"(v), "r"((uint32_t)p)
+                 : "memory");
+}
 __device__ __forceinline__ uint32_t blk_lds_if(bool p, uint32_t addr) {
     uint32_t v = 0u;
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.shared.u32 %0, [%1];\n\t}"
@@ -444,6 +454,8 @@ __global__ void __launch_bounds__(1024) k_fill_bins(RowArgs a, BinArgs g) {
     const int sh = g.shift;
     const int per = (g.nbins + NT - 1) / NT;  // bins per thread in the scan
     const uint64_t pol_keep = l2_policy_keep(), pol_out = l2_policy_stream(), pol_masks = pol_out;
+    const uint32_t list_s = (uint32_t)__cvta_generic_to_shared(list);
+    const uint32_t bins_s = (uint32_t)__cvta_generic_to_shared(bins);
     __syncthreads();
 
     __shared__ long long witem;
@@ -500,12 +512,12 @@ __global__ void __launch_bounds__(1024) k_fill_bins(RowArgs a, BinArgs g) {
                                  : "memory");
                 }
                 off = __shfl_sync(0xffffffffu, off, 0);
+                // predicated stores and reductions: no divergent branch per descriptor
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    if ((mw[u] >> lane) & 1u) {
-                        list[off + __popc(mw[u] & lt)] = x[u];
-                        atomicAdd(&bins[x[u] >> sh], 1);
-                    }
+                    const bool p = (mw[u] >> lane) & 1u;
+                    blk_sts_if(p, list_s + 4u * (uint32_t)(off + __popc(mw[u] & lt)), (uint32_t)x[u]);
+                    blk_red_add_if(p, bins_s + 4u * ((uint32_t)x[u] >> sh), 1u);
                     off += __popc(mw[u]);
                 }
             }
