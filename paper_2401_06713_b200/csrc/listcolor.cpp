@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <type_traits>
 #include <atomic>
+#include <new>
+#include <sys/mman.h>
 #include <cstdio>
 #include <cstdlib>
 #include <climits>
@@ -64,6 +66,44 @@ struct Pcg64 {
         }
         return (uint32_t)(m >> 32);
     }
+};
+
+// A flat array on 2 MB pages (madvise: the box's THP mode).  The coloring's arrays are
+// 0.1-0.3 GB each at config 3 and are read at random: on 4 KB pages most of those reads also
+// miss the TLB.
+template <typename T>
+struct HBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    explicit HBuf(size_t count) : n(count) {
+        const size_t H = (size_t)2 << 20;
+        const size_t bytes = ((std::max<size_t>(count * sizeof(T), 1) + H - 1) / H) * H;
+        p = static_cast<T *>(std::aligned_alloc(H, bytes));
+        if (!p) throw std::bad_alloc();
+        madvise(p, bytes, MADV_HUGEPAGE);
+    }
+    HBuf(size_t count, T v) : HBuf(count) { std::fill(p, p + n, v); }
+    ~HBuf() { std::free(p); }
+    HBuf(const HBuf &) = delete;
+    HBuf &operator=(const HBuf &) = delete;
+    T &operator[](size_t i) { return p[i]; }
+    const T &operator[](size_t i) const { return p[i]; }
+    T *data() { return p; }
+    size_t size() const { return n; }
+};
+
+// One size bucket of the dynamic scheme's queue, a slice of one big array on huge pages
+// (a bucket never holds more than nm members); the std::vector operations the queue uses.
+struct FlatBucket {
+    int32_t *p = nullptr;
+    int32_t n = 0;
+    bool empty() const { return n == 0; }
+    size_t size() const { return (size_t)n; }
+    int32_t &operator[](size_t i) { return p[i]; }
+    int32_t back() const { return p[n - 1]; }
+    void pop_back() { --n; }
+    void push_back(int32_t v) { p[n++] = v; }
+    int32_t *data() { return p; }
 };
 
 }  // namespace
@@ -279,10 +319,10 @@ int color_dynamic_buckets(int64_t nm, Adjacent &&adjacent, const int64_t *list_d
     for (int64_t x = 0; x < tot; ++x) ++bstart[list_data[x] - cmin + 1];
     for (int64_t r = 0; r < R; ++r) bstart[r + 1] += bstart[r];
     if (tot >= ((int64_t)1 << 31)) return 1;
-    std::vector<int32_t> bmem(tot);
-    std::vector<int32_t> ent(tot);      // list position -> its bucket entry
-    std::vector<int32_t> eslot(tot);    // bucket entry -> its current list position
-    std::vector<uint8_t> alive(tot, 1);
+    HBuf<int32_t> bmem(tot);
+    HBuf<int32_t> ent(tot);      // list position -> its bucket entry
+    HBuf<int32_t> eslot(tot);    // bucket entry -> its current list position
+    HBuf<uint8_t> alive(tot, 1);
     {
         std::vector<int64_t> fillp(bstart.begin(), bstart.end() - 1);
         for (int64_t k = 0; k < nm; ++k)
@@ -295,22 +335,24 @@ int color_dynamic_buckets(int64_t nm, Adjacent &&adjacent, const int64_t *list_d
                 eslot[p] = (int32_t)(x - list_off[k]);
             }
     }
-    std::vector<C> cols(tot);
+    HBuf<C> cols(tot);
     for (int64_t x = 0; x < tot; ++x) cols[x] = (C)list_data[x];
     // per member: remaining list length (= its size bucket while unprocessed) and its slot in
     // that bucket, side by side (one cache line per touched member)
     struct Mem {
         int32_t len, slot;
     };
-    std::vector<Mem> ms(nm);
+    HBuf<Mem> ms(nm);
     int32_t top = 0;
     for (int64_t k = 0; k < nm; ++k) {
         ms[k].len = (int32_t)(list_off[k + 1] - list_off[k]);
         top = std::max(top, ms[k].len);
     }
-    std::vector<std::vector<int32_t>> buckets(top + 1);
+    HBuf<int32_t> qdata((size_t)(top + 1) * (size_t)nm);
+    std::vector<FlatBucket> buckets(top + 1);
+    for (int32_t b = 0; b <= top; ++b) buckets[b].p = qdata.data() + (size_t)b * (size_t)nm;
     for (int64_t k = 0; k < nm; ++k) {
-        std::vector<int32_t> &bk = buckets[ms[k].len];
+        FlatBucket &bk = buckets[ms[k].len];
         ms[k].slot = (int32_t)bk.size();
         bk.push_back((int32_t)k);
     }
@@ -325,7 +367,7 @@ int color_dynamic_buckets(int64_t nm, Adjacent &&adjacent, const int64_t *list_d
         --left;
     };
     auto unlink = [&](int32_t k) {  // out of its size bucket (swap-with-last, as the reference)
-        std::vector<int32_t> &bk = buckets[ms[k].len];
+        FlatBucket &bk = buckets[ms[k].len];
         const int32_t s = ms[k].slot;
         const int32_t tail = bk.back();
         bk[s] = tail;
@@ -347,7 +389,7 @@ int color_dynamic_buckets(int64_t nm, Adjacent &&adjacent, const int64_t *list_d
             --left;  // (no live entries left)
             return;
         }
-        std::vector<int32_t> &nbk = buckets[b];
+        FlatBucket &nbk = buckets[b];
         ms[u].slot = (int32_t)nbk.size();
         nbk.push_back(u);
         if (b < lowest) lowest = b;
@@ -359,7 +401,7 @@ int color_dynamic_buckets(int64_t nm, Adjacent &&adjacent, const int64_t *list_d
     while (left) {
         const uint64_t a0 = trace ? __rdtsc() : 0;
         while (buckets[lowest].empty()) ++lowest;
-        std::vector<int32_t> &bk = buckets[lowest];
+        FlatBucket &bk = buckets[lowest];
         const int32_t v = bk[g.below(bk.size())];
         unlink(v);
         finish(v);
