@@ -135,7 +135,11 @@ int pcg_kernel_times(pcg_ctx *ctx, float *ms, int32_t n);
  * the same CSR; the defaults are the measured fastest.
  *   K1 (commuting pairs):  "k1_algo" 1 direct LOP3/POPC tiles, 5 four-Russians 8-bit slices
  *                          (default for q <= 128); "fr_ichunk" rows per work item; "k1_async"
- *                          1 runs K1 on a side stream (pcg_k1_result collects it)
+ *                          1 runs K1 on a side stream (pcg_k1_result collects it); "k1_early"
+ *                          with k1_async: 1 from the input prep (beside the owned masks), 0
+ *                          from the count pass, 2 (default) prep from 256K rows; "k1_warps"
+ *                          CTA size (0: 8 warps beside other kernels, else 16); "dyn_work" 1
+ *                          (default) owned masks and bins fill take items from atomic counters
  *   K2 (conflict rows):    "k2_mode" 1 partner gather, 2 bucket masks, 3 owned masks;
  *                          "own_algo" 0 four-Russians / 1 per-pair masks; "own_direct" 0 forces
  *                          the hash ownership table; "window" row-pass bitmap (ids)

@@ -358,7 +358,11 @@ static int run_k1(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t *pairs, 
 // pass of the same build (one shard) takes it over instead of launching K1 again.
 static int k1_launch_early(pcg_ctx *ctx, cudaStream_t s) {
     ctx->k1_early_valid = false;
-    if (!ctx->k1_async || !ctx->k1_early || ctx->n < 2) return PCG_OK;
+    // auto (k1_early 2, the default): early from 256K rows, where K1 outlasts the owned
+    // masks (measured: config 3 58.7 vs ~60.5 ms); below, K1 from the count pass overlaps the
+    // fill's start instead (config 2: 1.99 vs 2.07 ms)
+    const bool early = ctx->k1_early == 1 || (ctx->k1_early == 2 && ctx->n >= 262144);
+    if (!ctx->k1_async || !early || ctx->n < 2) return PCG_OK;
     if (!ctx->k1_stream) PCG_TRY_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->k1_stream, cudaStreamNonBlocking));
     if (!ctx->k1_fork) PCG_TRY_CUDA(ctx, cudaEventCreateWithFlags(&ctx->k1_fork, cudaEventDisableTiming));
     if (!ctx->k1_done) PCG_TRY_CUDA(ctx, cudaEventCreateWithFlags(&ctx->k1_done, cudaEventDisableTiming));

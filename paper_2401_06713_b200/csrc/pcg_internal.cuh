@@ -363,7 +363,7 @@ struct pcg_ctx {
     int64_t launch_total = 0;     // kernels launched by this context (pcg_launch_total)
     int rows_out32 = 0;           // pcg_fill_rows_device writes int32 ids (sharded exchange)
     int rows_out_abs = 0;         // ... at the rows' global CSR offsets (peer exchange buffer)
-    int k1_early = 1;             // with k1_async: launch K1 from the prep (k1_launch_early)
+    int k1_early = 2;  // K1 from the input prep (1), from the count pass (0), auto (2)
     bool k1_early_valid = false;  // an early K1 of the staged build is in flight (scal[7])
     int k1_slot = 0;              // scal word pcg_k1_result reads (0, or 7 for the early K1)
     int bins_threads = 0;  // bins fill: threads per CTA (0 = auto)

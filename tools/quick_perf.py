@@ -31,7 +31,7 @@ ap.add_argument("--bins-threads", type=int, default=0)
 ap.add_argument("--bins-shift", type=int, default=0)
 ap.add_argument("--bins-maxdeg", type=int, default=0)
 ap.add_argument("--async", dest="k1_async", type=int, default=0)
-ap.add_argument("--early", type=int, default=1)
+ap.add_argument("--early", type=int, default=2)
 ap.add_argument("--check", action="store_true", help="compare the CSR with the default fill")
 ap.add_argument("--pct", type=float, default=12.5)
 ap.add_argument("--ichunk", type=int, default=0)
