@@ -17,8 +17,7 @@ import numpy as np
 from .errors import DeviceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# (PICASSO_LIB: an alternative build of the same library, for A/B experiments)
-LIB_PATH = os.environ.get("PICASSO_LIB") or os.path.join(_HERE, "libpicasso_b200.so")
+LIB_PATH = os.path.join(_HERE, "libpicasso_b200.so")
 
 PCG_OK, PCG_E_ARG, PCG_E_CUDA, PCG_E_OOM, PCG_E_COLOR, PCG_E_STATE, PCG_E_DUPLICATE = range(7)
 
