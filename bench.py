@@ -491,7 +491,7 @@ def bench_gpu(args) -> None:
         line["secondary"] = {"config": config_for(args.secondary), "value": s["value"],
                              "unit": "pairs/s", "ms_per_step": s["ms_per_step"],
                              "e2e": {k: s["e2e"][k] for k in ("value", "unit", "ms_per_step",
-                                                            "h2d_bytes_per_step",
+                                                            "step_ms", "h2d_bytes_per_step",
                                                             "d2h_bytes_per_step")},
                              "kernel_ms": s["kernel_ms"], "roofline": s["roofline"],
                              "roofline_other": s["roofline_other"], "gpu_launches": s["launches"]}
