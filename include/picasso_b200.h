@@ -187,7 +187,8 @@ int pcg_color_dynamic_mt(int64_t nm, const int64_t *offsets, const int64_t *neig
  * packed 3-bit code words (nm x nwords, PauliSet.words[members], pauli.py:217); two members of
  * one color bucket are conflict neighbors iff their strings commute (graph.py:327-336).
  * Returns 1, having drawn nothing, when the colors do not suit the bucket form (color range
- * above 2^28, or a list naming a color twice): use pcg_color_dynamic_mt then. */
+ * above 2^28, or a list naming a color twice): use pcg_color_dynamic_mt then.  Both return -2
+ * when host memory runs out (no exception crosses the ABI). */
 int pcg_color_dynamic_words(int64_t nm, const uint64_t *words, int32_t nwords,
                             const int64_t *list_data, const int64_t *list_off, uint64_t *rng6,
                             int64_t *color_of, int64_t *removal_ops);

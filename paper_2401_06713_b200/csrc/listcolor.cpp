@@ -576,7 +576,7 @@ extern "C" {
 int pcg_color_dynamic_mt(int64_t nm, const int64_t *offsets, const int64_t *neighbors,
                          const int64_t *list_data, const int64_t *list_off, uint64_t *rng6,
                          int64_t *color_of, int64_t *removal_ops, int32_t threads,
-                         int64_t par_min_deg) {
+                         int64_t par_min_deg) try {
     Pcg64 g = load_rng(rng6);
     *removal_ops = 0;
     if (nm == 0) return 0;
@@ -600,6 +600,8 @@ int pcg_color_dynamic_mt(int64_t nm, const int64_t *offsets, const int64_t *neig
     if (rc) return rc;
     store_rng(g, rng6);  // numpy's Generator continues from here
     return 0;
+} catch (const std::bad_alloc &) {
+    return -2;  // out of host memory (nothing escapes the C ABI)
 }
 
 /*
@@ -610,7 +612,7 @@ int pcg_color_dynamic_mt(int64_t nm, const int64_t *offsets, const int64_t *neig
  */
 int pcg_color_dynamic_words(int64_t nm, const uint64_t *words, int32_t nwords,
                             const int64_t *list_data, const int64_t *list_off, uint64_t *rng6,
-                            int64_t *color_of, int64_t *removal_ops) {
+                            int64_t *color_of, int64_t *removal_ops) try {
     Pcg64 g = load_rng(rng6);
     *removal_ops = 0;
     if (nm == 0) return 0;
@@ -627,6 +629,8 @@ int pcg_color_dynamic_words(int64_t nm, const uint64_t *words, int32_t nwords,
     if (rc) return rc;
     store_rng(g, rng6);
     return 0;
+} catch (const std::bad_alloc &) {
+    return -2;
 }
 
 }  // extern "C"
