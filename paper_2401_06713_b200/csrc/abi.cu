@@ -241,6 +241,8 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "rows_out_abs")) ctx->rows_out_abs = (int)value;
     else if (!strcmp(key, "dyn_work")) ctx->dyn_work = (int)value;
     else if (!strcmp(key, "k1_warps")) ctx->k1_warps = (int)value;
+    else if (!strcmp(key, "k1_shard")) ctx->k1_shard = (int)value;
+    else if (!strcmp(key, "k1_nshards")) ctx->k1_nshards = (int)std::max<int64_t>(1, value);
     else if (!strcmp(key, "seg_warps")) ctx->seg_warps = (int)value;
     else return fail(ctx, PCG_E_ARG, std::string("unknown option ") + key);
     return PCG_OK;
@@ -374,8 +376,9 @@ static int k1_launch_early(pcg_ctx *ctx, cudaStream_t s) {
     if (ctx->prof) cudaEventRecord(ctx->ev[0], ks);
     int64_t pairs = 0;
     int l = 0;
-    int rc = run_k1(ctx, 0, 1, &pairs, &l, ks, anti);
+    int rc = run_k1(ctx, ctx->k1_shard, ctx->k1_nshards, &pairs, &l, ks, anti);
     if (rc) return rc;  // (counted in prep_launches)
+    ctx->k1_early_pairs = pairs;
     if (ctx->prof) cudaEventRecord(ctx->ev[1], ks);
     PCG_TRY_CUDA(ctx, cudaEventRecord(ctx->k1_done, ks));
     ctx->k1_pending = true;
@@ -840,7 +843,8 @@ static int count_impl(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t r0, 
     cudaStream_t s = ctx->stream;
     // an early K1 of this build (launched by the prep, own counter) is taken over by a
     // one-shard count; any other pending K1 is joined first
-    const bool take_early = ctx->k1_early_valid && ctx->k1_async && nshards == 1;
+    const bool take_early = ctx->k1_early_valid && ctx->k1_async && shard == ctx->k1_shard &&
+                            nshards == ctx->k1_nshards;
     if (!take_early) {
         k1_join(ctx);
         if (ctx->k1_early_valid) {  // a sharded count: the early sweep is not used
@@ -869,7 +873,7 @@ static int count_impl(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t r0, 
     int rc;
     // K1 only produces view_edges_scanned: with k1_async it runs on a side stream next to the
     // conflict-row passes and its count is collected later (pcg_k1_result)
-    const bool async = ctx->k1_async && nshards == 1;
+    const bool async = ctx->k1_async != 0;
     cudaStream_t ks = s;
     if (async && !take_early) {
         if (!ctx->k1_stream) PCG_TRY_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->k1_stream, cudaStreamNonBlocking));
@@ -880,7 +884,7 @@ static int count_impl(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t r0, 
         PCG_TRY_CUDA(ctx, cudaStreamWaitEvent(ks, ctx->k1_fork, 0));
     }
     if (take_early) {
-        pairs = ctx->n * (ctx->n - 1) / 2;  // the whole triangle, already being swept
+        pairs = ctx->k1_early_pairs;  // this shard's pairs, already being swept
         ctx->k1_slot = 7;
     } else {
         if (ctx->prof) cudaEventRecord(ctx->ev[0], ks);

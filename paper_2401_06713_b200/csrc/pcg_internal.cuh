@@ -333,6 +333,8 @@ struct pcg_ctx {
     pcg::DevBuf workctr;  // atomic work counters of the dynamically scheduled kernels
     int dyn_work = 1;     // K2a and the bins fill take their items from an atomic counter
     int k1_warps = 0;     // K1 CTA size: 0 auto (8 warps next to the row passes, else 16)
+    int k1_shard = 0, k1_nshards = 1;  // the K1 shard an early launch sweeps (sharded build)
+    int64_t k1_early_pairs = 0;        // pairs of that shard
     cudaIpcMemHandle_t xhandle{};
     void *xhandle_of = nullptr;  // the allocation xhandle was taken from
     std::vector<std::pair<std::string, void *>> xmaps;  // handle bytes -> mapped pointer

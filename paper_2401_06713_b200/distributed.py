@@ -315,9 +315,15 @@ def bench_sharded(args) -> None:
     ctx = _native.context(local)
     ranges = row_ranges(n, world)
     r0, r1 = ranges[rank]
-    # the prep computes the owned-mask rows of this rank's row range only
+    # the prep computes the owned-mask rows of this rank's row range only, and launches this
+    # rank's K1 shard on a side stream once the buckets are sorted (beside the owned masks,
+    # the count and the fill; joined at the end of the step)
     ctx.option("own_rows_lo", r0)
     ctx.option("own_rows_hi", r1)
+    ctx.option("k1_async", 1)
+    ctx.option("k1_early", 1)
+    ctx.option("k1_shard", rank)
+    ctx.option("k1_nshards", world)
     stage(view, lists, ctx)
     width = max(b - a for a, b in ranges)
     ctx.option("rows_out32", 1)  # the timed step exchanges int32 slices
@@ -332,6 +338,7 @@ def bench_sharded(args) -> None:
         ctx.option("rows_out_abs", 1)
         ctx.prep_device()
         ctx.count(rank, world, r0, r1)
+        ctx.k1_result()
         ctx.degrees_device(deg_local.data_ptr())
         dist.all_gather_into_tensor(gdeg_parts, deg_local)
         total_ids = int(gdeg_parts.to(torch.int64).sum().item())
@@ -350,6 +357,7 @@ def bench_sharded(args) -> None:
         mx = int(gdeg.max().item()) if n else 0
         if exchange == "p2p":  # the rows go straight into the root's HBM
             ctx.fill_rows_device(gdeg.data_ptr(), mx, xbase[0])
+            ctx.k1_result()  # this rank's K1 shard has finished too
             dist.barrier()
             return c
         lo, hi = ctx.fill_rows_device(gdeg.data_ptr(), mx, None)
@@ -362,6 +370,7 @@ def bench_sharded(args) -> None:
         # the slices gathered to the root rank's HBM, in rank order (the canonical CSR)
         parts = [torch.empty_like(buf) for _ in range(world)] if rank == 0 else None
         dist.gather(buf, parts, dst=0)
+        ctx.k1_result()
         return c
 
     for _ in range(args.warmup):
@@ -388,6 +397,8 @@ def bench_sharded(args) -> None:
 
     ctx.option("rows_out32", 0)
     ctx.option("rows_out_abs", 0)
+    for k, v in (("k1_async", 0), ("k1_early", 2), ("k1_shard", 0), ("k1_nshards", 1)):
+        ctx.option(k, v)
     ctx.option("own_rows_lo", 0)
     ctx.option("own_rows_hi", -1)
     # ---- end to end through the public sharded build (host inputs in, the canonical int64

@@ -578,3 +578,36 @@ def test_duplicate_colors_in_a_row(ragged):
     assert np.array_equal(gc.graph.offsets, want.graph.offsets)
     assert np.array_equal(gc.graph.neighbors, want.graph.neighbors)
     assert gc.view_edges_scanned == want.view_edges_scanned
+
+
+def test_early_k1_shards_sum_to_the_whole_sweep(golden_ref):
+    """The early K1 launch of a sharded build (options k1_async/k1_early/k1_shard/k1_nshards:
+    the rank's shard swept beside the owned masks) is taken over by the count of the same
+    shard; the shards' pairs and anticommuting counts add up to the one-shard sweep."""
+    from paper_2401_06713_b200.conflict import stage
+
+    g = golden_ref["builds_hashed"]["q32_n20000"]
+    v = pauli_view(20000, 32, 0)
+    lists = random_lists(v, seed=0)
+    ctx = _native.context()
+    n = v.n_active
+    want = None
+    try:
+        stage(v, lists, ctx)
+        c = ctx.count(0, 1, 0, n)
+        want = (int(c.pairs_in_shard), int(c.anticommuting))
+        for world in (2, 3):
+            pairs = anti = 0
+            for rank in range(world):
+                for k, val in (("k1_async", 1), ("k1_early", 1), ("k1_shard", rank),
+                               ("k1_nshards", world)):
+                    ctx.option(k, val)
+                stage(v, lists, ctx)
+                c = ctx.count(rank, world, 0, n)
+                pairs += int(c.pairs_in_shard)
+                anti += ctx.k1_result()
+            assert (pairs, anti) == want, (world, pairs, anti, want)
+        assert want[0] - want[1] == g["view_edges_scanned"]
+    finally:
+        for k, val in (("k1_async", 0), ("k1_early", 2), ("k1_shard", 0), ("k1_nshards", 1)):
+            ctx.option(k, val)
