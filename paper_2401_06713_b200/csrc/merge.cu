@@ -280,8 +280,28 @@ __global__ void __launch_bounds__(OWN_THREADS, (KW <= 4 ? 4 : 3)) k_owned_fr(Buc
             uint32_t naddr[NIB];
             {
                 uint32_t av[KW];
+                if (k < m) {  // the row's bits in 16-byte loads (one request per row)
+                    const uint32_t *ar = b.A + (int64_t)sid[k] * KW;
+                    if constexpr (KW % 4 == 0) {
 #pragma unroll
-                for (int q = 0; q < KW; ++q) av[q] = k < m ? __ldg(b.A + (int64_t)sid[k] * KW + q) : 0u;
+                        for (int q = 0; q < KW; q += 4) {
+                            const uint4 t4 = __ldg(reinterpret_cast<const uint4 *>(ar + q));
+                            av[q] = t4.x; av[q + 1] = t4.y; av[q + 2] = t4.z; av[q + 3] = t4.w;
+                        }
+                    } else if constexpr (KW % 2 == 0) {
+#pragma unroll
+                        for (int q = 0; q < KW; q += 2) {
+                            const uint2 t2 = __ldg(reinterpret_cast<const uint2 *>(ar + q));
+                            av[q] = t2.x; av[q + 1] = t2.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < KW; ++q) av[q] = __ldg(ar + q);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < KW; ++q) av[q] = 0u;
+                }
 #pragma unroll
                 for (int g = 0; g < NIB; ++g)
                     naddr[g] = T_s + (uint32_t)(g * 16 + ((av[g >> 3] >> (4 * (g & 7))) & 15u)) * 4u;
