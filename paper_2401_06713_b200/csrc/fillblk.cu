@@ -428,8 +428,11 @@ __device__ __forceinline__ void bins_sort_out(const int32_t *src, int k, OutT *d
         if (t < k) stg_pol(dst + t, COMPACT ? __ldg(compact + v[t]) : v[t], pol);
 }
 
+// 56 registers: six 192-thread CTAs per SM at config 3 (57 would leave five; the shared
+// memory also allows six) — the fill is latency-bound and barrier-heavy, more resident rows
+// hide both (measured 19.5 -> 17.8 ms at config 3)
 template <typename OutT, bool COMPACT>
-__global__ void __launch_bounds__(1024) k_fill_bins(RowArgs a, BinArgs g) {
+__global__ void __maxnreg__(56) k_fill_bins(RowArgs a, BinArgs g) {
     extern __shared__ __align__(16) uint32_t sm[];
     const int NT = blockDim.x, NW = NT >> 5;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
