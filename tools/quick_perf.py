@@ -27,6 +27,7 @@ ap.add_argument("--own-direct", type=int, default=1)
 ap.add_argument("--blk-threads", type=int, default=0)
 ap.add_argument("--blk-groups", type=int, default=0)
 ap.add_argument("--blk-ecap", type=int, default=0)
+ap.add_argument("--blk-dcap", type=int, default=0)
 ap.add_argument("--bins-threads", type=int, default=0)
 ap.add_argument("--bins-shift", type=int, default=0)
 ap.add_argument("--bins-maxdeg", type=int, default=0)
@@ -57,6 +58,7 @@ ctx.option("own_direct", a.own_direct)
 ctx.option("blk_threads", a.blk_threads)
 ctx.option("blk_groups", a.blk_groups)
 ctx.option("blk_ecap", a.blk_ecap)
+ctx.option("blk_dcap", a.blk_dcap)
 ctx.option("bins_threads", a.bins_threads)
 ctx.option("bins_shift", a.bins_shift)
 ctx.option("bins_maxdeg", a.bins_maxdeg)
