@@ -482,6 +482,16 @@ def bench_gpu(args) -> None:
                                               res.total_colors == gold["colors"])
         except (OSError, KeyError, ValueError):
             run["identical_to_golden"] = None
+        # the same run without materializing each iteration's CSR on the host (counts-only
+        # builds + the word-predicate list coloring: driver.run(conflict_rows=False))
+        t0 = time.perf_counter()
+        res2 = b200.run(view, b200.PaletteParams(*WORKLOADS[args.workload][3:6]), conflict_rows=False)
+        import hashlib
+
+        run["counts_only"] = {
+            "seconds": time.perf_counter() - t0, "colors": res2.total_colors,
+            "identical_to_full_run": bool(np.array_equal(res2.color, res.color)),
+            "color_sha": hashlib.sha256(np.ascontiguousarray(res2.color, dtype=np.int64).data).hexdigest()[:16]}
         line["run"] = run
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(view, lists, seconds=args.cpu_seconds)

@@ -37,7 +37,8 @@ from . import _native, hostpool
 from .errors import DeviceError, EdgeBudgetExceededError
 from .graph import ExplicitGraph, pair_chunks
 
-__all__ = ["ConflictGraph", "lists_intersect", "build", "build_reference", "BuildStats"]
+__all__ = ["ConflictGraph", "lists_intersect", "build", "build_counts", "build_reference",
+           "BuildStats"]
 
 
 @dataclass
@@ -224,6 +225,45 @@ def _build(view, lists, edge_budget, block_pairs, two_phase, budget_error):
         offsets[0] = 0
     return CG(members=members, graph=EG(n=nm, offsets=offsets, neighbors=neighbors),
               edge_count=total, view_edges_scanned=scanned)
+
+
+def build_counts(view, lists, *, edge_budget: Optional[int] = None, threads: int = 1,
+                 block_pairs: int = 1 << 20, two_phase: bool = True):
+    """The build's counts without its rows: members, CSR offsets, edge_count and
+    view_edges_scanned of ``build`` (same kernels up to the count pass: K0, K1, owned masks,
+    K2c), with ``graph.neighbors`` left empty (not materialized).
+
+    For consumers that need only the conflict vertices — the list coloring with the Pauli
+    view tests adjacency inside color buckets on the words (list_coloring.color_dynamic) —
+    so that a run at config 4 does not move a 115 GB CSR per iteration.  Same errors as
+    ``build``.
+    """
+    budget_error, device_error = _error_types(view)
+    CG, EG = _result_types(view)
+    try:
+        ctx = _native.context()
+        n = view.n_active
+        ctx.option("k1_async", 0)
+        stage(view, lists, ctx)
+        c = ctx.count(0, 1, 0, n)
+        total = int(c.deg_sum) // 2
+        if edge_budget is not None and total > edge_budget:
+            if two_phase:
+                raise budget_error(total, edge_budget)
+            _, degu = ctx.degrees(n)
+            raise budget_error(one_phase_projection(degu, block_pairs, edge_budget), edge_budget)
+        deg, _ = ctx.degrees(n)
+    except DeviceError as e:
+        if isinstance(e, device_error):
+            raise
+        raise device_error(*e.args) from e
+    has = deg > 0
+    members = np.ascontiguousarray(np.asarray(view.active, dtype=np.int64)[has])
+    offsets = np.zeros(members.size + 1, dtype=np.int64)
+    np.cumsum(deg[has].astype(np.int64), out=offsets[1:])
+    return CG(members=members, graph=EG(n=int(members.size), offsets=offsets,
+                                        neighbors=np.zeros(0, dtype=np.int64)),
+              edge_count=total, view_edges_scanned=int(c.pairs_in_shard - c.anticommuting))
 
 
 def build_reference(view, lists):

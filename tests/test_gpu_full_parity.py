@@ -172,3 +172,41 @@ def test_config5_grid_cell_full_hash(scale_gold, name):
     for k in ("members_sha", "offsets_sha", "neighbors_bsha", "n_members", "edge_count",
               "view_edges_scanned"):
         assert got[k] == want[k], (k, got[k], want[k])
+
+
+def _check_run(res, want):
+    assert sha16(res.color) == want["color_sha"]
+    assert sha16(res.colored_at) == want["colored_at_sha"]
+    assert res.total_colors == want["colors"]
+    assert len(res.iterations) == want["iterations"]
+    assert res.oracle_edges == want["oracle_edges"]
+    assert res.peak_conflict_edges == want["peak_conflict_edges"]
+    for r, w in zip(res.iterations, want["records"]):
+        for k in ("n_active", "palette_size", "list_size", "conflict_vertices", "conflict_edges",
+                  "colored_in_conflict", "uncolored"):
+            assert getattr(r, k) == w[k], (r.iteration, k)
+
+
+def test_whole_run_counts_only_c3_matches_the_csr_run(scale_gold):
+    """driver.run(conflict_rows=False): counts-only builds (no CSR on the host) and the
+    word-predicate list coloring give the c3 run of the golden (oracle CSR builds + CSR-row
+    coloring), iteration by iteration."""
+    want = scale_gold["runs"]["c3"]
+    t = time.perf_counter()
+    res = b200.run(_view("c3"), b200.PaletteParams(12.5, 2.0, seed=0), conflict_rows=False)
+    print(f"c3 counts-only whole run {time.perf_counter() - t:.1f} s, {res.total_colors} colors")
+    _check_run(res, want)
+
+
+def test_whole_run_counts_only_c4(scale_gold):
+    """Config 4 (4M x 128q, multiple Picasso iterations) as a whole run: counts-only GPU
+    builds + the word-predicate coloring against the oracle's counts-only run
+    (tools/make_golden_scale.py --runs-counts c4)."""
+    want = scale_gold.get("runs_counts", {}).get("c4")
+    if want is None:
+        pytest.skip("no c4 counts-only run golden")
+    t = time.perf_counter()
+    res = b200.run(_view("c4"), b200.PaletteParams(12.5, 2.0, seed=0), conflict_rows=False)
+    print(f"c4 counts-only whole run {time.perf_counter() - t:.1f} s, {res.total_colors} colors, "
+          f"{len(res.iterations)} iterations")
+    _check_run(res, want)

@@ -246,3 +246,32 @@ def test_build_reference_and_lists_intersect_match_goldens(golden_cases):
         case.check(build_reference(case.view, case.lists))
         done += 1
     assert done >= 5
+
+
+def test_counts_only_run_needs_pauli_view_and_defaults():
+    """driver.run(conflict_rows=False) is the default builder + coloring on a Pauli view only."""
+    v = pauli_view(50, 6, 1)
+    params = b200.PaletteParams(12.5, 2.0, seed=0)
+    with pytest.raises(b200.errors.BadParamsError):
+        b200.run(v, params, conflict_rows=False, builder=oracle_builder)
+    with pytest.raises(b200.errors.BadParamsError):
+        b200.run(v, params, conflict_rows=False, conflict_coloring=lambda *a, **k: None)
+
+
+def test_coloring_refuses_missing_rows_without_the_view():
+    """A counts-only conflict graph (rows not materialized) colors only with the Pauli view."""
+    from paper_2401_06713_b200 import list_coloring as lc
+    from paper_2401_06713_b200.conflict import ConflictGraph
+    from paper_2401_06713_b200.graph import ExplicitGraph
+
+    v = pauli_view(300, 6, 2)
+    plan = b200.plan_iteration(1, 300, b200.PaletteParams(12.5, 2.0, 0))
+    lists = b200.assign_random_lists(plan, v.active, 0)
+    gc = oracle_builder(v, lists)
+    bare = ConflictGraph(gc.members, ExplicitGraph(gc.graph.n, gc.graph.offsets, np.zeros(0, np.int64)),
+                         gc.edge_count, gc.view_edges_scanned)
+    with pytest.raises(ValueError):
+        lc.color_conflict_graph(bare, lists)
+    a = lc.color_conflict_graph(gc, lists)
+    b = lc.color_conflict_graph(bare, lists, view=v)
+    assert a.colored == b.colored and np.array_equal(a.uncolored, b.uncolored)

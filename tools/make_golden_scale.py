@@ -106,11 +106,67 @@ def golden_run(name):
     return out
 
 
+def golden_run_counts(name):
+    """A whole run whose builds are the oracle's counts only (members, offsets, edge counts:
+    bucket_oracle.c degrees) and whose coloring is the word-predicate list coloring — the
+    form of driver.run(conflict_rows=False), for configs whose per-iteration CSR does not fit
+    this host (config 4: 115 GB at iteration 1).  Iteration 1's view_edges_scanned is taken
+    from the config's build golden when present (its commute count alone is ~1.5 h here)."""
+    from paper_2401_06713_b200 import list_coloring
+    from paper_2401_06713_b200.conflict import ConflictGraph
+    from paper_2401_06713_b200.graph import ExplicitGraph
+
+    view, params = inputs(name)
+    known = json.load(open(OUT))["builds"].get(name, {}) if os.path.exists(OUT) else {}
+    trace = []
+
+    def counts_builder(v, lists, **kw):
+        t = time.time()
+        o = ScaleOracle(v.backing.words, v.active, lists)
+        deg, _ = o.degrees()
+        has = deg > 0
+        members = np.asarray(v.active, dtype=np.int64)[has]
+        offsets = np.zeros(members.size + 1, dtype=np.int64)
+        np.cumsum(deg[has], out=offsets[1:])
+        first = not trace
+        if first and known.get("lists_sha") == sha16(lists.array):
+            scanned = int(known["view_edges_scanned"])
+        else:
+            scanned = o.commute_count()
+        o.close()
+        h = dict(n_active=int(v.n_active), active_sha=sha16(v.active), lists_sha=sha16(lists.array),
+                 members_sha=sha16(members), offsets_sha=sha16(offsets), n_members=int(members.size),
+                 edge_count=int(deg.sum()) // 2, view_edges_scanned=scanned)
+        trace.append(h)
+        print(f"  counts n={v.n_active} |E_c|={h['edge_count']} {time.time() - t:.1f}s", flush=True)
+        return ConflictGraph(members, ExplicitGraph(int(members.size), offsets, np.zeros(0, np.int64)),
+                             h["edge_count"], scanned)
+
+    t = time.time()
+    # (the driver hands each iteration's view to the coloring: word-predicate adjacency)
+    res = b200.run(view, params, builder=counts_builder,
+                   conflict_coloring=list_coloring.color_conflict_graph)
+    out = dict(n=view.n_active, q=CONFIGS[name][1], colors=int(res.total_colors),
+               iterations=len(res.iterations), oracle_edges=int(res.oracle_edges),
+               peak_conflict_edges=int(res.peak_conflict_edges), color_sha=sha16(res.color),
+               colored_at_sha=sha16(res.colored_at), builds=trace,
+               records=[dict(n_active=r.n_active, palette_size=r.palette_size,
+                             list_size=r.list_size, conflict_vertices=r.conflict_vertices,
+                             conflict_edges=r.conflict_edges,
+                             colored_in_conflict=r.colored_in_conflict, uncolored=r.uncolored)
+                        for r in res.iterations],
+               counts_only=True, oracle_seconds=round(time.time() - t, 1))
+    print(name, {k: v for k, v in out.items() if k not in ("builds", "records")}, flush=True)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--builds", nargs="*", default=[])
     ap.add_argument("--runs", nargs="*", default=[])
     ap.add_argument("--skip-pin", action="store_true")
+    ap.add_argument("--runs-counts", nargs="*", default=[],
+                    help="whole runs in the counts-only form (driver.run(conflict_rows=False))")
     a = ap.parse_args()
     with open(os.path.join(ROOT, "tests", "golden", "reference.json")) as f:
         rec = json.load(f)["runs_recorded"]["q32_n50000"]
@@ -132,6 +188,13 @@ def main():
             json.dump(gold, f, indent=1)
     for name in a.runs:
         gold["runs"][name] = golden_run(name)
+        with open(OUT, "w") as f:
+            json.dump(gold, f, indent=1)
+    for name in a.runs_counts:
+        r = golden_run_counts(name)
+        with open(OUT) as f:  # (other writers may have added entries meanwhile)
+            gold = json.load(f)
+        gold.setdefault("runs_counts", {})[name] = r
         with open(OUT, "w") as f:
             json.dump(gold, f, indent=1)
     with open(OUT, "w") as f:
