@@ -240,6 +240,7 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "rows_out32")) ctx->rows_out32 = (int)value;
     else if (!strcmp(key, "rows_out_abs")) ctx->rows_out_abs = (int)value;
     else if (!strcmp(key, "dyn_work")) ctx->dyn_work = (int)value;
+    else if (!strcmp(key, "fuse_deg")) ctx->fuse_deg = (int)value;
     else if (!strcmp(key, "k1_warps")) ctx->k1_warps = (int)value;
     else if (!strcmp(key, "k1_shard")) ctx->k1_shard = (int)value;
     else if (!strcmp(key, "k1_nshards")) ctx->k1_nshards = (int)std::max<int64_t>(1, value);
@@ -425,6 +426,7 @@ struct PrepTrace {
 static int prep_device(pcg_ctx *ctx) {
     cudaStream_t s = ctx->stream;
     k1_join(ctx);
+    ctx->deg_fused = false;
     const int64_t n_active = ctx->n, entries = ctx->entries, P = ctx->P;
     if (n_active == 0) return PCG_OK;
     if (ctx->prof) cudaEventRecord(ctx->ev[10], s);
@@ -598,6 +600,17 @@ static int prep_device(pcg_ctx *ctx) {
                 PCG_ALLOC(ctx, ctx->workctr, 64);
                 PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->workctr.p, 0, 8, s));
                 o.work = ctx->workctr.as<unsigned long long>();
+            }
+            // the four-Russians kernel also produces the degrees (no separate K2c pass)
+            const bool fr_kernel = o.fr && (ctx->kw == 2 || ctx->kw == 4 || ctx->kw == 6 || ctx->kw == 8);
+            if (ctx->fuse_deg && fr_kernel) {
+                PCG_ALLOC(ctx, ctx->deg, (size_t)n_active * 4);
+                PCG_ALLOC(ctx, ctx->degu, (size_t)n_active * 4);
+                PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->deg.p, 0, (size_t)n_active * 4, s));
+                PCG_TRY_CUDA(ctx, cudaMemsetAsync(ctx->degu.p, 0, (size_t)n_active * 4, s));
+                o.deg = ctx->deg.as<int32_t>();
+                o.degu = ctx->degu.as<int32_t>();
+                ctx->deg_fused = true;
             }
             launch_owned_masks(b, o, ctx->sms, s);
             PCG_CHECK_LAUNCH(ctx);
@@ -899,8 +912,9 @@ static int count_impl(pcg_ctx *ctx, int32_t shard, int32_t nshards, int64_t r0, 
     }
     if (ctx->prof) cudaEventRecord(ctx->ev[8], s);
     const RowArgs a = row_args(ctx, r0, r1);
-    *launches += ctx->owned ? launch_count_owned(a, ctx->sms, s)
-                            : launch_rows(a, false, false, ctx->sms, s);
+    if (!(ctx->owned && ctx->deg_fused))  // (fused: the prep's owned-mask kernel counted)
+        *launches += ctx->owned ? launch_count_owned(a, ctx->sms, s)
+                                : launch_rows(a, false, false, ctx->sms, s);
     PCG_CHECK_LAUNCH(ctx);
     if (ctx->prof) cudaEventRecord(ctx->ev[2], s);
     if (r1 > r0) {

@@ -498,6 +498,24 @@ __global__ void __launch_bounds__(OWN_THREADS, (KW <= 4 ? 4 : 3)) k_owned_fr(Buc
             }
         }
         __syncthreads();
+        // the rows' degrees (K2c's popcounts, fused: the prep zeroed deg/degu): each mask row
+        // is final once the ownership clears above are done; re-read at L2 (.cg), where the
+        // clears' atomics landed
+        if (o.deg) {
+            for (int k = k_lo + tid; k < k_hi; k += OWN_THREADS) {
+                const uint32_t *row = out + (int64_t)k * W;
+                int cnt = 0, cntu = 0;
+                for (int w = 0; w < W; ++w) {
+                    const uint32_t x = __ldcg(row + w);
+                    cnt += __popc(x);
+                    const int d = k - 32 * w;  // partners t > k are the ids > the row's
+                    const uint32_t up = d < 0 ? 0xffffffffu : (d >= 31 ? 0u : ~((2u << d) - 1u));
+                    cntu += __popc(x & up);
+                }
+                if (cnt) atomicAdd(&o.deg[sid[k]], cnt);
+                if (cntu) atomicAdd(&o.degu[sid[k]], cntu);
+            }
+        }
         // reset the hash table (direct tags carry the color: nothing to reset)
         if (!o.direct) {
             for (int x = 4 * tid; x < HS; x += 4 * OWN_THREADS)

@@ -146,6 +146,8 @@ struct OwnArgs {
     int32_t row_lo, row_hi;  // four-Russians kernel: mask rows only for members in [lo, hi)
                              // (a sharded build's own rows; other rows are left unwritten)
     unsigned long long *work;  // if set (zeroed): colors handed out by an atomic counter
+    int32_t *deg, *degu;       // if set (zeroed): the four-Russians kernel also adds each
+                               // mask row's popcounts (the count pass's degrees)
 };
 
 // Work distribution of the persistent row/color loops.  Static (item += gridDim.x) when
@@ -332,6 +334,8 @@ struct pcg_ctx {
     pcg::DevBuf xbuf;
     pcg::DevBuf workctr;  // atomic work counters of the dynamically scheduled kernels
     int dyn_work = 1;     // K2a and the bins fill take their items from an atomic counter
+    int fuse_deg = 1;     // the owned-mask kernel computes the degrees (no K2c pass)
+    bool deg_fused = false;  // this prep's degrees came from the owned-mask kernel
     int k1_warps = 0;     // K1 CTA size: 0 auto (8 warps next to the row passes, else 16)
     int k1_shard = 0, k1_nshards = 1;  // the K1 shard an early launch sweeps (sharded build)
     int64_t k1_early_pairs = 0;        // pairs of that shard
