@@ -116,6 +116,16 @@ def _worker(rank, world, port, name, budget, two_phase, q, native=False, gather=
 
 def _run(world, name, budget=None, two_phase=True, native=False, gather="root", target=None,
          args=None, exchange="auto"):
+    # rank processes sharing one GPU: a transient CUDA initialisation failure of a freshly
+    # spawned process (seen once on a box: "no usable CUDA device") is retried, not reported
+    for attempt in range(3):
+        out = _run_once(world, name, budget, two_phase, native, gather, target, args, exchange)
+        if not (native and any(r[1] == "error" and "pcg_create" in str(r[2]) for r in out)):
+            return out
+    return out
+
+
+def _run_once(world, name, budget, two_phase, native, gather, target, args, exchange):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
