@@ -357,6 +357,7 @@ def measure_workload(name, args, local, clocks_on: bool):
     # K1 alone (outside the timed region): one build with K1 on the builder's stream, 16 warps,
     # nothing beside it — the kernel's own fraction of its bound, next to the in-step one
     ctx.option("k1_async", 0)
+    ctx.build_device()  # (warm-up: the 16-warp K1's first launch also loads its module)
     l2_flush(flush)
     ctx.build_device()
     k1_alone_ms = float(ctx.kernel_times()[0])
