@@ -141,8 +141,10 @@ int pcg_kernel_times(pcg_ctx *ctx, float *ms, int32_t n);
  *                          CTA size (0: 8 warps beside other kernels, else 16); "dyn_work" 1
  *                          (default) owned masks and bins fill take items from atomic counters
  *   K2 (conflict rows):    "k2_mode" 1 partner gather, 2 bucket masks, 3 owned masks;
- *                          "own_algo" 0 four-Russians / 1 per-pair masks; "own_direct" 0 forces
- *                          the hash ownership table; "window" row-pass bitmap (ids)
+ *                          "own_algo" 0 four-Russians / 1 per-pair masks; "own_direct" 0 turns
+ *                          off the direct-mapped ownership table (small palettes); "own_bitmap"
+ *                          0 turns off the exact color bitmap (then the hash table);
+ *                          "window" row-pass bitmap (ids)
  *   fill:                  "fill_algo" 0 auto, 3 lane bitmap, 5 block (CTA per row),
  *                          6 segmented, 7 bins (counting sort);
  *                          "blk_threads" "blk_groups" "blk_dcap" "blk_ecap"; "bins_threads"

@@ -219,6 +219,7 @@ int pcg_set_option(pcg_ctx *ctx, const char *key, int64_t value) {
     else if (!strcmp(key, "seg_bits")) ctx->seg_bits = (int)value;
     else if (!strcmp(key, "own_algo")) ctx->own_algo = (int)value;
     else if (!strcmp(key, "own_direct")) ctx->own_direct = (int)value;
+    else if (!strcmp(key, "own_bitmap")) ctx->own_bitmap = (int)value;
     else if (!strcmp(key, "d2h_chunk")) ctx->d2h_chunk = (int)value;
     else if (!strcmp(key, "d2h_threads")) ctx->d2h_threads = (int)value;
     else if (!strcmp(key, "d2h_mode")) ctx->d2h_mode = (int)value;
@@ -569,6 +570,12 @@ static int prep_device(pcg_ctx *ctx) {
             o.l16 = P < 65536 ? 1 : 0;
             o.direct = (o.fr && ctx->own_direct != 0 && !ctx->ragged && P <= 28672 &&
                         (int64_t)m_max * std::max(1, ctx->lmax - 1) <= 4 * P) ? 1 : 0;
+            // an exact bitmap over the colors replaces the hash table when it is smaller
+            // (config 3: 15.6 + 6 KB instead of 40 KB), so that two owned-mask CTAs fit next
+            // to K1 on an SM; see owned_bitmap_words
+            o.bm_words = (int32_t)((((int64_t)P + 31) / 32 + 3) & ~3LL);
+            o.bitmap = (o.fr && !o.direct && !ctx->ragged && ctx->own_bitmap != 0 &&
+                        owned_bitmap_words(o) < (int64_t)o.hash_slots + owned_hash_coll()) ? 1 : 0;
             // measured: staging the lists pays when they are u16 (small palettes); u32 lists
             // next to the hash table cost occupancy (config 3)
             o.stage_lists = (!ctx->ragged && o.l16) ? 1 : 0;

@@ -22,6 +22,8 @@ namespace {
 constexpr int OWN_THREADS = 256;
 constexpr int OWN_COLL = 2048;        // collision list capacity
 constexpr int OWN_LCAP = 1024;        // direct ownership: default losers per level (o.lcap)
+constexpr int OWN_BM_FILTER = 512;    // bitmap ownership: 16K-bit filter of the repeated colors
+constexpr int OWN_BM_COLL = 1024;     // bitmap ownership: holders of the repeated colors
 
 template <int KW>
 struct Vec {
@@ -205,8 +207,16 @@ __global__ void __launch_bounds__(OWN_THREADS, (KW <= 4 ? 4 : 3)) k_owned_fr(Buc
     uint32_t *lA = osm + o.dtab_words;                            // direct: losers (c'<<12|k)
     const int lcap = o.lcap > 0 ? o.lcap : OWN_LCAP;
     uint32_t *lB = lA + lcap;
-    int32_t *sid = reinterpret_cast<int32_t *>(osm + (o.direct ? o.dtab_words + 2 * lcap
-                                                               : HS + OWN_COLL));
+    // bitmap mode: bit c' of bm = color c' < c seen in the bucket; filt = a 16K-bit hash
+    // filter of the colors seen twice; coll = their holders (c'<<12 | k), the filter's false
+    // positives included (they pair with nothing: the pairing compares the colors)
+    uint32_t *bm = osm, *filt = osm + o.bm_words;
+    if (o.bitmap) coll = osm + o.bm_words + OWN_BM_FILTER;
+    const int coll_cap = o.bitmap ? OWN_BM_COLL : OWN_COLL;
+    const int state_words = o.bitmap ? o.bm_words + OWN_BM_FILTER : HS;  // zeroed per color
+    int32_t *sid = reinterpret_cast<int32_t *>(
+        osm + (o.direct ? o.dtab_words + 2 * lcap
+                        : o.bitmap ? o.bm_words + OWN_BM_FILTER + OWN_BM_COLL : HS + OWN_COLL));
     constexpr int NB = DB ? 2 : 1;  // table buffers
     uint32_t *T = reinterpret_cast<uint32_t *>(sid + ((o.m_cap + 3) & ~3));  // NB x NIB*16 tables
     uint32_t *BT = T + NB * NIB * 16;                             // NB x 32*KW transposed bits
@@ -226,7 +236,7 @@ __global__ void __launch_bounds__(OWN_THREADS, (KW <= 4 ? 4 : 3)) k_owned_fr(Buc
     if (o.direct) {
         for (int x = tid; x < o.dtab_words; x += OWN_THREADS) osm[x] = 0u;
     } else {
-        for (int x = tid; x < HS; x += OWN_THREADS) osm[x] = 0u;
+        for (int x = tid; x < state_words; x += OWN_THREADS) osm[x] = 0u;
     }
     __shared__ long long witem;
     for (int64_t c = work_first(o.work, &witem); c < b.P; c = work_next(o.work, &witem, c)) {
@@ -442,6 +452,41 @@ __global__ void __launch_bounds__(OWN_THREADS, (KW <= 4 ? 4 : 3)) k_owned_fr(Buc
                 src = dst;
                 dst = t;
             }
+        } else if (o.bitmap) {
+            // pass 1: every (member k, color c' < c) item sets bit c' of bm; an item that finds
+            // the bit set marks c' in the filter.  Pass 2: the items whose color passes the
+            // filter are listed; every pair of holders of one color is cleared below.
+            constexpr int OWN_BATCH = 8;
+            const uint32_t items = (uint32_t)m * (uint32_t)o.L;
+            for (int pass = 0; pass < 2; ++pass) {
+                for (uint32_t e0 = tid; e0 < items; e0 += OWN_BATCH * OWN_THREADS) {
+                    int32_t cx[OWN_BATCH];
+                    int kk[OWN_BATCH];
+#pragma unroll
+                    for (int u = 0; u < OWN_BATCH; ++u) {
+                        const uint32_t e = e0 + (uint32_t)(u * OWN_THREADS);
+                        const int k = (int)__umulhi(e, o.l_magic);
+                        kk[u] = k;
+                        cx[u] = e >= items ? INT_MAX
+                              : !stage_lists ? __ldg(o.lrel + (int64_t)sid[k] * o.L + (e - (uint32_t)k * (uint32_t)o.L))
+                              : o.l16 ? (int32_t)sL16[e] : sL32[e];
+                    }
+#pragma unroll
+                    for (int u = 0; u < OWN_BATCH; ++u) {
+                        if (cx[u] >= c) continue;
+                        const uint32_t h = ((uint32_t)cx[u] * 0x9E3779B1u) >> 18;  // 14 bits
+                        if (pass == 0) {
+                            const uint32_t bit = 1u << (cx[u] & 31);
+                            if (atomicOr(&bm[cx[u] >> 5], bit) & bit) atomicOr(&filt[h >> 5], 1u << (h & 31));
+                        } else if ((filt[h >> 5] >> (h & 31)) & 1u) {
+                            const int q = atomicAdd(&ncoll, 1);
+                            if (q < OWN_BM_COLL) coll[q] = ((uint32_t)cx[u] << 12) | (uint32_t)kk[u];
+                            else overflow = 1;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
         } else if (!o.loff) {
             // the list loads of OWN_BATCH items are issued together (the inserts' atomics
             // would otherwise serialise each load behind the previous item's insert)
@@ -473,13 +518,27 @@ __global__ void __launch_bounds__(OWN_THREADS, (KW <= 4 ? 4 : 3)) k_owned_fr(Buc
             }
         }
         __syncthreads();
-        const int nc = o.direct ? 0 : min(ncoll, OWN_COLL);
+        const int nc = o.direct ? 0 : min(ncoll, coll_cap);
         if (overflow && tid == 0) atomicMax(o.overflow, overflow);
         // every collision entry (a later holder k2 of a color c' < c) pairs with the first
         // holder (the table slot) and with the earlier collision entries of the same slot, so
         // each pair of a group sharing c' is cleared exactly once (groups are almost always
         // pairs: ~(L-1)^2/P of a bucket's pairs share a second color)
-        for (int q = tid; q < nc; q += OWN_THREADS) {
+        if (o.bitmap) {  // every pair of holders of one color, once
+            for (int q = tid; q < nc; q += OWN_THREADS) {
+                const uint32_t cq = coll[q];
+                const int k2 = (int)(cq & 0xfffu);
+                for (int p = 0; p < q; ++p) {
+                    const uint32_t cp = coll[p];
+                    if ((cp >> 12) == (cq >> 12)) {
+                        const int k0 = (int)(cp & 0xfffu);
+                        atomicAnd(&out[(int64_t)k0 * W + (k2 >> 5)], ~(1u << (k2 & 31)));
+                        atomicAnd(&out[(int64_t)k2 * W + (k0 >> 5)], ~(1u << (k0 & 31)));
+                    }
+                }
+            }
+        }
+        for (int q = tid; q < (o.bitmap ? 0 : nc); q += OWN_THREADS) {
             const uint32_t cq = coll[q];
             const uint32_t slot = cq >> 12;
             const int k2 = (int)(cq & 0xfffu);
@@ -516,9 +575,9 @@ __global__ void __launch_bounds__(OWN_THREADS, (KW <= 4 ? 4 : 3)) k_owned_fr(Buc
                 if (cntu) atomicAdd(&o.degu[sid[k]], cntu);
             }
         }
-        // reset the hash table (direct tags carry the color: nothing to reset)
+        // reset the hash table or the bitmaps (direct tags carry the color: nothing to reset)
         if (!o.direct) {
-            for (int x = 4 * tid; x < HS; x += 4 * OWN_THREADS)
+            for (int x = 4 * tid; x < state_words; x += 4 * OWN_THREADS)
                 *reinterpret_cast<uint4 *>(table + x) = make_uint4(0u, 0u, 0u, 0u);
         }
         __syncthreads();
@@ -580,7 +639,8 @@ int run_owned(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s) {
 
 size_t owned_fr_smem(const OwnArgs &o, int kw, bool db = false) {
     const size_t state = o.direct ? (size_t)o.dtab_words + 2 * (size_t)(o.lcap > 0 ? o.lcap : OWN_LCAP)
-                                  : (size_t)o.hash_slots + OWN_COLL;
+                         : o.bitmap ? (size_t)owned_bitmap_words(o)
+                                    : (size_t)o.hash_slots + OWN_COLL;
     const size_t lists = o.stage_lists ? (size_t)o.m_cap * o.L * (o.l16 ? 2 : 4) : 0;
     const size_t nb = db ? 2 : 1;
     return (state + ((o.m_cap + 3) & ~3) + nb * 8 * (size_t)kw * 16 + nb * 32 * (size_t)kw +
@@ -608,6 +668,11 @@ int run_owned_fr(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s)
 }
 
 }  // namespace
+
+// ownership state words of the bitmap mode (bitmap + filter + holders) and of the hash's
+// collision list
+int64_t owned_bitmap_words(const OwnArgs &o) { return (int64_t)o.bm_words + OWN_BM_FILTER + OWN_BM_COLL; }
+int64_t owned_hash_coll() { return OWN_COLL; }
 
 // dynamic shared memory the owned-mask kernel launch_owned_masks picks would request
 size_t owned_masks_smem(const OwnArgs &o, int kw) {

@@ -143,6 +143,8 @@ struct OwnArgs {
     int32_t l16;           // members' lists staged as u16 (palette < 65536)
     int32_t stage_lists;   // stage the members' lists in shared memory (direct mode, or u16)
     int32_t lcap;          // direct mode: losers per level (0: 1024)
+    int32_t bitmap;        // 1: an exact bitmap over the colors instead of the hash table
+    int32_t bm_words;      // its words (>= P/32, multiple of 4)
     int32_t row_lo, row_hi;  // four-Russians kernel: mask rows only for members in [lo, hi)
                              // (a sharded build's own rows; other rows are left unwritten)
     unsigned long long *work;  // if set (zeroed): colors handed out by an atomic counter
@@ -242,6 +244,8 @@ int launch_rows(const RowArgs &a, bool fill, bool out64, int sms, cudaStream_t s
 int launch_bucket_layout(const BucketArgs &b, int64_t entries, cudaStream_t s);
 int launch_bucket_masks(const BucketArgs &b, int sms, cudaStream_t s);
 size_t owned_masks_smem(const OwnArgs &o, int kw);
+int64_t owned_bitmap_words(const OwnArgs &o);
+int64_t owned_hash_coll();
 int launch_owned_masks(const BucketArgs &b, const OwnArgs &o, int sms, cudaStream_t s);
 int launch_count_owned(const RowArgs &a, int sms, cudaStream_t s);
 int launch_assign_lists(const int64_t *active, int64_t n, uint64_t base_key, int64_t P, int L,
@@ -300,6 +304,7 @@ struct pcg_ctx {
     int seg_bits = 0;   // segmented fill: max window bits per warp (0 auto)
     int seg_warps = 0;  // segmented fill: warps per block (0 auto)
     int own_algo = 0;   // owned masks: 0 four-Russians tables (when kw allows), 1 per-pair
+    int own_bitmap = 1;   // ownership: exact color bitmap when smaller than the hash table
     int own_direct = 1; // ownership: 1 direct-mapped color table when P is small, 0 hash
     int k2_mode = 0;    // 0 auto, 1 partner gathers, 2 bucket masks + bitmap dedupe, 3 owned masks
 

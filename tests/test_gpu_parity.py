@@ -37,15 +37,17 @@ def test_every_golden_build(golden_cases, k1_algo, k2_mode):
         case.check(b200.build(case.view, case.lists))
 
 
-@pytest.mark.parametrize("own_algo,own_direct", [(0, 1), (0, 0), (1, 0)],
-                         ids=["own-fourrussians-direct", "own-fourrussians-hash", "own-perpair"])
-def test_owned_mask_kernels(golden_cases, golden_ref, own_algo, own_direct):
-    """The owned-mask kernels (table-driven / per-pair masks; direct-mapped / hashed
-    ownership) give the reference CSR."""
+@pytest.mark.parametrize("own_algo,own_direct,own_bitmap", [(0, 1, 1), (0, 0, 1), (0, 0, 0), (1, 0, 1)],
+                         ids=["own-fourrussians-direct", "own-fourrussians-bitmap",
+                              "own-fourrussians-hash", "own-perpair"])
+def test_owned_mask_kernels(golden_cases, golden_ref, own_algo, own_direct, own_bitmap):
+    """The owned-mask kernels (table-driven / per-pair masks; direct-mapped / bitmap /
+    hashed ownership) give the reference CSR."""
     ctx = _native.context()
     ctx.option("k2_mode", 3)
     ctx.option("own_algo", own_algo)
     ctx.option("own_direct", own_direct)
+    ctx.option("own_bitmap", own_bitmap)
     try:
         for case in golden_cases:
             case.check(b200.build(case.view, case.lists))
@@ -58,6 +60,7 @@ def test_owned_mask_kernels(golden_cases, golden_ref, own_algo, own_direct):
     finally:
         ctx.option("own_algo", 0)
         ctx.option("own_direct", 1)
+        ctx.option("own_bitmap", 1)
         ctx.option("k2_mode", 0)
 
 
@@ -288,7 +291,7 @@ def test_commute_count_both_kernels_vs_oracle(n, q, k1_algo):
 @pytest.mark.parametrize("n,pct", [(40000, 50.0), (60000, 45.0)])
 def test_owned_direct_table_large_palette(n, pct):
     """Palettes between 14336 and 28672 colors take the 16-bit direct ownership table: the CSR
-    must equal the hash-table path's, and sampled rows the oracle's."""
+    must equal the bitmap and hash-table paths', and sampled rows the oracle's."""
     from oracle.oracle import OracleInstance
 
     v = pauli_view(n, 32, 5)
@@ -302,10 +305,15 @@ def test_owned_direct_table_large_palette(n, pct):
         nb, off = a.graph.neighbors.copy(), a.graph.offsets.copy()
         a = None
         ctx.option("own_direct", 0)
-        b = b200.build(v, lists)
+        b = b200.build(v, lists)  # exact color bitmap
+        assert (sha(b.graph.offsets), sha(b.graph.neighbors), b.view_edges_scanned) == want
+        b = None
+        ctx.option("own_bitmap", 0)
+        b = b200.build(v, lists)  # hash table
         assert (sha(b.graph.offsets), sha(b.graph.neighbors), b.view_edges_scanned) == want
     finally:
         ctx.option("own_direct", 1)
+        ctx.option("own_bitmap", 1)
     inst = OracleInstance(v.backing.words, v.active, lists)
     for i in (0, n // 2, n - 1):
         row, _ = inst.row(i)

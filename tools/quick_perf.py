@@ -38,6 +38,7 @@ ap.add_argument("--pct", type=float, default=12.5)
 ap.add_argument("--ichunk", type=int, default=0)
 ap.add_argument("--k1-warps", type=int, default=0)
 ap.add_argument("--dyn", type=int, default=1)
+ap.add_argument("--own-bitmap", type=int, default=1)
 ap.add_argument("--alpha", type=float, default=2.0)
 a = ap.parse_args()
 
@@ -67,6 +68,7 @@ ctx.option("k1_early", a.early)
 ctx.option("fr_ichunk", a.ichunk)
 ctx.option("k1_warps", a.k1_warps)
 ctx.option("dyn_work", a.dyn)
+ctx.option("own_bitmap", a.own_bitmap)
 ctx.profiling(True)
 stage(v, lists, ctx)
 print("prep ms", ctx.kernel_times()[4])
