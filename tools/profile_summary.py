@@ -81,13 +81,15 @@ for f in sorted(os.listdir(src)):
     out.append("")
 with open(prefix + "_ncu_summary.md", "w") as fh:
     fh.write("\n".join(out) + "\n")
-if os.path.exists(os.path.join(src, "launches.csv")):
+for lname in sorted(os.listdir(src)):
+    if not (lname.startswith("launches") and lname.endswith(".csv")):
+        continue
     r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "launch_table.py"),
-                        os.path.join(src, "launches.csv"), "5"], capture_output=True, text=True).stdout
-    with open(prefix + "_launches.txt", "w") as fh:
+                        os.path.join(src, lname), "5"], capture_output=True, text=True).stdout
+    with open(prefix + "_" + lname[:-4] + ".txt", "w") as fh:
         fh.write("ncu --metrics gpu__time_duration.sum --clock-control none, "
                  "bench.py --steps 2 --warmup 3 (5 device builds + 5 public builds)\n" + r)
-for name in ("bench.json", "bench_ref.json"):
+for name in ("bench.json", "bench_ref.json", "bench_sharded1.json"):
     p = os.path.join(src, name)
     if os.path.exists(p):
         lines = [ln for ln in open(p).read().splitlines() if ln.strip().startswith("{")]
