@@ -574,7 +574,14 @@ static int prep_device(pcg_ctx *ctx) {
             // (config 3: 15.6 + 6 KB instead of 40 KB), so that two owned-mask CTAs fit next
             // to K1 on an SM; see owned_bitmap_words
             o.bm_words = (int32_t)((((int64_t)P + 31) / 32 + 3) & ~3LL);
+            // ... and while the holders of repeated colors stay well inside the holder list:
+            // near the top of the palette a color's m·(L-1) items repeat ~(m(L-1))^2 / 2P
+            // colors; past ~1K holders the pairing (quadratic in them) and the overflow
+            // fallback cost more than the hash table (500k ids, P' = 20%, alpha = 4.5: 193 vs
+            // 113 ms; config 3 sits at ~525)
+            const double own_items = (double)m_max * (double)std::max(1, ctx->lmax - 1);
             o.bitmap = (o.fr && !o.direct && !ctx->ragged && ctx->own_bitmap != 0 &&
+                        own_items * own_items <= 1024.0 * (double)P &&
                         owned_bitmap_words(o) < (int64_t)o.hash_slots + owned_hash_coll()) ? 1 : 0;
             // measured: staging the lists pays when they are u16 (small palettes); u32 lists
             // next to the hash table cost occupancy (config 3)

@@ -1,4 +1,5 @@
-"""Config 5 (500k x 64q) palette/list grid on one B200: device build time and |E_c| per cell
+"""Config 5 (500k x 64q) palette/list grid on one B200: device build time, |E_c|, and the
+whole run's colors, iterations and time per cell
 (P' in {1, 2.5, ..., 20}, alpha in {0.5, ..., 4.5}, seed 0).  The densest corner
 (P'=1, alpha=4.5: ~3.2e10 conflict edges, a 253 GB CSR) goes through the public build with an
 edge budget and must raise the reference's EdgeBudgetExceededError before allocating."""
@@ -12,7 +13,7 @@ import torch
 import paper_2401_06713_b200 as b200
 from paper_2401_06713_b200 import _native
 from paper_2401_06713_b200.conflict import stage
-from paper_2401_06713_b200.errors import EdgeBudgetExceededError
+from paper_2401_06713_b200.errors import EdgeBudgetExceededError, IterationLimitError
 
 n, q = 500_000, 64
 t0 = time.time()
@@ -21,8 +22,8 @@ print(f"inputs {time.time() - t0:.1f} s", flush=True)
 ctx = _native.context()
 pairs = n * (n - 1) // 2
 cells = [(12.5, 2.0), (20.0, 0.5), (1.0, 0.5), (20.0, 4.5), (5.0, 2.0), (2.5, 3.0), (10.0, 1.0)]
-print("| P' % | alpha | P | L | |E_c| | device build | pairs/s |")
-print("|---|---|---|---|---|---|---|")
+print("| P' % | alpha | P | L | |E_c| | device build | pairs/s | colors | iterations | whole run |")
+print("|---|---|---|---|---|---|---|---|---|---|")
 for pct, alpha in cells:
     plan = b200.plan_iteration(1, n, b200.PaletteParams(pct, alpha, seed=0))
     lists = b200.assign_random_lists(plan, view.active, 0)
@@ -35,8 +36,19 @@ for pct, alpha in cells:
         torch.cuda.synchronize()
         dt = time.perf_counter() - t
         best = dt if best is None else min(best, dt)
+    # the whole Picasso run of the cell (counts-only builds + word-predicate list coloring:
+    # the same coloring as the CSR run, driver.run(conflict_rows=False)): the colors-vs-time
+    # side of the trade-off
+    del lists
+    t = time.perf_counter()
+    try:
+        res = b200.run(view, b200.PaletteParams(pct, alpha, seed=0), conflict_rows=False)
+        colors, iters = str(res.total_colors), str(len(res.iterations))
+    except IterationLimitError as e:  # the reference's own limit (driver.py), same exception
+        colors, iters = f"IterationLimitError: {e}", "limit"
+    rt = time.perf_counter() - t
     print(f"| {pct} | {alpha} | {plan.palette_size} | {plan.list_size} | {c.deg_sum // 2:.3e} | "
-          f"{best * 1e3:.1f} ms | {pairs / best:.2e} |", flush=True)
+          f"{best * 1e3:.1f} ms | {pairs / best:.2e} | {colors} | {iters} | {rt:.2f} s |", flush=True)
 # densest corner: budget error from the count pass, nothing allocated for the CSR
 plan = b200.plan_iteration(1, n, b200.PaletteParams(1.0, 4.5, seed=0))
 lists = b200.assign_random_lists(plan, view.active, 0)
